@@ -1,0 +1,142 @@
+/* matq.h -- C ABI of libmatq.so, the B200 (sm_100a) sliced weight-only linear.
+ *
+ * This is the drop-in boundary for the reference's native layer.  The
+ * reference binds its C kernels through Cython
+ * (pkg/src/nestquant/kernels/_core.pyx:8-16 -> packed_kernels.h:17-30);
+ * libmatq exports the equivalents below, plain pointers and sizes only.
+ * INTEGRATION.md shows the Cython / ctypes stubs a maintainer adds.
+ *
+ * Conventions
+ *   - Every pointer argument except the host-side query functions is a
+ *     DEVICE pointer (cudaMalloc / torch CUDA tensor storage), caller-owned;
+ *     libmatq never allocates or frees (as the reference C core never does,
+ *     _core.pyx:42-45 allocates on the Python side).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Hot-path calls (mq_gemv, mq_pack_planes, mq_tile_scales,
+ *     mq_slice, mq_dequant, mq_materialize_child) are asynchronous, do no
+ *     host synchronisation and no allocation, and are CUDA-graph capturable.
+ *     The format helpers that validate data (mq_slice_elementwise,
+ *     mq_dequant_f64, mq_pack_ref_layout) synchronise `stream` to report
+ *     MQ_ERR_CODE_RANGE, as the reference validates synchronously.
+ *   - Return value: MQ_OK or an MQ_ERR_* status; mq_last_error() gives a
+ *     thread-local message (replaces the reference's Python-side exception
+ *     texts, matmul.py:106-109, slicing.py:58-64, which the Python layer
+ *     keeps verbatim).
+ *
+ * Device parent layout "P8": planes uint32[8][Np/16][Kp/256][32][4],
+ * plane 0 = code MSB; tiled scales fp32[Np/16][ngp][16]; Np = ceil16(N),
+ * Kp = ceil256(K), ngp = ceil(Kp / G).  A child ("mode C") has the same
+ * layout with r planes holding the sliced r-bit code, MSB first.
+ */
+#ifndef MATQ_H
+#define MATQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MQ_API __attribute__((visibility("default")))
+#else
+#define MQ_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MQ_OK 0
+#define MQ_ERR_INVALID 1    /* bad shape / bit-width / group size / pointer      */
+#define MQ_ERR_CODE_RANGE 2 /* a code exceeds its bit-width                      */
+#define MQ_ERR_WORKSPACE 3  /* workspace missing or smaller than required        */
+#define MQ_ERR_CUDA 4       /* CUDA runtime error (see mq_last_error)            */
+
+/* mq_gemv flags */
+#define MQ_CHILD 1 /* planes are an r-plane child (mode C); else the 8-plane parent (mode P) */
+#define MQ_X_F32 2 /* X is fp32 [B][ldx] (split on device into bf16 hi + lo terms); else bf16 */
+#define MQ_Y_F32 4 /* Y is fp32 [B][ldy]; else bf16 */
+#define MQ_PDL 8   /* programmatic dependent launch (overlap with the previous kernel) */
+
+/* Capability query; replaces nq_simd_kind (packed_kernels.h:29-30,
+ * packed_kernels.c:27).  Returns 100 for the sm_100a build. */
+MQ_API int mq_arch(void);
+MQ_API const char* mq_version(void);
+MQ_API const char* mq_last_error(void);
+
+/* Layout sizes (host-side, no CUDA calls). */
+MQ_API int mq_layout_dims(int N, int K, int G, int* Np, int* Kp, int* ngp);
+MQ_API size_t mq_planes_bytes(int N, int K, int nplanes);
+MQ_API size_t mq_tscales_bytes(int N, int K, int G);
+
+/* K1: codes (N, K) uint8 with `nbits` significant bits (8 for the int8
+ * parent, r for a child) -> MSB-first bit planes in the P8 layout.  Replaces
+ * the reference's child packer pack() (packing.py:81-110) and the raw-byte
+ * parent storage (checkpoint.py:66-75) with one device layout. */
+MQ_API int mq_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits,
+                   uint32_t* planes, void* stream);
+
+/* Group scales (N, ceil(K/G)) fp32 row-major (QuantGrid.scales, grid.py:293)
+ * -> tiled scales. */
+MQ_API int mq_tile_scales(const float* scales, int N, int K, int G, float* tscales, void* stream);
+
+/* K2a: r-bit sliced codes (N, K) uint8 from planes, with the bitsliced
+ * slice the GEMV uses.  Replaces slice_to_code over a layer
+ * (slicing.py:87-90, slice_layer :158-171).  child=1: planes already hold r
+ * planes. */
+MQ_API int mq_slice(const uint32_t* planes, int N, int K, int r, int child, uint8_t* codes_out,
+             long long ldo, void* stream);
+
+/* K2b: decode through the exact GEMV register path.  vals_out (optional):
+ * int8 s - 2^(r-1); w_out (optional): fp32 (s - z) * tscale * out_scale,
+ * i.e. PackedLayer.dense_f32 (matmul.py:232-237) when out_scale = 2^(8-r). */
+MQ_API int mq_dequant(const uint32_t* planes, const float* tscales, int N, int K, int G, int r,
+               int child, float out_scale, int8_t* vals_out, float* w_out, long long ldw,
+               void* stream);
+
+/* K2c: materialise an r-plane child (mode C) from the parent planes. */
+MQ_API int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uint32_t* child,
+                         void* stream);
+
+/* K3: Y = X @ dequant(slice_r(planes)).T, fp32 accumulation.
+ * Replaces _core.packed_matmul (_core.pyx:24-64) -> nq_group_lane_sums /
+ * nq_gemv / nq_gemm (packed_kernels.h:17-27), for r in {2,3,4,6,8} and
+ * 1 <= B <= 32 (B <= 16 with MQ_X_F32).  X (B, K) with row stride ldx,
+ * Y (B, N) with row stride ldy.  out_scale multiplies the tiled scales
+ * (2^(c-r) for a parent slice, exact; 1.0 for a child with effective scales).
+ * G must be a multiple of 32.  `workspace` must hold
+ * mq_gemv_workspace_bytes(N, K, B, flags) bytes, zero-filled once at
+ * allocation; calls leave it zeroed.  One workspace per stream. */
+MQ_API size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags);
+MQ_API int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y,
+            int ldy, int B, int N, int K, int G, int r, float out_scale, int flags,
+            void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- format-layer helpers behind the drop-in Python API --------------- */
+
+/* slice_code / slice_to_code (slicing.py:67-90) over n codes at master
+ * bit-width c; err_dev: one device int of scratch.  Synchronises. */
+MQ_API int mq_slice_elementwise(const uint8_t* q, long long n, int c, int r, int on_master,
+                         uint8_t* out, int* err_dev, void* stream);
+
+/* dequant (grid.py:346-367) in float64.  Synchronises. */
+MQ_API int mq_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int ng, int G, int c,
+                   int r, double* out, int* err_dev, void* stream);
+
+/* dequant_value (grid.py:346-358): out[i] = scale[i] * (2^(c-r) * (q[i] - 2^(r-1)))
+ * with a per-element float64 scale.  Synchronises. */
+MQ_API int mq_dequant_value_f64(const uint8_t* q, const double* scale, long long n, int c, int r,
+                                double* out, int* err_dev, void* stream);
+
+/* matmul_ref (matmul.py:253-260), bit-exact float32 k-ascending. */
+MQ_API int mq_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y, void* stream);
+
+/* The reference's child bit-plane layout (packing.py:81-126).  Synchronises. */
+MQ_API int mq_pack_ref_layout(const uint8_t* codes, int N, int K, int bits, uint64_t* base, uint32_t* b2,
+                       uint32_t* b3, int* err_dev, void* stream);
+MQ_API int mq_unpack_ref_layout(const uint64_t* base, const uint32_t* b2, const uint32_t* b3, int N, int K,
+                         uint8_t* codes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MATQ_H */

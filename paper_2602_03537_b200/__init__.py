@@ -1,0 +1,20 @@
+"""B200-native sliced weight-only linear (MatGPTQ inference hot path).
+
+Drop-in for the hot-path surface of the reference package ``nestquant``
+(/root/reference/pkg/src/nestquant/__init__.py:10-34): slicing, grid
+dequantisation, the child packing format and the packed matmul, plus the
+device-resident parent planes (``PlaneTensor``) and a torch module
+(``MatLinear``).  All compute goes through libmatq.so (sm_100a CUDA behind a
+C ABI, include/matq.h); there is no CPU fallback.
+"""
+
+from . import _lib  # noqa: F401  (fails loudly if libmatq.so is missing)
+from .device import PlaneTensor, algorithmic_bytes, reserve_workspace
+from .grid import BitWidthSet, GridError, QuantGrid, base_scale, dequant, dequant_value
+from .matmul import (MatmulError, MatmulTask, PackedLayer, bench, matmul_packed,
+                     matmul_packed_device, matmul_ref, random_task)
+from .packing import PackedTensor, PackError, pack, pack_slice, to_canonical, to_interleaved, unpack
+from .slicing import (BitConfig, NestedLayer, SlicedLayer, SliceError, slice_code, slice_layer,
+                      slice_model, slice_to_code)
+
+__version__ = "0.1.0"

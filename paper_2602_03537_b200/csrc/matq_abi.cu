@@ -1,0 +1,330 @@
+// matq_abi.cu -- extern "C" entry points of libmatq.so (include/matq.h):
+// argument validation, launch configuration, error reporting.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/matq.h"
+#include "matq_gemv.cuh"
+#include "matq_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return MQ_OK;
+    return fail(MQ_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool valid_r(int r) { return r == 2 || r == 3 || r == 4 || r == 6 || r == 8; }
+
+int sm_count() {
+    static int cached[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = 148;
+        cached[dev] = n;
+    }
+    return cached[dev];
+}
+
+struct GemvConfig {
+    int NT, RT, KW, ITERS, S;
+    size_t smem;
+    int xs_stride;
+};
+
+constexpr size_t kSmemMax = 96 * 1024;
+
+// Decomposition heuristic: one 16-row tile per warp, 8 warps
+// per CTA split RT (row tiles) x KW (K slices); RT grows with the batch so
+// the staged X is reused by more rows.  K is further split across S CTAs
+// until the grid covers ~2 CTAs per SM or a warp is down to 2 steps, and
+// until the staged X fits the shared-memory budget.
+GemvConfig choose_gemv_config(int N, int K, int Bx) {
+    GemvConfig c{};
+    const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
+    c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
+    c.RT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
+    c.KW = 8 / c.RT;
+    const int rows_ctas = mq::cdiv(n_rt, c.RT);
+    const int target = 2 * sm_count();
+    int S = 1;
+    int iters = mq::cdiv(nsteps, c.KW);
+    auto smem_for = [&](int it) {
+        const int kc = c.KW * it * 256;
+        const size_t xs = (size_t)Bx * (kc + 8) * 2;
+        const size_t red = (size_t)c.NT * 4096;
+        return xs > red ? xs : red;
+    };
+    while (true) {
+        iters = mq::cdiv(nsteps, c.KW * S);
+        const bool small_grid = (long long)rows_ctas * S < target && iters > 2;
+        const bool too_big = smem_for(iters) > kSmemMax && iters > 1;
+        if (!small_grid && !too_big) break;
+        ++S;
+    }
+    c.ITERS = iters;
+    c.S = mq::cdiv(nsteps, c.KW * c.ITERS);
+    c.smem = smem_for(c.ITERS);
+    c.xs_stride = c.KW * c.ITERS * 256 + 8;
+    return c;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t gemv_ws_bytes(int N, const GemvConfig& c, int B) {
+    if (c.S <= 1) return 0;
+    const int rows_ctas = mq::cdiv(mq::pad16(N) / 16, c.RT);
+    return align256((size_t)rows_ctas * sizeof(int)) + (size_t)c.S * B * mq::pad16(N) * sizeof(float);
+}
+
+mq::GemvLaunchFn gemv_launcher(int r) {
+    switch (r) {
+        case 2: return mq::launch_gemv_r<2>;
+        case 3: return mq::launch_gemv_r<3>;
+        case 4: return mq::launch_gemv_r<4>;
+        case 6: return mq::launch_gemv_r<6>;
+        case 8: return mq::launch_gemv_r<8>;
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mq_arch(void) { return 100; }
+
+const char* mq_version(void) { return "matq 0.1.0 (sm_100a)"; }
+
+const char* mq_last_error(void) { return g_err; }
+
+int mq_layout_dims(int N, int K, int G, int* Np, int* Kp, int* ngp) {
+    if (N < 1 || K < 1 || G < 1) return fail(MQ_ERR_INVALID, "bad layout dims N=%d K=%d G=%d", N, K, G);
+    if (Np) *Np = mq::pad16(N);
+    if (Kp) *Kp = mq::pad256(K);
+    if (ngp) *ngp = mq::cdiv(mq::pad256(K), G);
+    return MQ_OK;
+}
+
+size_t mq_planes_bytes(int N, int K, int nplanes) {
+    if (N < 1 || K < 1 || nplanes < 1) return 0;
+    return (size_t)nplanes * mq::pad16(N) * (size_t)mq::pad256(K) / 8;
+}
+
+size_t mq_tscales_bytes(int N, int K, int G) {
+    if (N < 1 || K < 1 || G < 1) return 0;
+    return (size_t)mq::pad16(N) * mq::cdiv(mq::pad256(K), G) * sizeof(float);
+}
+
+int mq_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits, uint32_t* planes,
+                   void* stream) {
+    if (!codes || !planes) return fail(MQ_ERR_INVALID, "null pointer");
+    if (N < 1 || K < 1 || ldc < K) return fail(MQ_ERR_INVALID, "bad shape N=%d K=%d ldc=%lld", N, K, ldc);
+    if (nbits < 2 || nbits > 8) return fail(MQ_ERR_INVALID, "nbits must lie in [2, 8]");
+    return cuda_status(mq::launch_pack_planes(codes, ldc, N, K, nbits, planes, (cudaStream_t)stream),
+                       "mq_pack_planes");
+}
+
+int mq_tile_scales(const float* scales, int N, int K, int G, float* tscales, void* stream) {
+    if (!scales || !tscales) return fail(MQ_ERR_INVALID, "null pointer");
+    if (N < 1 || K < 1 || G < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    const int ng = mq::cdiv(K, G), ngp = mq::cdiv(mq::pad256(K), G);
+    return cuda_status(mq::launch_tile_scales(scales, N, ng, ngp, tscales, (cudaStream_t)stream),
+                       "mq_tile_scales");
+}
+
+int mq_slice(const uint32_t* planes, int N, int K, int r, int child, uint8_t* codes_out,
+             long long ldo, void* stream) {
+    if (!planes || !codes_out) return fail(MQ_ERR_INVALID, "null pointer");
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (N < 1 || K < 1 || ldo < K) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_slice_codes(r, child != 0, planes, N, K, codes_out, ldo,
+                                              (cudaStream_t)stream),
+                       "mq_slice");
+}
+
+int mq_dequant(const uint32_t* planes, const float* tscales, int N, int K, int G, int r, int child,
+               float out_scale, int8_t* vals_out, float* w_out, long long ldw, void* stream) {
+    if (!planes || (!vals_out && !w_out)) return fail(MQ_ERR_INVALID, "null pointer");
+    if (w_out && !tscales) return fail(MQ_ERR_INVALID, "w_out needs tscales");
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (N < 1 || K < 1 || ldw < K || G < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_decode_dense(r, child != 0, planes, tscales, G, out_scale, N, K,
+                                               vals_out, w_out, ldw, (cudaStream_t)stream),
+                       "mq_dequant");
+}
+
+int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uint32_t* child,
+                         void* stream) {
+    if (!planes || !child) return fail(MQ_ERR_INVALID, "null pointer");
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (N < 1 || K < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_materialize_child(r, planes, N, K, child, (cudaStream_t)stream),
+                       "mq_materialize_child");
+}
+
+size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
+    if (N < 1 || K < 1 || B < 1) return 0;
+    const int Bx = (flags & MQ_X_F32) ? 2 * B : B;
+    if (Bx > 32) return 0;
+    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx), B);
+}
+
+int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y, int ldy,
+            int B, int N, int K, int G, int r, float out_scale, int flags, void* workspace,
+            size_t workspace_bytes, void* stream) {
+    if (!planes || !tscales || !X || !Y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (G < 32 || G % 32 != 0) return fail(MQ_ERR_INVALID, "group size must be a multiple of 32");
+    if (N < 1 || K < 1 || B < 1) return fail(MQ_ERR_INVALID, "bad shape B=%d N=%d K=%d", B, N, K);
+    if (ldx < K || ldy < N) return fail(MQ_ERR_INVALID, "bad leading dimension");
+    const bool xf32 = flags & MQ_X_F32;
+    const int Bx = xf32 ? 2 * B : B;
+    if (Bx > 32) return fail(MQ_ERR_INVALID, "batch %d above the GEMV limit (32 rows, 16 with fp32 X)", B);
+
+    const GemvConfig c = choose_gemv_config(N, K, Bx);
+    const size_t need = gemv_ws_bytes(N, c, B);
+    if (need > workspace_bytes || (need && !workspace))
+        return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+
+    mq::GemvParams p{};
+    p.planes = planes;
+    p.plane_stride = (long long)(mq::pad16(N) / 16) * (mq::pad256(K) / 256) * 128;
+    p.tscales = tscales;
+    p.X = X;
+    p.Y = Y;
+    const int rows_ctas = mq::cdiv(mq::pad16(N) / 16, c.RT);
+    if (need) {
+        p.tickets = reinterpret_cast<int*>(workspace);
+        p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
+                                        align256((size_t)rows_ctas * sizeof(int)));
+    }
+    p.out_scale = out_scale;
+    p.ldx = ldx;
+    p.ldy = ldy;
+    p.B = B;
+    p.Bx = Bx;
+    p.N = N;
+    p.Np = mq::pad16(N);
+    p.K = K;
+    p.Kp = mq::pad256(K);
+    p.G = G;
+    p.ngp = mq::cdiv(p.Kp, G);
+    p.nsteps = p.Kp / 256;
+    p.RT = c.RT;
+    p.KW = c.KW;
+    p.ITERS = c.ITERS;
+    p.S = c.S;
+    p.x_f32 = xf32 ? 1 : 0;
+    p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
+    p.xs_stride = c.xs_stride;
+    const dim3 grid(rows_ctas, c.S, 1);
+    const int gs = (G == 128) ? 128 : 0;
+    const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, c.smem,
+                                           (cudaStream_t)stream, (flags & MQ_PDL) != 0);
+    return cuda_status(e, "mq_gemv");
+}
+
+static int sync_and_check(cudaError_t launch, int* err_dev, cudaStream_t s, const char* where,
+                          const char* range_msg) {
+    if (launch != cudaSuccess) return cuda_status(launch, where);
+    int h = 0;
+    cudaError_t e = cudaMemcpyAsync(&h, err_dev, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, where);
+    if (h) return fail(MQ_ERR_CODE_RANGE, "%s", range_msg);
+    return MQ_OK;
+}
+
+int mq_slice_elementwise(const uint8_t* q, long long n, int c, int r, int on_master, uint8_t* out,
+                         int* err_dev, void* stream) {
+    if (c < 2 || c > 8) return fail(MQ_ERR_INVALID, "master bit-width must lie in [2, 8]");
+    if (r > c) return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d", r, c);
+    if (r < 2) return fail(MQ_ERR_INVALID, "target bit-width must be >= 2");
+    if (n < 0 || (n > 0 && (!q || !out || !err_dev))) return fail(MQ_ERR_INVALID, "null pointer");
+    if (n == 0) return MQ_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(err_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_slice_elementwise");
+    static char msg[64];
+    snprintf(msg, sizeof(msg), "code out of range for bit-width %d", c);
+    return sync_and_check(mq::launch_slice_elementwise(q, n, c, r, on_master, out, err_dev, s),
+                          err_dev, s, "mq_slice_elementwise", msg);
+}
+
+int mq_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int ng, int G, int c,
+                   int r, double* out, int* err_dev, void* stream) {
+    if (c < 2 || c > 8 || r < 2 || r > c) return fail(MQ_ERR_INVALID, "bad bit-widths c=%d r=%d", c, r);
+    if (N < 1 || K < 1 || G < 1 || ng < mq::cdiv(K, G)) return fail(MQ_ERR_INVALID, "bad shape");
+    if (!codes || !scales || !out || !err_dev) return fail(MQ_ERR_INVALID, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(err_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_dequant_f64");
+    static char msg[64];
+    snprintf(msg, sizeof(msg), "code out of range for bit-width %d", r);
+    return sync_and_check(mq::launch_dequant_f64(codes, N, K, scales, ng, G, c, r, out, err_dev, s),
+                          err_dev, s, "mq_dequant_f64", msg);
+}
+
+int mq_dequant_value_f64(const uint8_t* q, const double* scale, long long n, int c, int r,
+                         double* out, int* err_dev, void* stream) {
+    if (c < 2 || c > 8 || r < 2 || r > c) return fail(MQ_ERR_INVALID, "bad bit-widths c=%d r=%d", c, r);
+    if (n < 0 || (n > 0 && (!q || !scale || !out || !err_dev))) return fail(MQ_ERR_INVALID, "null pointer");
+    if (n == 0) return MQ_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(err_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_dequant_value_f64");
+    static char msg[64];
+    snprintf(msg, sizeof(msg), "code out of range for bit-width %d", r);
+    return sync_and_check(mq::launch_dequant_value_f64(q, scale, n, c, r, out, err_dev, s), err_dev,
+                          s, "mq_dequant_value_f64", msg);
+}
+
+int mq_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y, void* stream) {
+    if (!X || !W || !Y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (B < 1 || K < 1 || N < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_matmul_ref(X, B, K, W, N, Y, (cudaStream_t)stream), "mq_matmul_ref");
+}
+
+int mq_pack_ref_layout(const uint8_t* codes, int N, int K, int bits, uint64_t* base, uint32_t* b2,
+                       uint32_t* b3, int* err_dev, void* stream) {
+    if (bits < 2 || bits > 4) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (!codes || !base || !err_dev || (bits >= 3 && !b2) || (bits == 4 && !b3))
+        return fail(MQ_ERR_INVALID, "null pointer");
+    if (N < 1 || K < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(err_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_pack_ref_layout");
+    static char msg[64];
+    snprintf(msg, sizeof(msg), "code overflow for %d bits", bits);
+    return sync_and_check(
+        mq::launch_pack_ref_layout(codes, N, K, bits, reinterpret_cast<unsigned long long*>(base),
+                                   bits >= 3 ? b2 : nullptr, bits == 4 ? b3 : nullptr, err_dev, s),
+        err_dev, s, "mq_pack_ref_layout", msg);
+}
+
+int mq_unpack_ref_layout(const uint64_t* base, const uint32_t* b2, const uint32_t* b3, int N, int K,
+                         uint8_t* codes, void* stream) {
+    if (!base || !codes) return fail(MQ_ERR_INVALID, "null pointer");
+    if (N < 1 || K < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_unpack_ref_layout(reinterpret_cast<const unsigned long long*>(base),
+                                                    b2, b3, N, K, codes, (cudaStream_t)stream),
+                       "mq_unpack_ref_layout");
+}
+
+}  // extern "C"

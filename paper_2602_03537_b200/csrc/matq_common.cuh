@@ -1,0 +1,300 @@
+// matq_common.cuh -- device building blocks shared by every matq kernel.
+//
+// Device parent layout "P8":
+//   planes : uint32[8][Np/16][Kp/256][32 lanes][4 words]   plane 0 = code MSB
+//   tscales: fp32 [Np/16][ngp][16]                          tiled group scales
+// Np = N rounded up to 16, Kp = K rounded up to 256, ngp = ceil(Kp / G).
+// One uint32 word of one plane holds one bit of 32 weights of a 16-row x
+// 64-column block, arranged so that the word a lane loads is exactly the set
+// of weights that lane holds in the A fragments of four mma.m16n8k16 steps:
+//   lane = 4g + t, bit p in [0,16) and p + 16 of word w of a 256-column step:
+//     s = p >> 2 (k16 step), q = p & 3 (A register a0..a3)
+//     row = 16*rt + g + 8*(q & 1)
+//     col = 256*step + 64*w + 16*s + 8*(q >> 1) + 2*t + (bit >= 16)
+// so a warp's 128-bit load of one plane is 512 contiguous bytes, and every
+// r-slice reads planes 0..r (r+1 planes, all 8 at r = 8) and nothing else.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+
+#define MQ_HD __host__ __device__ __forceinline__
+
+namespace mq {
+
+constexpr int kTileRows = 16;   // rows per warp tile (mma M)
+constexpr int kStepCols = 256;  // columns per 128-bit load per plane
+constexpr int kWordCols = 64;   // columns per lane word
+
+__host__ __device__ constexpr int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+__host__ __device__ constexpr int pad16(int n) { return cdiv(n, 16) * 16; }
+__host__ __device__ constexpr int pad256(int k) { return cdiv(k, 256) * 256; }
+
+// Position of bit `bit` (0..31) of word `w` (0..3) for lane `lane` within a
+// (row tile, step) block: returns (row offset in tile, column offset in step).
+__host__ __device__ __forceinline__ void word_bit_pos(int lane, int w, int bit, int& row, int& col) {
+    const int g = lane >> 2, t = lane & 3;
+    const int p = bit & 15, h = bit >> 4;
+    const int s = p >> 2, q = p & 3;
+    row = g + 8 * (q & 1);
+    col = 64 * w + 16 * s + 8 * (q >> 1) + 2 * t + h;
+}
+
+// ----------------------------------------------------------------------------
+// bf16 constants (exact small dyadic values), computed at compile time.
+__host__ __device__ constexpr uint32_t bf16_bits(int num, int sh) {  // num * 2^-sh
+    if (num == 0) return 0u;
+    uint32_t sgn = num < 0 ? 0x8000u : 0u;
+    int a = num < 0 ? -num : num;
+    int e = 0;
+    while ((a >> e) > 1) ++e;
+    uint32_t m = e <= 7 ? (((uint32_t)a << (7 - e)) & 0x7Fu) : (((uint32_t)a >> (e - 7)) & 0x7Fu);
+    return sgn | ((uint32_t)(e - sh + 127) << 7) | m;
+}
+__host__ __device__ constexpr uint32_t x2(uint32_t h) { return h | (h << 16); }
+static_assert(bf16_bits(128, 0) == 0x4300u, "bf16 128");
+static_assert(bf16_bits(-130, 0) == 0xC302u, "bf16 -130");
+static_assert(bf16_bits(1, 4) == 0x3D80u, "bf16 1/16");
+
+// Host emulation (tests/test_layout_emulation.py): every use below produces an
+// exactly representable small integer, so float arithmetic + truncation to
+// bf16 reproduces the device instruction bit for bit.
+MQ_HD float host_bf16(uint32_t h) {
+    union { uint32_t u; float f; } v;
+    v.u = (h & 0xFFFFu) << 16;
+    return v.f;
+}
+MQ_HD uint32_t host_to_bf16(float f) {
+    union { uint32_t u; float f; } v;
+    v.f = f;
+    return v.u >> 16;
+}
+MQ_HD uint32_t hfma2(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+#else
+    const float lo = host_bf16(a) * host_bf16(b) + host_bf16(c);
+    const float hi = host_bf16(a >> 16) * host_bf16(b >> 16) + host_bf16(c >> 16);
+    return host_to_bf16(lo) | (host_to_bf16(hi) << 16);
+#endif
+}
+MQ_HD uint32_t hsub2(uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+#else
+    const float lo = host_bf16(a) - host_bf16(b);
+    const float hi = host_bf16(a >> 16) - host_bf16(b >> 16);
+    return host_to_bf16(lo) | (host_to_bf16(hi) << 16);
+#endif
+}
+
+// Field of R bits at bit offset O of both 16-bit halves of w -> bf16x2 of
+// (field - 2^(R-1)), exact.  (w & mask) | 0x4300 is bf16 128 + field*2^O; one
+// bf16x2 FMA by 2^-O with addend -(128*2^-O + z) lands on field - z exactly.
+template <int R, int O>
+MQ_HD uint32_t field_bf16(uint32_t w) {
+    static_assert(O + R <= 7, "field must sit inside the bf16 mantissa");
+    constexpr uint32_t m = ((1u << R) - 1u) << O;
+    const uint32_t v = (w & x2(m)) | 0x43004300u;
+    constexpr uint32_t mul = x2(bf16_bits(1, O));
+    constexpr uint32_t add = x2(bf16_bits(-((128 >> O) + (1 << (R - 1))), 0));
+    return hfma2(v, mul, add);
+}
+
+// 8-bit field at offset 0 (bit 7 would land in the bf16 exponent):
+// (low7 | 0x4300) - (bit7 ? 128 : 256) = code - 128, exact.
+MQ_HD uint32_t field8_bf16(uint32_t w) {
+    const uint32_t a = (w & 0x007F007Fu) | 0x43004300u;
+    const uint32_t b = (w & 0x00800080u) ^ 0x43804380u;
+    return hsub2(a, b);
+}
+
+// ----------------------------------------------------------------------------
+// Bitsliced rounding slice (slicing.py:67-84), 32 weights per instruction.
+// T[0..R-1] = top R code bits (T[0] = MSB), T[R] = the rounding bit k-1.
+//   carry = T[R] & ~(T[0] & ... & T[R-1])      (clamp: no carry into all-ones)
+//   S = T + carry  (ripple from the LSB; cannot overflow because of the clamp)
+// This is exactly min((q + 2^(k-1)) >> k, 2^r - 1) (finding 1;
+// exhaustively checked in tests/test_oracle.py::test_slice_decomposition_identity
+// and on device by tests/test_gpu_parity.py).
+template <int R>
+MQ_HD void slice_bitsliced(const uint32_t (&T)[R + 1], uint32_t (&S)[R]) {
+    uint32_t all = T[0];
+#pragma unroll
+    for (int j = 1; j < R; ++j) all &= T[j];
+    uint32_t c = T[R] & ~all;
+#pragma unroll
+    for (int j = R - 1; j >= 0; --j) {
+        S[j] = T[j] ^ c;
+        c &= T[j];
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Plane -> field transpose networks.  Input P[0..NP-1] LSB-plane first.
+// After the network, word W_i holds, in field f (f-th NP-bit field of the
+// word), the NP-bit value of the weight at bit position NP*f + i.  Each stage
+// is a masked exchange of bit blocks between two words (2 shifts + 2 LOP3).
+MQ_HD void xchg(uint32_t& a, uint32_t& b, int s, uint32_t m) {
+    const uint32_t na = (a & m) | ((b << s) & ~m);
+    const uint32_t nb = ((a >> s) & m) | (b & ~m);
+    a = na;
+    b = nb;
+}
+template <int NP>
+MQ_HD void transpose_planes(uint32_t (&P)[NP]) {
+    if constexpr (NP == 8) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xchg(P[j], P[j + 4], 4, 0x0F0F0F0Fu);
+    }
+    if constexpr (NP >= 4) {
+#pragma unroll
+        for (int j0 = 0; j0 < NP; j0 += 4) {
+            xchg(P[j0 + 0], P[j0 + 2], 2, 0x33333333u);
+            xchg(P[j0 + 1], P[j0 + 3], 2, 0x33333333u);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NP; j += 2) xchg(P[j], P[j + 1], 1, 0x55555555u);
+}
+
+// ----------------------------------------------------------------------------
+// Decode one lane word-set into the 16 bf16x2 A registers of four mma k16
+// steps: A[p] holds weights at bit positions p (low half) and p + 16 (high
+// half) as exact bf16 (s - 2^(R-1)).  S[0..R-1] are the sliced planes, MSB
+// first.
+template <int R>
+MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
+    if constexpr (R == 2) {
+        uint32_t P[2] = {S[1], S[0]};
+        transpose_planes<2>(P);
+        // W_i field n (offset 2n) <-> position 2n + i
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const uint32_t w0 = P[i], w6 = P[i] >> 6, w12 = P[i] >> 12;
+            A[0 + i] = field_bf16<2, 0>(w0);
+            A[2 + i] = field_bf16<2, 2>(w0);
+            A[4 + i] = field_bf16<2, 4>(w0);
+            A[6 + i] = field_bf16<2, 0>(w6);
+            A[8 + i] = field_bf16<2, 2>(w6);
+            A[10 + i] = field_bf16<2, 4>(w6);
+            A[12 + i] = field_bf16<2, 0>(w12);
+            A[14 + i] = field_bf16<2, 2>(w12);
+        }
+    } else if constexpr (R == 3 || R == 4) {
+        uint32_t P[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) P[j] = j < R ? S[R - 1 - j] : 0u;
+        transpose_planes<4>(P);
+        // W_i nibble n (offset 4n) <-> position 4n + i
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t w = P[i];
+            if constexpr (R == 3) {
+                const uint32_t w8 = w >> 8;
+                A[0 + i] = field_bf16<3, 0>(w);
+                A[4 + i] = field_bf16<3, 4>(w);
+                A[8 + i] = field_bf16<3, 0>(w8);
+                A[12 + i] = field_bf16<3, 4>(w8);
+            } else {
+                A[0 + i] = field_bf16<4, 0>(w);
+                A[4 + i] = field_bf16<4, 3>(w >> 1);
+                A[8 + i] = field_bf16<4, 0>(w >> 8);
+                A[12 + i] = field_bf16<4, 3>(w >> 9);
+            }
+        }
+    } else {
+        static_assert(R == 6 || R == 8, "R must be on the ladder {2,3,4,6,8}");
+        uint32_t P[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) P[j] = j < R ? S[R - 1 - j] : 0u;
+        transpose_planes<8>(P);
+        // W_i byte b (offset 8b) <-> position 8b + i
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if constexpr (R == 6) {
+                A[0 + i] = field_bf16<6, 0>(P[i]);
+                A[8 + i] = field_bf16<6, 0>(P[i] >> 8);
+            } else {
+                A[0 + i] = field8_bf16(P[i]);
+                A[8 + i] = field8_bf16(P[i] >> 8);
+            }
+        }
+    }
+}
+
+// Loaded planes -> sliced planes.  CHILD: planes already hold the r-bit code
+// (mode C, r planes).  Parent mode P: R+1 planes (top R + rounding bit), or
+// 8 planes at R = 8 (identity slice).
+template <int R, bool CHILD>
+struct PlaneCount {
+    static constexpr int value = CHILD ? R : (R < 8 ? R + 1 : 8);
+};
+
+template <int R, bool CHILD>
+MQ_HD void slice_loaded(const uint32_t (&T)[PlaneCount<R, CHILD>::value],
+                                             uint32_t (&S)[R]) {
+    if constexpr (CHILD || R == 8) {
+#pragma unroll
+        for (int j = 0; j < R; ++j) S[j] = T[j];
+    } else {
+        slice_bitsliced<R>(T, S);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// Memory / tensor-core wrappers.
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t word_of(const uint4& v, int w) {
+    return w == 0 ? v.x : (w == 1 ? v.y : (w == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t (&d)[4], uint32_t saddr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+                 : "r"(saddr));
+}
+
+// D += A * B, m16n8k16, bf16 inputs, fp32 accumulate.
+__device__ __forceinline__ void mma_acc(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                        uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// D = A * B (zero accumulator input).
+__device__ __forceinline__ void mma_zero(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%10,%10,%10,%10};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.0f));
+}
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
+    return __uint_as_float(((uint32_t)h) << 16);
+}
+__device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// Programmatic dependent launch controls (no-ops when launched without PDL).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;");
+}
+
+}  // namespace mq

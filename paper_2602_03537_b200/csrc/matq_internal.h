@@ -1,0 +1,34 @@
+// Internal launcher declarations shared by matq_abi.cu and the kernel units.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mq {
+
+cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits,
+                               uint32_t* planes, cudaStream_t s);
+cudaError_t launch_tile_scales(const float* scales, int N, int ng, int ngp, float* ts,
+                               cudaStream_t s);
+cudaError_t launch_slice_codes(int r, bool child, const uint32_t* planes, int N, int K,
+                               uint8_t* out, long long ldo, cudaStream_t s);
+cudaError_t launch_decode_dense(int r, bool child, const uint32_t* planes, const float* ts, int G,
+                                float out_scale, int N, int K, int8_t* vals, float* W,
+                                long long ldw, cudaStream_t s);
+cudaError_t launch_materialize_child(int r, const uint32_t* planes, int N, int K, uint32_t* child,
+                                     cudaStream_t s);
+cudaError_t launch_slice_elementwise(const uint8_t* q, long long n, int c, int r, int on_master,
+                                     uint8_t* out, int* err, cudaStream_t s);
+cudaError_t launch_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int ng,
+                               int G, int c, int r, double* out, int* err, cudaStream_t s);
+cudaError_t launch_dequant_value_f64(const uint8_t* q, const double* scale, long long n, int c,
+                                     int r, double* out, int* err, cudaStream_t s);
+cudaError_t launch_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y,
+                              cudaStream_t s);
+cudaError_t launch_pack_ref_layout(const uint8_t* codes, int N, int K, int bits,
+                                   unsigned long long* base, uint32_t* b2, uint32_t* b3, int* err,
+                                   cudaStream_t s);
+cudaError_t launch_unpack_ref_layout(const unsigned long long* base, const uint32_t* b2,
+                                     const uint32_t* b3, int N, int K, uint8_t* codes,
+                                     cudaStream_t s);
+
+}  // namespace mq
