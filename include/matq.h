@@ -103,8 +103,10 @@ MQ_API int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uin
  * Y (B, N) with row stride ldy.  out_scale multiplies the tiled scales
  * (2^(c-r) for a parent slice, exact; 1.0 for a child with effective scales).
  * G must be a multiple of 32.  `workspace` must hold
- * mq_gemv_workspace_bytes(N, K, B, flags) bytes, zero-filled once at
- * allocation; calls leave it zeroed.  One workspace per stream. */
+ * mq_gemv_workspace_bytes(N, K, B, flags) bytes (0 when the launch needs no
+ * cross-CTA split-K) and be zero-filled once at allocation: its first 64 KiB
+ * are split-K tickets that every call leaves at zero, so one workspace (sized
+ * for the largest layer) serves any sequence of GEMVs on one stream. */
 MQ_API size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags);
 MQ_API int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y,
             int ldy, int B, int N, int K, int G, int r, float out_scale, int flags,

@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 
 #include "../../include/matq.h"
@@ -45,16 +46,20 @@ struct GemvConfig {
     int NT, RT, KW, ITERS, S;
     size_t smem;
     int xs_stride;
+    int stages;
+    int xs_bytes;
 };
 
-constexpr size_t kSmemMax = 96 * 1024;
+constexpr size_t kXsMax = 48 * 1024;       // activations staged per CTA
+constexpr size_t kSmemPerCta2 = 113 * 1024; // two CTAs per SM
+constexpr size_t kSmemPerCta1 = 220 * 1024; // one CTA per SM
 
 // Decomposition heuristic: one 16-row tile per warp, 8 warps
 // per CTA split RT (row tiles) x KW (K slices); RT grows with the batch so
 // the staged X is reused by more rows.  K is further split across S CTAs
 // until the grid covers ~2 CTAs per SM or a warp is down to 2 steps, and
 // until the staged X fits the shared-memory budget.
-GemvConfig choose_gemv_config(int N, int K, int Bx) {
+GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
     GemvConfig c{};
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
@@ -73,23 +78,33 @@ GemvConfig choose_gemv_config(int N, int K, int Bx) {
     while (true) {
         iters = mq::cdiv(nsteps, c.KW * S);
         const bool small_grid = (long long)rows_ctas * S < target && iters > 2;
-        const bool too_big = smem_for(iters) > kSmemMax && iters > 1;
+        const bool too_big = smem_for(iters) > kXsMax && iters > 1;
         if (!small_grid && !too_big) break;
         ++S;
     }
     c.ITERS = iters;
     c.S = mq::cdiv(nsteps, c.KW * c.ITERS);
-    c.smem = smem_for(c.ITERS);
+    c.xs_bytes = (int)((smem_for(c.ITERS) + 15) & ~(size_t)15);
     c.xs_stride = c.KW * c.ITERS * 256 + 8;
+    // per-warp TMA ring: as deep as fits while keeping 2 CTAs/SM (max 4)
+    const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
+    const size_t fixed = c.xs_bytes + 512;
+    int d = (int)((kSmemPerCta2 - std::min(fixed, kSmemPerCta2)) / (8 * stage));
+    if (d < 2) d = (int)((kSmemPerCta1 - std::min(fixed, kSmemPerCta1)) / (8 * stage));
+    c.stages = std::max(1, std::min(4, d));
+    c.smem = fixed + 8 * (size_t)c.stages * stage;
     return c;
 }
 
-size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+// Workspace layout: [kTicketBytes of int tickets][fp32 partials].  The ticket
+// region has a fixed size so that every GEMV sharing a workspace (any shape,
+// any decomposition) finds its tickets where the previous one left them at 0.
+constexpr size_t kTicketBytes = 64 * 1024;
+constexpr int kMaxTickets = (int)(kTicketBytes / sizeof(int));
 
 size_t gemv_ws_bytes(int N, const GemvConfig& c, int B) {
     if (c.S <= 1) return 0;
-    const int rows_ctas = mq::cdiv(mq::pad16(N) / 16, c.RT);
-    return align256((size_t)rows_ctas * sizeof(int)) + (size_t)c.S * B * mq::pad16(N) * sizeof(float);
+    return kTicketBytes + (size_t)c.S * B * mq::pad16(N) * sizeof(float);
 }
 
 mq::GemvLaunchFn gemv_launcher(int r) {
@@ -182,7 +197,7 @@ size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
     if (N < 1 || K < 1 || B < 1) return 0;
     const int Bx = (flags & MQ_X_F32) ? 2 * B : B;
     if (Bx > 32) return 0;
-    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx), B);
+    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, 8, true), B);
 }
 
 int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y, int ldy,
@@ -197,7 +212,9 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     const int Bx = xf32 ? 2 * B : B;
     if (Bx > 32) return fail(MQ_ERR_INVALID, "batch %d above the GEMV limit (32 rows, 16 with fp32 X)", B);
 
-    const GemvConfig c = choose_gemv_config(N, K, Bx);
+    const bool child_mode = (flags & MQ_CHILD) != 0;
+    const int npl = (child_mode || r == 8) ? r : r + 1;
+    const GemvConfig c = choose_gemv_config(N, K, Bx, npl, G == 128);
     const size_t need = gemv_ws_bytes(N, c, B);
     if (need > workspace_bytes || (need && !workspace))
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
@@ -210,9 +227,9 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.Y = Y;
     const int rows_ctas = mq::cdiv(mq::pad16(N) / 16, c.RT);
     if (need) {
+        if (rows_ctas > kMaxTickets) return fail(MQ_ERR_INVALID, "N=%d too large for split-K", N);
         p.tickets = reinterpret_cast<int*>(workspace);
-        p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) +
-                                        align256((size_t)rows_ctas * sizeof(int)));
+        p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kTicketBytes);
     }
     p.out_scale = out_scale;
     p.ldx = ldx;
@@ -233,6 +250,8 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.x_f32 = xf32 ? 1 : 0;
     p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
     p.xs_stride = c.xs_stride;
+    p.stages = c.stages;
+    p.xs_bytes = c.xs_bytes;
     const dim3 grid(rows_ctas, c.S, 1);
     const int gs = (G == 128) ? 128 : 0;
     const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, c.smem,

@@ -92,6 +92,54 @@ MQ_HD uint32_t hsub2(uint32_t a, uint32_t b) {
 #endif
 }
 
+// ----------------------------------------------------------------------------
+// Pipe-balanced integer primitives.  The decode is ALU-bound, and the SM has
+// two half-rate integer-capable pipes: LOP3/SHF issue on the ALU pipe,
+// IMAD/HFMA2 on the FMA pipe.  Left shifts are written as IMAD.SHL and right
+// shifts as IMAD.HI (x * 2^(32-s) >> 32) so they land on the FMA pipe, and
+// every 3-input boolean is one explicit LOP3 (ptxas otherwise splits
+// (x & imm) | imm into two).
+template <uint32_t LUT>
+MQ_HD uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+    return d;
+#else
+    uint32_t d = 0;
+    for (int i = 0; i < 8; ++i)
+        if ((LUT >> i) & 1u)
+            d |= ((i & 4) ? a : ~a) & ((i & 2) ? b : ~b) & ((i & 1) ? c : ~c);
+    return d;
+#endif
+}
+// LUTs over (a = 0xF0, b = 0xCC, c = 0xAA)
+constexpr uint32_t kAndOr = 0xEA;   // (a & b) | c
+constexpr uint32_t kAndXor = 0x6A;  // (a & b) ^ c
+constexpr uint32_t kSelect = 0xE4;  // (a & c) | (b & ~c)
+
+template <int S>
+MQ_HD uint32_t shl(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << S));
+    return d;
+#else
+    return x << S;
+#endif
+}
+template <int S>
+MQ_HD uint32_t shr(uint32_t x) {
+    static_assert(S > 0 && S < 32, "shift");
+#ifdef __CUDA_ARCH__
+    uint32_t d;
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - S)));
+    return d;
+#else
+    return x >> S;
+#endif
+}
+
 // Field of R bits at bit offset O of both 16-bit halves of w -> bf16x2 of
 // (field - 2^(R-1)), exact.  (w & mask) | 0x4300 is bf16 128 + field*2^O; one
 // bf16x2 FMA by 2^-O with addend -(128*2^-O + z) lands on field - z exactly.
@@ -99,7 +147,7 @@ template <int R, int O>
 MQ_HD uint32_t field_bf16(uint32_t w) {
     static_assert(O + R <= 7, "field must sit inside the bf16 mantissa");
     constexpr uint32_t m = ((1u << R) - 1u) << O;
-    const uint32_t v = (w & x2(m)) | 0x43004300u;
+    const uint32_t v = lop3<kAndOr>(w, x2(m), 0x43004300u);
     constexpr uint32_t mul = x2(bf16_bits(1, O));
     constexpr uint32_t add = x2(bf16_bits(-((128 >> O) + (1 << (R - 1))), 0));
     return hfma2(v, mul, add);
@@ -108,8 +156,8 @@ MQ_HD uint32_t field_bf16(uint32_t w) {
 // 8-bit field at offset 0 (bit 7 would land in the bf16 exponent):
 // (low7 | 0x4300) - (bit7 ? 128 : 256) = code - 128, exact.
 MQ_HD uint32_t field8_bf16(uint32_t w) {
-    const uint32_t a = (w & 0x007F007Fu) | 0x43004300u;
-    const uint32_t b = (w & 0x00800080u) ^ 0x43804380u;
+    const uint32_t a = lop3<kAndOr>(w, 0x007F007Fu, 0x43004300u);
+    const uint32_t b = lop3<kAndXor>(w, 0x00800080u, 0x43804380u);
     return hsub2(a, b);
 }
 
@@ -139,9 +187,10 @@ MQ_HD void slice_bitsliced(const uint32_t (&T)[R + 1], uint32_t (&S)[R]) {
 // After the network, word W_i holds, in field f (f-th NP-bit field of the
 // word), the NP-bit value of the weight at bit position NP*f + i.  Each stage
 // is a masked exchange of bit blocks between two words (2 shifts + 2 LOP3).
-MQ_HD void xchg(uint32_t& a, uint32_t& b, int s, uint32_t m) {
-    const uint32_t na = (a & m) | ((b << s) & ~m);
-    const uint32_t nb = ((a >> s) & m) | (b & ~m);
+template <int S>
+MQ_HD void xchg(uint32_t& a, uint32_t& b, uint32_t m) {
+    const uint32_t na = lop3<kSelect>(a, shl<S>(b), m);
+    const uint32_t nb = lop3<kSelect>(shr<S>(a), b, m);
     a = na;
     b = nb;
 }
@@ -149,17 +198,17 @@ template <int NP>
 MQ_HD void transpose_planes(uint32_t (&P)[NP]) {
     if constexpr (NP == 8) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) xchg(P[j], P[j + 4], 4, 0x0F0F0F0Fu);
+        for (int j = 0; j < 4; ++j) xchg<4>(P[j], P[j + 4], 0x0F0F0F0Fu);
     }
     if constexpr (NP >= 4) {
 #pragma unroll
         for (int j0 = 0; j0 < NP; j0 += 4) {
-            xchg(P[j0 + 0], P[j0 + 2], 2, 0x33333333u);
-            xchg(P[j0 + 1], P[j0 + 3], 2, 0x33333333u);
+            xchg<2>(P[j0 + 0], P[j0 + 2], 0x33333333u);
+            xchg<2>(P[j0 + 1], P[j0 + 3], 0x33333333u);
         }
     }
 #pragma unroll
-    for (int j = 0; j < NP; j += 2) xchg(P[j], P[j + 1], 1, 0x55555555u);
+    for (int j = 0; j < NP; j += 2) xchg<1>(P[j], P[j + 1], 0x55555555u);
 }
 
 // ----------------------------------------------------------------------------
@@ -175,7 +224,7 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         // W_i field n (offset 2n) <-> position 2n + i
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            const uint32_t w0 = P[i], w6 = P[i] >> 6, w12 = P[i] >> 12;
+            const uint32_t w0 = P[i], w6 = shr<6>(P[i]), w12 = shr<12>(P[i]);
             A[0 + i] = field_bf16<2, 0>(w0);
             A[2 + i] = field_bf16<2, 2>(w0);
             A[4 + i] = field_bf16<2, 4>(w0);
@@ -195,16 +244,16 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         for (int i = 0; i < 4; ++i) {
             const uint32_t w = P[i];
             if constexpr (R == 3) {
-                const uint32_t w8 = w >> 8;
+                const uint32_t w8 = shr<8>(w);
                 A[0 + i] = field_bf16<3, 0>(w);
                 A[4 + i] = field_bf16<3, 4>(w);
                 A[8 + i] = field_bf16<3, 0>(w8);
                 A[12 + i] = field_bf16<3, 4>(w8);
             } else {
                 A[0 + i] = field_bf16<4, 0>(w);
-                A[4 + i] = field_bf16<4, 3>(w >> 1);
-                A[8 + i] = field_bf16<4, 0>(w >> 8);
-                A[12 + i] = field_bf16<4, 3>(w >> 9);
+                A[4 + i] = field_bf16<4, 3>(shr<1>(w));
+                A[8 + i] = field_bf16<4, 0>(shr<8>(w));
+                A[12 + i] = field_bf16<4, 3>(shr<9>(w));
             }
         }
     } else {
@@ -218,10 +267,10 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         for (int i = 0; i < 8; ++i) {
             if constexpr (R == 6) {
                 A[0 + i] = field_bf16<6, 0>(P[i]);
-                A[8 + i] = field_bf16<6, 0>(P[i] >> 8);
+                A[8 + i] = field_bf16<6, 0>(shr<8>(P[i]));
             } else {
                 A[0 + i] = field8_bf16(P[i]);
-                A[8 + i] = field8_bf16(P[i] >> 8);
+                A[8 + i] = field8_bf16(shr<8>(P[i]));
             }
         }
     }
@@ -289,6 +338,61 @@ __device__ __forceinline__ float bf16_to_f32(uint16_t h) {
 }
 __device__ __forceinline__ uint16_t f32_to_bf16_rn(float f) {
     return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+
+// ---- TMA bulk copies + mbarriers (per-warp staging ring) --------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float lds32f(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
 }
 
 // Programmatic dependent launch controls (no-ops when launched without PDL).

@@ -5,8 +5,11 @@
 // This replaces the reference's nq_gemv / nq_gemm (packed_kernels.c:84-210,
 // driven by kernels/_core.pyx:24-64).  Work decomposition:
 //   * a warp owns one 16-row tile and a contiguous run of 256-column steps;
-//   * per step it issues one 128-bit streaming load per plane (512 B/warp),
-//     software-pipelined one step ahead, plus the step's group scales;
+//   * per step it needs one 512-byte slab per plane (the 16 x 256 tile of
+//     that plane is contiguous) plus 128 bytes of group scales; lane 0 of
+//     each warp keeps a ring of `stages` such steps in flight with TMA bulk
+//     copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first), so the
+//     memory pipeline costs no registers and one instruction per slab;
 //   * each lane slices its words bitsliced (32 weights / op), transposes the
 //     planes into packed fields and converts them to exact bf16 (s - z) in
 //     registers, already in mma A-fragment order (the P8 layout guarantees
@@ -39,10 +42,12 @@ struct GemvParams {
     int x_f32;                // X is fp32 (split into hi + lo bf16 rows)
     int y_f32;                // Y is fp32
     int xs_stride;            // smem X row stride (elements)
+    int stages;               // per-warp TMA ring depth
+    int xs_bytes;             // smem bytes reserved for X staging / reduction (16-aligned)
 };
 
 template <int R, int NT, bool CHILD, int GS>
-__global__ void __launch_bounds__(256, 1) k_gemv(const GemvParams p) {
+__global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams p) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
@@ -58,29 +63,40 @@ __global__ void __launch_bounds__(256, 1) k_gemv(const GemvParams p) {
     const int st1 = min(st0 + p.ITERS, p.nsteps);
     const bool has_work = rt < n_rt && st0 < st1;
 
-    const long long pstride4 = p.plane_stride >> 2;  // in uint4
-    const uint4* wbase = reinterpret_cast<const uint4*>(p.planes) +
-                         (long long)(has_work ? rt : 0) * p.nsteps * 32 + lane;
     const float* sbase = p.tscales + (long long)(has_work ? rt : 0) * p.ngp * 16;
 
-    uint4 bufA[NPL], bufB[NPL];
-    float scA[4], scB[4];
-
-    auto load_step = [&](uint4 (&buf)[NPL], float (&sc)[4], int st) {
+    // ---- per-warp TMA bulk ring: stage = NPL plane slabs (512 B) + scales --
+    constexpr uint32_t kSlab = 512;
+    constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;
+    constexpr uint32_t kStageBytes = NPL * kSlab + kScaleBytes;
+    const int D = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
+    uint8_t* ring = smem + p.xs_bytes + 8 * 8 * 8;  // 8 warps x up to 8 stages x 8 B
+    const uint32_t my_bar0 = smem_addr(bars + warp * 8);
+    const uint32_t my_ring0 = smem_addr(ring + (size_t)warp * D * kStageBytes);
+    const uint32_t* gplanes = p.planes + ((long long)(has_work ? rt : 0) * p.nsteps) * 128;
+    const float* gscales = sbase;
+    uint64_t policy = 0;
+    if (lane == 0) {
+        policy = policy_evict_first();
+        for (int i = 0; i < D; ++i) mbar_init(my_bar0 + 8 * i, 1);
+        fence_mbar_init();
+    }
+    __syncwarp();
+    auto issue = [&](int st, int stage) {  // lane 0 only
+        const uint32_t bar = my_bar0 + 8 * stage;
+        const uint32_t dst = my_ring0 + stage * kStageBytes;
+        mbar_expect_tx(bar, kStageBytes);
 #pragma unroll
-        for (int j = 0; j < NPL; ++j) buf[j] = ldg_stream(wbase + j * pstride4 + (long long)st * 32);
-        if constexpr (GS == 128) {
-            const float* sp = sbase + (2 * st) * 16 + g;
-            sc[0] = __ldg(sp);
-            sc[1] = __ldg(sp + 8);
-            sc[2] = __ldg(sp + 16);
-            sc[3] = __ldg(sp + 24);
-        }
+        for (int j = 0; j < NPL; ++j)
+            bulk_g2s(dst + j * kSlab, gplanes + j * p.plane_stride + (long long)st * 128, kSlab, bar,
+                     policy);
+        if constexpr (GS == 128) bulk_g2s(dst + NPL * kSlab, gscales + (2 * st) * 16, kScaleBytes, bar, policy);
     };
-
-    // Weights do not depend on the previous kernel: start streaming before
+    // Weights do not depend on the previous kernel: fill the ring before
     // waiting on the programmatic dependency (X / workspace).
-    if (has_work) load_step(bufA, scA, st0);
+    if (has_work && lane == 0)
+        for (int i = 0; i < D && st0 + i < st1; ++i) issue(st0 + i, i);
     pdl_launch_dependents();
     pdl_wait();
 
@@ -223,15 +239,27 @@ __global__ void __launch_bounds__(256, 1) k_gemv(const GemvParams p) {
     };
 
     if (has_work) {
-        int st = st0;
 #pragma unroll 1
-        while (true) {
-            if (st + 1 < st1) load_step(bufB, scB, st + 1);
-            process(bufA, scA, st);
-            if (++st >= st1) break;
-            if (st + 1 < st1) load_step(bufA, scA, st + 1);
-            process(bufB, scB, st);
-            if (++st >= st1) break;
+        for (int i = 0, st = st0; st < st1; ++i, ++st) {
+            const int stage = i % D;
+            mbar_wait(my_bar0 + 8 * stage, (uint32_t)((i / D) & 1));
+            const uint32_t src = my_ring0 + stage * kStageBytes;
+            uint4 buf[NPL];
+#pragma unroll
+            for (int j = 0; j < NPL; ++j) buf[j] = lds128(src + j * kSlab + lane * 16);
+            float sc[4];
+            if constexpr (GS == 128) {
+                sc[0] = lds32f(src + NPL * kSlab + g * 4);
+                sc[1] = lds32f(src + NPL * kSlab + (g + 8) * 4);
+                sc[2] = lds32f(src + NPL * kSlab + (16 + g) * 4);
+                sc[3] = lds32f(src + NPL * kSlab + (24 + g) * 4);
+            }
+            __syncwarp();
+            if (lane == 0 && st + D < st1) {
+                fence_proxy_async_smem();
+                issue(st + D, stage);
+            }
+            process(buf, sc, st);
         }
         if constexpr (GS == 0) flush_generic();
     }
