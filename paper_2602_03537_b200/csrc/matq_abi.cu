@@ -43,56 +43,52 @@ int sm_count() {
 }
 
 struct GemvConfig {
-    int NT, RT, KW, ITERS, S;
+    int NT, S, cs, grid, nwarps, stages;
     size_t smem;
-    int xs_stride;
-    int stages;
-    int xs_bytes;
+    int xs_stride, xs_bytes;
 };
 
-constexpr size_t kXsMax = 48 * 1024;       // activations staged per CTA
-constexpr size_t kSmemPerCta2 = 113 * 1024; // two CTAs per SM
-constexpr size_t kSmemPerCta1 = 220 * 1024; // one CTA per SM
+constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA
+constexpr size_t kSmemHalfSm = 113 * 1024;  // leave room for the next layer's CTA (PDL)
+constexpr size_t kSmemFullSm = 220 * 1024;
 
-// Decomposition heuristic: one 16-row tile per warp, 8 warps
-// per CTA split RT (row tiles) x KW (K slices); RT grows with the batch so
-// the staged X is reused by more rows.  K is further split across S CTAs
-// until the grid covers ~2 CTAs per SM or a warp is down to 2 steps, and
-// until the staged X fits the shared-memory budget.
+// Decomposition.  One CTA of 8 independent warps per SM.  The
+// K range is cut into S chunks of cs steps; chunk kc is owned by grid/S CTAs
+// whose warps take row tiles round-robin.  S is chosen to minimise the
+// critical path in steps (units per warp x cs) plus a small per-chunk fixup
+// cost, subject to the staged activation chunk fitting kXsMax.
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
     GemvConfig c{};
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
-    c.RT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
-    c.KW = 8 / c.RT;
-    const int rows_ctas = mq::cdiv(n_rt, c.RT);
-    const int target = 2 * sm_count();
-    int S = 1;
-    int iters = mq::cdiv(nsteps, c.KW);
-    auto smem_for = [&](int it) {
-        const int kc = c.KW * it * 256;
-        const size_t xs = (size_t)Bx * (kc + 8) * 2;
-        const size_t red = (size_t)c.NT * 4096;
-        return xs > red ? xs : red;
-    };
-    while (true) {
-        iters = mq::cdiv(nsteps, c.KW * S);
-        const bool small_grid = (long long)rows_ctas * S < target && iters > 2;
-        const bool too_big = smem_for(iters) > kXsMax && iters > 1;
-        if (!small_grid && !too_big) break;
-        ++S;
+    c.nwarps = 8;
+    const int sms = sm_count();
+    double best = 1e30;
+    for (int S = 1; S <= std::min(nsteps, 64); ++S) {
+        const int cs = mq::cdiv(nsteps, S);
+        if (mq::cdiv(nsteps, cs) != S) continue;  // would leave an empty chunk
+        const size_t xs = (size_t)Bx * (cs * 256 + 8) * 2;
+        if (xs > kXsMax && cs > 1) continue;
+        int cpc = sms / S;
+        if (cpc < 1) break;
+        cpc = std::min(cpc, mq::cdiv(n_rt, c.nwarps));
+        const int units_per_warp = mq::cdiv(n_rt, cpc * c.nwarps);
+        const double cost = (double)units_per_warp * cs + (S > 1 ? 0.25 + 0.02 * S : 0.0);
+        if (cost < best - 1e-9) {
+            best = cost;
+            c.S = S;
+            c.cs = cs;
+            c.grid = cpc * S;
+        }
     }
-    c.ITERS = iters;
-    c.S = mq::cdiv(nsteps, c.KW * c.ITERS);
-    c.xs_bytes = (int)((smem_for(c.ITERS) + 15) & ~(size_t)15);
-    c.xs_stride = c.KW * c.ITERS * 256 + 8;
-    // per-warp TMA ring: as deep as fits while keeping 2 CTAs/SM (max 4)
+    c.xs_stride = c.cs * 256 + 8;
+    c.xs_bytes = (int)(((size_t)Bx * c.xs_stride * 2 + 15) & ~(size_t)15);
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
-    const size_t fixed = c.xs_bytes + 512;
-    int d = (int)((kSmemPerCta2 - std::min(fixed, kSmemPerCta2)) / (8 * stage));
-    if (d < 2) d = (int)((kSmemPerCta1 - std::min(fixed, kSmemPerCta1)) / (8 * stage));
-    c.stages = std::max(1, std::min(4, d));
-    c.smem = fixed + 8 * (size_t)c.stages * stage;
+    const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
+    int d = (int)((kSmemHalfSm - std::min(fixed, kSmemHalfSm)) / (c.nwarps * stage));
+    if (d < 2) d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (c.nwarps * stage));
+    c.stages = std::max(1, std::min(8, d));
+    c.smem = fixed + (size_t)c.nwarps * c.stages * stage;
     return c;
 }
 
@@ -225,9 +221,9 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.tscales = tscales;
     p.X = X;
     p.Y = Y;
-    const int rows_ctas = mq::cdiv(mq::pad16(N) / 16, c.RT);
+    const int n_rt = mq::pad16(N) / 16;
     if (need) {
-        if (rows_ctas > kMaxTickets) return fail(MQ_ERR_INVALID, "N=%d too large for split-K", N);
+        if (n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "N=%d too large for split-K", N);
         p.tickets = reinterpret_cast<int*>(workspace);
         p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(workspace) + kTicketBytes);
     }
@@ -243,18 +239,18 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.G = G;
     p.ngp = mq::cdiv(p.Kp, G);
     p.nsteps = p.Kp / 256;
-    p.RT = c.RT;
-    p.KW = c.KW;
-    p.ITERS = c.ITERS;
+    p.n_rt = n_rt;
     p.S = c.S;
+    p.cs = c.cs;
+    p.ctas_per_chunk = c.grid / c.S;
     p.x_f32 = xf32 ? 1 : 0;
     p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
     p.xs_stride = c.xs_stride;
-    p.stages = c.stages;
     p.xs_bytes = c.xs_bytes;
-    const dim3 grid(rows_ctas, c.S, 1);
+    p.stages = c.stages;
+    const dim3 grid(c.grid, 1, 1), block(32 * c.nwarps, 1, 1);
     const int gs = (G == 128) ? 128 : 0;
-    const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, c.smem,
+    const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, block, c.smem,
                                            (cudaStream_t)stream, (flags & MQ_PDL) != 0);
     return cuda_status(e, "mq_gemv");
 }

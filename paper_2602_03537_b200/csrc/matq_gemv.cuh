@@ -2,24 +2,29 @@
 //
 // Y[b, n] = sum_g scale[n, g] * out_scale * sum_{k in g} (s_r(q[n,k]) - 2^(r-1)) * X[b, k]
 //
-// This replaces the reference's nq_gemv / nq_gemm (packed_kernels.c:84-210,
-// driven by kernels/_core.pyx:24-64).  Work decomposition:
-//   * a warp owns one 16-row tile and a contiguous run of 256-column steps;
-//   * per step it needs one 512-byte slab per plane (the 16 x 256 tile of
-//     that plane is contiguous) plus 128 bytes of group scales; lane 0 of
-//     each warp keeps a ring of `stages` such steps in flight with TMA bulk
-//     copies (cp.async.bulk + mbarrier complete_tx, L2 evict_first), so the
-//     memory pipeline costs no registers and one instruction per slab;
-//   * each lane slices its words bitsliced (32 weights / op), transposes the
-//     planes into packed fields and converts them to exact bf16 (s - z) in
-//     registers, already in mma A-fragment order (the P8 layout guarantees
-//     it), and feeds mma.m16n8k16 with fp32 accumulation per scale group;
-//   * X for the CTA's column range is staged once in shared memory and read
-//     as B fragments with ldmatrix;
-//   * warps of a CTA split K and reduce through shared memory in fixed
-//     order; CTAs that split K further write fp32 partials to a workspace
-//     and the last CTA to arrive (atomic ticket) reduces them in split order
-//     -- deterministic, one launch, graph-capturable.
+// Replaces the reference's nq_gemv / nq_gemm (packed_kernels.c:84-210, driven
+// by kernels/_core.pyx:24-64).  Structure:
+//   * Persistent streaming grid: one CTA per SM, sized to use at most half of
+//     the SM (registers, shared memory), so that under programmatic dependent
+//     launch the NEXT layer's CTAs become resident while this one runs and
+//     stream their first weights before waiting on this layer's output.
+//   * Work unit = (16-row tile, K chunk of `cs` 256-column steps).  K chunk kc
+//     is owned by CTAs with blockIdx % S == kc; each warp walks its units'
+//     steps as one flattened sequence, so its TMA ring never drains between
+//     row tiles.  Warps are independent: no intra-CTA reduction.
+//   * Per step a warp needs one 512-byte slab per plane (the 16 x 256 tile of
+//     a plane is contiguous in the P8 layout) plus 128 bytes of group scales;
+//     lane 0 keeps `stages` steps in flight with TMA bulk copies
+//     (cp.async.bulk + mbarrier complete_tx, L2 evict_first).
+//   * Each lane slices its words bitsliced (32 weights per instruction),
+//     transposes planes into packed fields, converts them to exact bf16
+//     (s - z) already in mma A-fragment order, and feeds mma.m16n8k16 with
+//     fp32 accumulation per scale group; activations for the CTA's K chunk
+//     are staged once in shared memory and read with ldmatrix.
+//   * S == 1: the warp writes Y straight from its accumulators.  S > 1: fp32
+//     partials go to a workspace and the last warp to finish a row tile (an
+//     atomic ticket per tile) sums them in chunk order -- deterministic, one
+//     launch, graph-capturable; tickets return to zero.
 #pragma once
 #include "matq_common.cuh"
 
@@ -32,50 +37,49 @@ struct GemvParams {
     const void* X;            // bf16 [B][ldx] or fp32 [B][ldx]
     void* Y;                  // bf16 [B][ldy] or fp32 [B][ldy]
     float* ws;                // fp32 [S][B][Np] when S > 1
-    int* tickets;             // [gridDim.x] zero-initialised, self-resetting
+    int* tickets;             // [n_rt] zero-initialised, self-resetting
     float out_scale;          // 2^(c - r) for parent slices, 1 for children
     int ldx, ldy;
     int B;                    // logical batch rows
-    int Bx;                   // activation rows in the mma N dim (2B when x_split)
-    int N, Np, K, Kp, G, ngp, nsteps;
-    int RT, KW, ITERS, S;     // decomposition (see choose_gemv_config)
+    int Bx;                   // activation rows in the mma N dim (2B when x_f32)
+    int N, Np, K, Kp, G, ngp, nsteps, n_rt;
+    int S, cs;                // K chunks, steps per chunk
+    int ctas_per_chunk;       // gridDim.x / S
     int x_f32;                // X is fp32 (split into hi + lo bf16 rows)
     int y_f32;                // Y is fp32
     int xs_stride;            // smem X row stride (elements)
-    int stages;               // per-warp TMA ring depth
-    int xs_bytes;             // smem bytes reserved for X staging / reduction (16-aligned)
+    int xs_bytes;             // smem bytes of the X staging area (16-aligned)
+    int stages;               // per-warp TMA ring depth (<= 8)
 };
 
+constexpr int kMaxWarps = 8;
+
 template <int R, int NT, bool CHILD, int GS>
-__global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams p) {
+__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_gemv(const GemvParams p) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
-    extern __shared__ __align__(16) uint8_t smem[];
-    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = lane >> 2;
-    const int rt_l = warp % p.RT, ks = warp / p.RT;
-    const int n_rt = p.Np / kTileRows;
-    const int rt = blockIdx.x * p.RT + rt_l;
-    const int split = blockIdx.y;
-    const int cta_step0 = split * p.KW * p.ITERS;
-    const int st0 = cta_step0 + ks * p.ITERS;
-    const int st1 = min(st0 + p.ITERS, p.nsteps);
-    const bool has_work = rt < n_rt && st0 < st1;
-
-    const float* sbase = p.tscales + (long long)(has_work ? rt : 0) * p.ngp * 16;
-
-    // ---- per-warp TMA bulk ring: stage = NPL plane slabs (512 B) + scales --
     constexpr uint32_t kSlab = 512;
     constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;
     constexpr uint32_t kStageBytes = NPL * kSlab + kScaleBytes;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
+
+    const int nwarps = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t = lane & 3;
+    const int kc = blockIdx.x % p.S, j = blockIdx.x / p.S;
+    const int chunk0 = kc * p.cs;
+    const int ns = max(0, min(chunk0 + p.cs, p.nsteps) - chunk0);
+    const int rt_first = j * nwarps + warp;
+    const int rt_stride = p.ctas_per_chunk * nwarps;
+    const int n_units = (rt_first < p.n_rt && ns > 0) ? (p.n_rt - 1 - rt_first) / rt_stride + 1 : 0;
+    const int total = n_units * ns;  // flattened (unit, step) sequence of this warp
+
+    // ---- per-warp TMA ring --------------------------------------------------
     const int D = p.stages;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
-    uint8_t* ring = smem + p.xs_bytes + 8 * 8 * 8;  // 8 warps x up to 8 stages x 8 B
+    uint8_t* ring = smem + p.xs_bytes + kMaxWarps * 8 * 8;
     const uint32_t my_bar0 = smem_addr(bars + warp * 8);
     const uint32_t my_ring0 = smem_addr(ring + (size_t)warp * D * kStageBytes);
-    const uint32_t* gplanes = p.planes + ((long long)(has_work ? rt : 0) * p.nsteps) * 128;
-    const float* gscales = sbase;
     uint64_t policy = 0;
     if (lane == 0) {
         policy = policy_evict_first();
@@ -83,26 +87,30 @@ __global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams 
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](int st, int stage) {  // lane 0 only
+    auto issue = [&](int f, int stage) {  // lane 0 only
+        const int m = f / ns, st = chunk0 + (f - m * ns);
+        const int rt = rt_first + m * rt_stride;
         const uint32_t bar = my_bar0 + 8 * stage;
         const uint32_t dst = my_ring0 + stage * kStageBytes;
+        const uint32_t* src = p.planes + ((long long)rt * p.nsteps + st) * 128;
         mbar_expect_tx(bar, kStageBytes);
 #pragma unroll
-        for (int j = 0; j < NPL; ++j)
-            bulk_g2s(dst + j * kSlab, gplanes + j * p.plane_stride + (long long)st * 128, kSlab, bar,
-                     policy);
-        if constexpr (GS == 128) bulk_g2s(dst + NPL * kSlab, gscales + (2 * st) * 16, kScaleBytes, bar, policy);
+        for (int jj = 0; jj < NPL; ++jj)
+            bulk_g2s(dst + jj * kSlab, src + jj * p.plane_stride, kSlab, bar, policy);
+        if constexpr (GS == 128)
+            bulk_g2s(dst + NPL * kSlab, p.tscales + ((long long)rt * p.ngp + 2 * st) * 16,
+                     kScaleBytes, bar, policy);
     };
     // Weights do not depend on the previous kernel: fill the ring before
-    // waiting on the programmatic dependency (X / workspace).
-    if (has_work && lane == 0)
-        for (int i = 0; i < D && st0 + i < st1; ++i) issue(st0 + i, i);
+    // waiting on the programmatic dependency (X, workspace, Y).
+    if (lane == 0)
+        for (int i = 0; i < D && i < total; ++i) issue(i, i);
     pdl_launch_dependents();
     pdl_wait();
 
-    // ---- stage X[:, cta columns] into shared memory as bf16 rows ----------
-    const int Kc = p.KW * p.ITERS * kStepCols;
-    const int col_base = cta_step0 * kStepCols;
+    // ---- stage X[:, chunk columns] into shared memory as bf16 rows ----------
+    const int Kc = p.cs * kStepCols;
+    const int col_base = chunk0 * kStepCols;
     if (!p.x_f32) {
         const uint16_t* X = reinterpret_cast<const uint16_t*>(p.X);
         const bool vec = ((p.ldx & 7) == 0) && ((p.K & 7) == 0) &&
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams 
     // ldmatrix row addresses: matrix mi = lane >> 3 covers k offset 8*mi of a
     // 32-column pair of k16 steps; row n = nt*8 + (lane & 7) (rows >= Bx read
     // row 0: their outputs are discarded).
-    const uint32_t xs_saddr = static_cast<uint32_t>(__cvta_generic_to_shared(xs));
+    const uint32_t xs_saddr = smem_addr(xs);
     uint32_t xrow_addr[NT];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
@@ -158,16 +166,10 @@ __global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams 
 #pragma unroll
         for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f, acc[nt][i] = 0.0f;
 
-    // generic group size bookkeeping (GS == 0)
-    int next_bound = 0, cur_grp = 0;
-    if constexpr (GS == 0) {
-        const int c0 = st0 * kStepCols;
-        cur_grp = c0 / p.G;
-        next_bound = (cur_grp + 1) * p.G;
-    }
-
+    // generic group size bookkeeping (GS == 0): groups may straddle steps
+    int next_bound = 0, cur_grp = 0, cur_rt = 0;
     auto flush_generic = [&]() {
-        const float* sp = sbase + cur_grp * 16 + g;
+        const float* sp = p.tscales + ((long long)cur_rt * p.ngp + cur_grp) * 16 + g;
         const float s_lo = __ldg(sp), s_hi = __ldg(sp + 8);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -185,7 +187,7 @@ __global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams 
         for (int w = 0; w < 4; ++w) {
             uint32_t T[NPL];
 #pragma unroll
-            for (int j = 0; j < NPL; ++j) T[j] = word_of(buf[j], w);
+            for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
             uint32_t S[R];
             slice_loaded<R, CHILD>(T, S);
             uint32_t A[16];
@@ -238,108 +240,129 @@ __global__ void __launch_bounds__(256, NT >= 4 ? 1 : 2) k_gemv(const GemvParams 
         }
     };
 
-    if (has_work) {
-#pragma unroll 1
-        for (int i = 0, st = st0; st < st1; ++i, ++st) {
-            const int stage = i % D;
-            mbar_wait(my_bar0 + 8 * stage, (uint32_t)((i / D) & 1));
-            const uint32_t src = my_ring0 + stage * kStageBytes;
-            uint4 buf[NPL];
-#pragma unroll
-            for (int j = 0; j < NPL; ++j) buf[j] = lds128(src + j * kSlab + lane * 16);
-            float sc[4];
-            if constexpr (GS == 128) {
-                sc[0] = lds32f(src + NPL * kSlab + g * 4);
-                sc[1] = lds32f(src + NPL * kSlab + (g + 8) * 4);
-                sc[2] = lds32f(src + NPL * kSlab + (16 + g) * 4);
-                sc[3] = lds32f(src + NPL * kSlab + (24 + g) * 4);
-            }
-            __syncwarp();
-            if (lane == 0 && st + D < st1) {
-                fence_proxy_async_smem();
-                issue(st + D, stage);
-            }
-            process(buf, sc, st);
-        }
-        if constexpr (GS == 0) flush_generic();
-    }
-
-    // ---- epilogue: fixed-order reduction over the CTA's K warps ------------
-    __syncthreads();  // X staging area is reused as the reduction buffer
-    float* red = reinterpret_cast<float*>(smem);
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) red[((warp * NT + nt) * 4 + i) * 32 + lane] = tot[nt][i];
-    __syncthreads();
-
-    const int rows_cta = p.RT * kTileRows;
-    const int row0 = blockIdx.x * rows_cta;
-    const bool multi = p.S > 1;
-    for (int idx = threadIdx.x; idx < p.B * rows_cta; idx += blockDim.x) {
-        const int b = idx / rows_cta, rl = idx - b * rows_cta;
-        const int rtl = rl >> 4, r16 = rl & 15;
-        const int gg = r16 & 7, hi = r16 >> 3;
-        float v = 0.0f;
-        if (!p.x_f32) {
-            const int nt = b >> 3, cc = b & 7;
-            const int ln = gg * 4 + (cc >> 1), i = hi * 2 + (cc & 1);
-            for (int k2 = 0; k2 < p.KW; ++k2) v += red[(((k2 * p.RT + rtl) * NT + nt) * 4 + i) * 32 + ln];
-        } else {
-            const int c = 2 * b, nt = c >> 3, cc = c & 7;
-            const int ln = gg * 4 + (cc >> 1), i = hi * 2;
-            float vh = 0.0f, vl = 0.0f;
-            for (int k2 = 0; k2 < p.KW; ++k2) {
-                const float* rp = red + (((k2 * p.RT + rtl) * NT + nt) * 4 + i) * 32 + ln;
-                vh += rp[0];
-                vl += rp[32];
-            }
-            v = vh + vl;
-        }
-        v *= p.out_scale;
-        const int row = row0 + rl;
-        if (multi) {
-            p.ws[((long long)split * p.B + b) * p.Np + row] = v;
-        } else if (row < p.N) {
-            if (p.y_f32)
-                reinterpret_cast<float*>(p.Y)[(long long)b * p.ldy + row] = v;
-            else
-                reinterpret_cast<uint16_t*>(p.Y)[(long long)b * p.ldy + row] = f32_to_bf16_rn(v);
-        }
-    }
-    if (!multi) return;
-
-    // ---- cross-CTA split-K: last CTA to arrive reduces in split order -------
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(p.tickets + blockIdx.x, 1);
-        s_last = (prev == p.S - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int idx = threadIdx.x; idx < p.B * rows_cta; idx += blockDim.x) {
-        const int b = idx / rows_cta, rl = idx - b * rows_cta;
-        const int row = row0 + rl;
-        if (row >= p.N) continue;
-        float v = 0.0f;
-        for (int s = 0; s < p.S; ++s) v += __ldcg(p.ws + ((long long)s * p.B + b) * p.Np + row);
+    // Output element (b, row) held by this thread for accumulator (nt, i):
+    // row = 16 rt + g + 8 (i >> 1), mma column n = 8 nt + 2 t + (i & 1);
+    // plain X: b = n; split X: columns (2b, 2b+1) = (hi, lo) of b = 4 nt + t.
+    auto store_y = [&](int b, int row, float v) {
         if (p.y_f32)
             reinterpret_cast<float*>(p.Y)[(long long)b * p.ldy + row] = v;
         else
             reinterpret_cast<uint16_t*>(p.Y)[(long long)b * p.ldy + row] = f32_to_bf16_rn(v);
+    };
+    auto finalize = [&](int rt) {
+        if constexpr (GS == 0) flush_generic();
+        const int r0 = rt * kTileRows + g;
+        float v[NT][2][2];  // [nt][row half][column parity | hi+lo combined]
+        int bcol[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            if (!p.x_f32) {
+                v[nt][0][0] = tot[nt][0] * p.out_scale;
+                v[nt][0][1] = tot[nt][1] * p.out_scale;
+                v[nt][1][0] = tot[nt][2] * p.out_scale;
+                v[nt][1][1] = tot[nt][3] * p.out_scale;
+                bcol[nt][0] = nt * 8 + 2 * t;
+                bcol[nt][1] = nt * 8 + 2 * t + 1;
+            } else {
+                v[nt][0][0] = (tot[nt][0] + tot[nt][1]) * p.out_scale;
+                v[nt][1][0] = (tot[nt][2] + tot[nt][3]) * p.out_scale;
+                v[nt][0][1] = v[nt][1][1] = 0.0f;
+                bcol[nt][0] = nt * 4 + t;
+                bcol[nt][1] = 1 << 30;  // no second column
+            }
+        }
+        if (p.S == 1) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int row = r0 + 8 * h, b = bcol[nt][c];
+                        if (b < p.B && row < p.N) store_y(b, row, v[nt][h][c]);
+                    }
+            return;
+        }
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int row = r0 + 8 * h, b = bcol[nt][c];
+                    if (b < p.B && row < p.N)
+                        p.ws[((long long)kc * p.B + b) * p.Np + row] = v[nt][h][c];
+                }
+        __threadfence();
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) last = (atomicAdd(p.tickets + rt, 1) == p.S - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (!last) return;
+        __threadfence();
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int row = r0 + 8 * h, b = bcol[nt][c];
+                    if (b < p.B && row < p.N) {
+                        float s = 0.0f;
+                        for (int q = 0; q < p.S; ++q)
+                            s += __ldcg(p.ws + ((long long)q * p.B + b) * p.Np + row);
+                        store_y(b, row, s);
+                    }
+                }
+        __syncwarp();
+        if (lane == 0) p.tickets[rt] = 0;
+    };
+
+#pragma unroll 1
+    for (int f = 0; f < total; ++f) {
+        const int m = f / ns, li = f - m * ns;
+        const int st = chunk0 + li;
+        const int rt = rt_first + m * rt_stride;
+        if (li == 0) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
+            if constexpr (GS == 0) {
+                cur_rt = rt;
+                cur_grp = (st * kStepCols) / p.G;
+                next_bound = (cur_grp + 1) * p.G;
+            }
+        }
+        const int stage = f % D;
+        mbar_wait(my_bar0 + 8 * stage, (uint32_t)((f / D) & 1));
+        const uint32_t src = my_ring0 + stage * kStageBytes;
+        uint4 buf[NPL];
+#pragma unroll
+        for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + jj * kSlab + lane * 16);
+        float sc[4];
+        if constexpr (GS == 128) {
+            sc[0] = lds32f(src + NPL * kSlab + g * 4);
+            sc[1] = lds32f(src + NPL * kSlab + (g + 8) * 4);
+            sc[2] = lds32f(src + NPL * kSlab + (16 + g) * 4);
+            sc[3] = lds32f(src + NPL * kSlab + (24 + g) * 4);
+        }
+        __syncwarp();
+        if (lane == 0 && f + D < total) {
+            fence_proxy_async_smem();
+            issue(f + D, stage);
+        }
+        process(buf, sc, st);
+        if (li == ns - 1) finalize(rt);
     }
-    if (threadIdx.x == 0) p.tickets[blockIdx.x] = 0;
 }
 
 // Host-side launcher table entry, implemented per R in matq_gemv_r*.cu.
 using GemvLaunchFn = cudaError_t (*)(const GemvParams&, int nt, bool child, int gs, dim3 grid,
-                                     size_t smem, cudaStream_t stream, bool pdl);
+                                     dim3 block, size_t smem, cudaStream_t stream, bool pdl);
 
 template <int R>
-cudaError_t launch_gemv_r(const GemvParams& p, int nt, bool child, int gs, dim3 grid, size_t smem,
-                          cudaStream_t stream, bool pdl);
+cudaError_t launch_gemv_r(const GemvParams& p, int nt, bool child, int gs, dim3 grid, dim3 block,
+                          size_t smem, cudaStream_t stream, bool pdl);
 
 }  // namespace mq

@@ -5,7 +5,7 @@
 namespace mq {
 
 template <typename K>
-static cudaError_t launch_one(K kernel, const GemvParams& p, dim3 grid, size_t smem,
+static cudaError_t launch_one(K kernel, const GemvParams& p, dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, bool pdl, int& smem_set) {
     if ((int)smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -15,7 +15,7 @@ static cudaError_t launch_one(K kernel, const GemvParams& p, dim3 grid, size_t s
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -30,7 +30,7 @@ static cudaError_t launch_one(K kernel, const GemvParams& p, dim3 grid, size_t s
 
 template <>
 cudaError_t launch_gemv_r<MQ_R>(const GemvParams& p, int nt, bool child, int gs, dim3 grid,
-                                size_t smem, cudaStream_t stream, bool pdl) {
+                                dim3 block, size_t smem, cudaStream_t stream, bool pdl) {
     constexpr int R = MQ_R;
     constexpr bool kChildOk = R < 8;  // at r = 8 a child is the parent
     static int smem_set[3][2][2] = {};
@@ -39,7 +39,7 @@ cudaError_t launch_gemv_r<MQ_R>(const GemvParams& p, int nt, bool child, int gs,
     const int gi = gs == 128 ? 0 : 1;
     int& ss = smem_set[ni][ci][gi];
 #define MQ_L(NT_, CH_, GS_) \
-    return launch_one(k_gemv<R, NT_, (CH_ && kChildOk), GS_>, p, grid, smem, stream, pdl, ss)
+    return launch_one(k_gemv<R, NT_, (CH_ && kChildOk), GS_>, p, grid, block, smem, stream, pdl, ss)
 #define MQ_GS(NT_, CH_)          \
     if (gi == 0) MQ_L(NT_, CH_, 128); \
     MQ_L(NT_, CH_, 0)

@@ -52,7 +52,8 @@ def test_host_layout_queries():
     assert L.mq_tscales_bytes(4096, 4096, 128) == 4096 * 32 * 4
     assert L.mq_layout_dims(0, 10, 128, None, None, None) == _lib.MQ_ERR_INVALID
     # workspace query is host-only
-    assert L.mq_gemv_workspace_bytes(4096, 4096, 1, 0) == 0
+    assert L.mq_gemv_workspace_bytes(16, 256, 1, 0) == 0  # one K step: no split-K
+    assert L.mq_gemv_workspace_bytes(4096, 4096, 1, 0) % 4 == 0
     assert L.mq_gemv_workspace_bytes(4096, 4096, 33, 0) == 0  # above the GEMV limit
 
 
