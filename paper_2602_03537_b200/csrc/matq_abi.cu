@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "../../include/matq.h"
@@ -49,7 +50,6 @@ struct GemvConfig {
 };
 
 constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA
-constexpr size_t kSmemHalfSm = 113 * 1024;  // leave room for the next layer's CTA (PDL)
 constexpr size_t kSmemFullSm = 220 * 1024;
 
 // Decomposition.  One CTA of 8 independent warps per SM.  The
@@ -57,23 +57,32 @@ constexpr size_t kSmemFullSm = 220 * 1024;
 // whose warps take row tiles round-robin.  S is chosen to minimise the
 // critical path in steps (units per warp x cs) plus a small per-chunk fixup
 // cost, subject to the staged activation chunk fitting kXsMax.
+int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
     GemvConfig c{};
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
-    c.nwarps = 8;
+    // tuning overrides (scripts/sweep_gemv.py): MQ_GEMV_WARPS, MQ_GEMV_SPLIT, MQ_GEMV_STAGES
+    c.nwarps = std::max(1, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
+    const int force_s = env_int("MQ_GEMV_SPLIT", 0);
+    const double fixup = 2.0;  // a split-K tile costs ~2 steps (partials, ticket, reduction)
     const int sms = sm_count();
     double best = 1e30;
     for (int S = 1; S <= std::min(nsteps, 64); ++S) {
+        if (force_s && S != std::min(force_s, nsteps)) continue;
         const int cs = mq::cdiv(nsteps, S);
-        if (mq::cdiv(nsteps, cs) != S) continue;  // would leave an empty chunk
+        if (mq::cdiv(nsteps, cs) != S && !force_s) continue;  // would leave an empty chunk
         const size_t xs = (size_t)Bx * (cs * 256 + 8) * 2;
         if (xs > kXsMax && cs > 1) continue;
         int cpc = sms / S;
         if (cpc < 1) break;
         cpc = std::min(cpc, mq::cdiv(n_rt, c.nwarps));
         const int units_per_warp = mq::cdiv(n_rt, cpc * c.nwarps);
-        const double cost = (double)units_per_warp * cs + (S > 1 ? 0.25 + 0.02 * S : 0.0);
+        const double cost = (double)units_per_warp * (cs + (S > 1 ? fixup : 0.0));
         if (cost < best - 1e-9) {
             best = cost;
             c.S = S;
@@ -85,9 +94,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
     c.xs_bytes = (int)(((size_t)Bx * c.xs_stride * 2 + 15) & ~(size_t)15);
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
     const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
-    int d = (int)((kSmemHalfSm - std::min(fixed, kSmemHalfSm)) / (c.nwarps * stage));
-    if (d < 2) d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (c.nwarps * stage));
-    c.stages = std::max(1, std::min(8, d));
+    int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (c.nwarps * stage));
+    c.stages = std::max(1, std::min(std::min(8, env_int("MQ_GEMV_STAGES", 4)), d));
     c.smem = fixed + (size_t)c.nwarps * c.stages * stage;
     return c;
 }

@@ -52,10 +52,10 @@ struct GemvParams {
     int stages;               // per-warp TMA ring depth (<= 8)
 };
 
-constexpr int kMaxWarps = 8;
+constexpr int kMaxWarps = 16;
 
 template <int R, int NT, bool CHILD, int GS>
-__global__ void __launch_bounds__(kMaxWarps * 32, 1) k_gemv(const GemvParams p) {
+__global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(const GemvParams p) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512;
     constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;
@@ -293,13 +293,13 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_gemv(const GemvParams p) 
                     if (b < p.B && row < p.N)
                         p.ws[((long long)kc * p.B + b) * p.Np + row] = v[nt][h][c];
                 }
-        __threadfence();
+        // publish: warp barrier orders all lanes' partials before lane 0's
+        // release-RMW on the tile ticket; the last arriver acquires.
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = (atomicAdd(p.tickets + rt, 1) == p.S - 1);
+        if (lane == 0) last = (atom_add_acq_rel(p.tickets + rt, 1) == p.S - 1);
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) return;
-        __threadfence();
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -308,9 +308,16 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_gemv(const GemvParams p) 
                 for (int c = 0; c < 2; ++c) {
                     const int row = r0 + 8 * h, b = bcol[nt][c];
                     if (b < p.B && row < p.N) {
+                        const float* wp = p.ws + (long long)b * p.Np + row;
+                        const long long cstride = (long long)p.B * p.Np;
                         float s = 0.0f;
-                        for (int q = 0; q < p.S; ++q)
-                            s += __ldcg(p.ws + ((long long)q * p.B + b) * p.Np + row);
+                        int q = 0;
+                        for (; q + 4 <= p.S; q += 4) {  // independent loads, ordered sum
+                            const float a0 = __ldcg(wp + q * cstride), a1 = __ldcg(wp + (q + 1) * cstride);
+                            const float a2 = __ldcg(wp + (q + 2) * cstride), a3 = __ldcg(wp + (q + 3) * cstride);
+                            s += a0; s += a1; s += a2; s += a3;
+                        }
+                        for (; q < p.S; ++q) s += __ldcg(wp + q * cstride);
                         store_y(b, row, s);
                     }
                 }
