@@ -256,6 +256,7 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.xs_stride = c.xs_stride;
     p.xs_bytes = c.xs_bytes;
     p.stages = c.stages;
+    p.debug = env_int("MQ_GEMV_DEBUG", 0);
     const dim3 grid(c.grid, 1, 1), block(32 * c.nwarps, 1, 1);
     const int gs = (G == 128) ? 128 : 0;
     const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, block, c.smem,

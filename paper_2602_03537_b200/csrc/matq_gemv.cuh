@@ -50,6 +50,7 @@ struct GemvParams {
     int xs_stride;            // smem X row stride (elements)
     int xs_bytes;             // smem bytes of the X staging area (16-aligned)
     int stages;               // per-warp TMA ring depth (<= 8)
+    int debug;                // profiling only: 1 = skip decode, 2 = skip weight loads
 };
 
 constexpr int kMaxWarps = 16;
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     };
     // Weights do not depend on the previous kernel: fill the ring before
     // waiting on the programmatic dependency (X, workspace, Y).
-    if (lane == 0)
+    if (lane == 0 && !(p.debug & 2))
         for (int i = 0; i < D && i < total; ++i) issue(i, i);
     pdl_launch_dependents();
     pdl_wait();
@@ -188,10 +189,15 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             uint32_t T[NPL];
 #pragma unroll
             for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
-            uint32_t S[R];
-            slice_loaded<R, CHILD>(T, S);
             uint32_t A[16];
-            decode_word<R>(S, A);
+            if (p.debug & 1) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) A[q] = T[q % NPL] & 0x3F3F3F3Fu;
+            } else {
+                uint32_t S[R];
+                slice_loaded<R, CHILD>(T, S);
+                decode_word<R>(S, A);
+            }
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 uint32_t bf[NT][4];
@@ -342,7 +348,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             }
         }
         const int stage = f % D;
-        mbar_wait(my_bar0 + 8 * stage, (uint32_t)((f / D) & 1));
+        if (!(p.debug & 2)) mbar_wait(my_bar0 + 8 * stage, (uint32_t)((f / D) & 1));
         const uint32_t src = my_ring0 + stage * kStageBytes;
         uint4 buf[NPL];
 #pragma unroll
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             sc[3] = lds32f(src + NPL * kSlab + (24 + g) * 4);
         }
         __syncwarp();
-        if (lane == 0 && f + D < total) {
+        if (lane == 0 && f + D < total && !(p.debug & 2)) {
             fence_proxy_async_smem();
             issue(f + D, stage);
         }
