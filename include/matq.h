@@ -12,7 +12,7 @@
  *     libmatq never allocates or frees (as the reference C core never does,
  *     _core.pyx:42-45 allocates on the Python side).
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
- *     stream).  Hot-path calls (mq_gemv, mq_pack_planes, mq_tile_scales,
+ *     stream).  Hot-path calls (mq_gemv, mq_pack_blob,
  *     mq_slice, mq_dequant, mq_materialize_child) are asynchronous, do no
  *     host synchronisation and no allocation, and are CUDA-graph capturable.
  *     The format helpers that validate data (mq_slice_elementwise,
@@ -23,10 +23,16 @@
  *     texts, matmul.py:106-109, slicing.py:58-64, which the Python layer
  *     keeps verbatim).
  *
- * Device parent layout "P8": planes uint32[8][Np/16][Kp/256][32][4],
- * plane 0 = code MSB; tiled scales fp32[Np/16][ngp][16]; Np = ceil16(N),
- * Kp = ceil256(K), ngp = ceil(Kp / G).  A child ("mode C") has the same
- * layout with r planes holding the sliced r-bit code, MSB first.
+ * Device layout: a "blob" of uint32 blocks, one per (16-row
+ * tile rt, 256-column step st), each = [scale block][plane 0 slab]...[plane
+ * P-1 slab]; a slab is 32 lanes x 4 words = 512 B, plane 0 = code MSB, and the
+ * scale block holds the fp32 group scales of the step (spg = 256/G groups x 16
+ * rows for G in {32,64,128}; 1 group for G a multiple of 256; none otherwise).
+ * A parent has P = nbits planes (8 for the int8 parent); an r-bit child
+ * ("mode C") has P = r.  Slice r of a parent reads the first scale block +
+ * (r+1) slabs of every block -- one contiguous bulk copy per step.
+ * Np = ceil16(N), Kp = ceil256(K).  For G != 128 a tiled scale array
+ * tscales fp32[Np/16][ceil(Kp/G)][16] accompanies the blob.
  */
 #ifndef MATQ_H
 #define MATQ_H
@@ -51,7 +57,7 @@ extern "C" {
 #define MQ_ERR_CUDA 4       /* CUDA runtime error (see mq_last_error)            */
 
 /* mq_gemv flags */
-#define MQ_CHILD 1 /* planes are an r-plane child (mode C); else the 8-plane parent (mode P) */
+#define MQ_CHILD 1 /* informational: mode C is implied by nplanes == r */
 #define MQ_X_F32 2 /* X is fp32 [B][ldx] (split on device into bf16 hi + lo terms); else bf16 */
 #define MQ_Y_F32 4 /* Y is fp32 [B][ldy]; else bf16 */
 #define MQ_PDL 8   /* programmatic dependent launch (overlap with the previous kernel) */
@@ -64,39 +70,38 @@ MQ_API const char* mq_last_error(void);
 
 /* Layout sizes (host-side, no CUDA calls). */
 MQ_API int mq_layout_dims(int N, int K, int G, int* Np, int* Kp, int* ngp);
-MQ_API size_t mq_planes_bytes(int N, int K, int nplanes);
+MQ_API size_t mq_blob_bytes(int N, int K, int G, int nplanes);
 MQ_API size_t mq_tscales_bytes(int N, int K, int G);
 
 /* K1: codes (N, K) uint8 with `nbits` significant bits (8 for the int8
- * parent, r for a child) -> MSB-first bit planes in the P8 layout.  Replaces
- * the reference's child packer pack() (packing.py:81-110) and the raw-byte
- * parent storage (checkpoint.py:66-75) with one device layout. */
-MQ_API int mq_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits,
-                   uint32_t* planes, void* stream);
+ * parent, r for a child) + group scales (N, ceil(K/G)) fp32 row-major
+ * (QuantGrid.scales, grid.py:293) -> blob (+ tscales, required when
+ * G != 128).  Replaces the reference's child packer pack() (packing.py:81-110)
+ * and its raw-byte parent storage (checkpoint.py:66-75) with one device
+ * layout. */
+MQ_API int mq_pack_blob(const uint8_t* codes, long long ldc, int N, int K, int nbits,
+                        const float* scales, int G, uint32_t* blob, float* tscales, void* stream);
 
-/* Group scales (N, ceil(K/G)) fp32 row-major (QuantGrid.scales, grid.py:293)
- * -> tiled scales. */
-MQ_API int mq_tile_scales(const float* scales, int N, int K, int G, float* tscales, void* stream);
-
-/* K2a: r-bit sliced codes (N, K) uint8 from planes, with the bitsliced
- * slice the GEMV uses.  Replaces slice_to_code over a layer
- * (slicing.py:87-90, slice_layer :158-171).  child=1: planes already hold r
- * planes. */
-MQ_API int mq_slice(const uint32_t* planes, int N, int K, int r, int child, uint8_t* codes_out,
-             long long ldo, void* stream);
+/* K2a: r-bit sliced codes (N, K) uint8 from a blob of `nplanes` planes, with
+ * the bitsliced slice the GEMV uses (nplanes == r: the blob is a child).
+ * Replaces slice_to_code over a layer (slicing.py:87-90, slice_layer
+ * :158-171). */
+MQ_API int mq_slice(const uint32_t* blob, int N, int K, int G, int nplanes, int r,
+                    uint8_t* codes_out, long long ldo, void* stream);
 
 /* K2b: decode through the exact GEMV register path.  vals_out (optional):
- * int8 s - 2^(r-1); w_out (optional): fp32 (s - z) * tscale * out_scale,
- * i.e. PackedLayer.dense_f32 (matmul.py:232-237) when out_scale = 2^(8-r). */
-MQ_API int mq_dequant(const uint32_t* planes, const float* tscales, int N, int K, int G, int r,
-               int child, float out_scale, int8_t* vals_out, float* w_out, long long ldw,
-               void* stream);
+ * int8 s - 2^(r-1); w_out (optional): fp32 (s - z) * scale * out_scale, i.e.
+ * PackedLayer.dense_f32 (matmul.py:232-237) when out_scale = 2^(c-r). */
+MQ_API int mq_dequant(const uint32_t* blob, const float* tscales, int N, int K, int G, int nplanes,
+                      int r, float out_scale, int8_t* vals_out, float* w_out, long long ldw,
+                      void* stream);
 
-/* K2c: materialise an r-plane child (mode C) from the parent planes. */
-MQ_API int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uint32_t* child,
-                         void* stream);
+/* K2c: materialise an r-plane child (mode C) from an 8-plane parent blob;
+ * the child keeps the parent's master scales (use out_scale = 2^(8-r)). */
+MQ_API int mq_materialize_child(const uint32_t* blob, int N, int K, int G, int r, uint32_t* child,
+                                void* stream);
 
-/* K3: Y = X @ dequant(slice_r(planes)).T, fp32 accumulation.
+/* K3: Y = X @ dequant(slice_r(blob)).T, fp32 accumulation.
  * Replaces _core.packed_matmul (_core.pyx:24-64) -> nq_group_lane_sums /
  * nq_gemv / nq_gemm (packed_kernels.h:17-27), for r in {2,3,4,6,8} and
  * 1 <= B <= 32 (B <= 16 with MQ_X_F32).  X (B, K) with row stride ldx,
@@ -108,9 +113,9 @@ MQ_API int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uin
  * are split-K tickets that every call leaves at zero, so one workspace (sized
  * for the largest layer) serves any sequence of GEMVs on one stream. */
 MQ_API size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags);
-MQ_API int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y,
-            int ldy, int B, int N, int K, int G, int r, float out_scale, int flags,
-            void* workspace, size_t workspace_bytes, void* stream);
+MQ_API int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, void* Y,
+                   int ldy, int B, int N, int K, int G, int nplanes, int r, float out_scale,
+                   int flags, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- format-layer helpers behind the drop-in Python API --------------- */
 

@@ -45,15 +45,14 @@ _SIGS = {
     "mq_version": ([], ctypes.c_char_p),
     "mq_last_error": ([], ctypes.c_char_p),
     "mq_layout_dims": ([_i, _i, _i, _vp, _vp, _vp], _i),
-    "mq_planes_bytes": ([_i, _i, _i], _sz),
+    "mq_blob_bytes": ([_i, _i, _i, _i], _sz),
     "mq_tscales_bytes": ([_i, _i, _i], _sz),
-    "mq_pack_planes": ([_vp, _ll, _i, _i, _i, _vp, _vp], _i),
-    "mq_tile_scales": ([_vp, _i, _i, _i, _vp, _vp], _i),
-    "mq_slice": ([_vp, _i, _i, _i, _i, _vp, _ll, _vp], _i),
+    "mq_pack_blob": ([_vp, _ll, _i, _i, _i, _vp, _i, _vp, _vp, _vp], _i),
+    "mq_slice": ([_vp, _i, _i, _i, _i, _i, _vp, _ll, _vp], _i),
     "mq_dequant": ([_vp, _vp, _i, _i, _i, _i, _i, _f, _vp, _vp, _ll, _vp], _i),
-    "mq_materialize_child": ([_vp, _i, _i, _i, _vp, _vp], _i),
+    "mq_materialize_child": ([_vp, _i, _i, _i, _i, _vp, _vp], _i),
     "mq_gemv_workspace_bytes": ([_i, _i, _i, _i], _sz),
-    "mq_gemv": ([_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
+    "mq_gemv": ([_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
     "mq_slice_elementwise": ([_vp, _ll, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_f64": ([_vp, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_value_f64": ([_vp, _vp, _ll, _i, _i, _vp, _vp, _vp], _i),

@@ -80,7 +80,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
         if (xs > kXsMax && cs > 1) continue;
         int cpc = sms / S;
         if (cpc < 1) break;
-        cpc = std::min(cpc, mq::cdiv(n_rt, c.nwarps));
+        cpc = std::min(cpc, n_rt);  // at least one row tile per CTA
         const int units_per_warp = mq::cdiv(n_rt, cpc * c.nwarps);
         const double cost = (double)units_per_warp * (cs + (S > 1 ? fixup : 0.0));
         if (cost < best - 1e-9) {
@@ -140,9 +140,9 @@ int mq_layout_dims(int N, int K, int G, int* Np, int* Kp, int* ngp) {
     return MQ_OK;
 }
 
-size_t mq_planes_bytes(int N, int K, int nplanes) {
-    if (N < 1 || K < 1 || nplanes < 1) return 0;
-    return (size_t)nplanes * mq::pad16(N) * (size_t)mq::pad256(K) / 8;
+size_t mq_blob_bytes(int N, int K, int G, int nplanes) {
+    if (N < 1 || K < 1 || G < 1 || nplanes < 1 || nplanes > 8) return 0;
+    return (size_t)mq::Layout::make(N, K, G, nplanes).total_words() * 4;
 }
 
 size_t mq_tscales_bytes(int N, int K, int G) {
@@ -150,50 +150,64 @@ size_t mq_tscales_bytes(int N, int K, int G) {
     return (size_t)mq::pad16(N) * mq::cdiv(mq::pad256(K), G) * sizeof(float);
 }
 
-int mq_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits, uint32_t* planes,
-                   void* stream) {
-    if (!codes || !planes) return fail(MQ_ERR_INVALID, "null pointer");
+static bool valid_group(int G) { return G >= 32 && G % 32 == 0; }
+
+int mq_pack_blob(const uint8_t* codes, long long ldc, int N, int K, int nbits, const float* scales,
+                 int G, uint32_t* blob, float* tscales, void* stream) {
+    if (!codes || !blob || !scales) return fail(MQ_ERR_INVALID, "null pointer");
     if (N < 1 || K < 1 || ldc < K) return fail(MQ_ERR_INVALID, "bad shape N=%d K=%d ldc=%lld", N, K, ldc);
     if (nbits < 2 || nbits > 8) return fail(MQ_ERR_INVALID, "nbits must lie in [2, 8]");
-    return cuda_status(mq::launch_pack_planes(codes, ldc, N, K, nbits, planes, (cudaStream_t)stream),
-                       "mq_pack_planes");
+    if (!valid_group(G)) return fail(MQ_ERR_INVALID, "group size must be a multiple of 32");
+    if (G != 128 && !tscales) return fail(MQ_ERR_INVALID, "tscales required when G != 128");
+    const mq::Layout L = mq::Layout::make(N, K, G, nbits);
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = mq::launch_pack_planes(codes, ldc, L, nbits, blob, s);
+    if (e == cudaSuccess) e = mq::launch_pack_scales(scales, L, mq::cdiv(K, G), blob, tscales, s);
+    return cuda_status(e, "mq_pack_blob");
 }
 
-int mq_tile_scales(const float* scales, int N, int K, int G, float* tscales, void* stream) {
-    if (!scales || !tscales) return fail(MQ_ERR_INVALID, "null pointer");
-    if (N < 1 || K < 1 || G < 1) return fail(MQ_ERR_INVALID, "bad shape");
-    const int ng = mq::cdiv(K, G), ngp = mq::cdiv(mq::pad256(K), G);
-    return cuda_status(mq::launch_tile_scales(scales, N, ng, ngp, tscales, (cudaStream_t)stream),
-                       "mq_tile_scales");
-}
-
-int mq_slice(const uint32_t* planes, int N, int K, int r, int child, uint8_t* codes_out,
-             long long ldo, void* stream) {
-    if (!planes || !codes_out) return fail(MQ_ERR_INVALID, "null pointer");
+static int check_slice(const uint32_t* blob, int N, int K, int G, int nplanes, int r) {
+    if (!blob) return fail(MQ_ERR_INVALID, "null pointer");
     if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
-    if (N < 1 || K < 1 || ldo < K) return fail(MQ_ERR_INVALID, "bad shape");
-    return cuda_status(mq::launch_slice_codes(r, child != 0, planes, N, K, codes_out, ldo,
+    if (N < 1 || K < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    if (!valid_group(G)) return fail(MQ_ERR_INVALID, "group size must be a multiple of 32");
+    if (nplanes < r || nplanes > 8) return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d", r, nplanes);
+    if (nplanes != r && nplanes < r + 1) return fail(MQ_ERR_INVALID, "need %d planes", r + 1);
+    return MQ_OK;
+}
+
+int mq_slice(const uint32_t* blob, int N, int K, int G, int nplanes, int r, uint8_t* codes_out,
+             long long ldo, void* stream) {
+    int st = check_slice(blob, N, K, G, nplanes, r);
+    if (st) return st;
+    if (!codes_out || ldo < K) return fail(MQ_ERR_INVALID, "bad output");
+    const mq::Layout L = mq::Layout::make(N, K, G, nplanes);
+    return cuda_status(mq::launch_slice_codes(r, nplanes == r, blob, L, codes_out, ldo,
                                               (cudaStream_t)stream),
                        "mq_slice");
 }
 
-int mq_dequant(const uint32_t* planes, const float* tscales, int N, int K, int G, int r, int child,
+int mq_dequant(const uint32_t* blob, const float* tscales, int N, int K, int G, int nplanes, int r,
                float out_scale, int8_t* vals_out, float* w_out, long long ldw, void* stream) {
-    if (!planes || (!vals_out && !w_out)) return fail(MQ_ERR_INVALID, "null pointer");
-    if (w_out && !tscales) return fail(MQ_ERR_INVALID, "w_out needs tscales");
-    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
-    if (N < 1 || K < 1 || ldw < K || G < 1) return fail(MQ_ERR_INVALID, "bad shape");
-    return cuda_status(mq::launch_decode_dense(r, child != 0, planes, tscales, G, out_scale, N, K,
-                                               vals_out, w_out, ldw, (cudaStream_t)stream),
+    int st = check_slice(blob, N, K, G, nplanes, r);
+    if (st) return st;
+    if (!vals_out && !w_out) return fail(MQ_ERR_INVALID, "null pointer");
+    const mq::Layout L = mq::Layout::make(N, K, G, nplanes);
+    if (w_out && L.spg == 0 && !tscales) return fail(MQ_ERR_INVALID, "w_out needs tscales");
+    if (ldw < K) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_decode_dense(r, nplanes == r, blob, tscales, L, out_scale, vals_out,
+                                               w_out, ldw, (cudaStream_t)stream),
                        "mq_dequant");
 }
 
-int mq_materialize_child(const uint32_t* planes, int N, int K, int r, uint32_t* child,
+int mq_materialize_child(const uint32_t* blob, int N, int K, int G, int r, uint32_t* child,
                          void* stream) {
-    if (!planes || !child) return fail(MQ_ERR_INVALID, "null pointer");
-    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
-    if (N < 1 || K < 1) return fail(MQ_ERR_INVALID, "bad shape");
-    return cuda_status(mq::launch_materialize_child(r, planes, N, K, child, (cudaStream_t)stream),
+    int st = check_slice(blob, N, K, G, 8, r);
+    if (st) return st;
+    if (!child) return fail(MQ_ERR_INVALID, "null pointer");
+    if (r == 8) return fail(MQ_ERR_INVALID, "an 8-bit child is the parent");
+    const mq::Layout L = mq::Layout::make(N, K, G, 8);
+    return cuda_status(mq::launch_materialize_child(r, blob, L, child, (cudaStream_t)stream),
                        "mq_materialize_child");
 }
 
@@ -204,10 +218,13 @@ size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
     return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, 8, true), B);
 }
 
-int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx, void* Y, int ldy,
-            int B, int N, int K, int G, int r, float out_scale, int flags, void* workspace,
-            size_t workspace_bytes, void* stream) {
-    if (!planes || !tscales || !X || !Y) return fail(MQ_ERR_INVALID, "null pointer");
+int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, void* Y, int ldy,
+            int B, int N, int K, int G, int nplanes, int r, float out_scale, int flags,
+            void* workspace, size_t workspace_bytes, void* stream) {
+    if (!blob || !X || !Y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (G != 128 && !tscales) return fail(MQ_ERR_INVALID, "tscales required when G != 128");
+    if (nplanes < r || nplanes > 8 || (nplanes != r && nplanes < r + 1))
+        return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", r, nplanes);
     if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
     if (G < 32 || G % 32 != 0) return fail(MQ_ERR_INVALID, "group size must be a multiple of 32");
     if (N < 1 || K < 1 || B < 1) return fail(MQ_ERR_INVALID, "bad shape B=%d N=%d K=%d", B, N, K);
@@ -216,16 +233,18 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     const int Bx = xf32 ? 2 * B : B;
     if (Bx > 32) return fail(MQ_ERR_INVALID, "batch %d above the GEMV limit (32 rows, 16 with fp32 X)", B);
 
-    const bool child_mode = (flags & MQ_CHILD) != 0;
+    const bool child_mode = nplanes == r;
     const int npl = (child_mode || r == 8) ? r : r + 1;
     const GemvConfig c = choose_gemv_config(N, K, Bx, npl, G == 128);
     const size_t need = gemv_ws_bytes(N, c, B);
     if (need > workspace_bytes || (need && !workspace))
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
 
+    const mq::Layout L = mq::Layout::make(N, K, G, nplanes);
     mq::GemvParams p{};
-    p.planes = planes;
-    p.plane_stride = (long long)(mq::pad16(N) / 16) * (mq::pad256(K) / 256) * 128;
+    p.blob = blob;
+    p.step_words = L.step_words;
+    p.sb_words = 16 * L.spg;
     p.tscales = tscales;
     p.X = X;
     p.Y = Y;
@@ -256,10 +275,9 @@ int mq_gemv(const uint32_t* planes, const float* tscales, const void* X, int ldx
     p.xs_stride = c.xs_stride;
     p.xs_bytes = c.xs_bytes;
     p.stages = c.stages;
-    p.debug = env_int("MQ_GEMV_DEBUG", 0);
     const dim3 grid(c.grid, 1, 1), block(32 * c.nwarps, 1, 1);
     const int gs = (G == 128) ? 128 : 0;
-    const cudaError_t e = gemv_launcher(r)(p, c.NT, (flags & MQ_CHILD) != 0, gs, grid, block, c.smem,
+    const cudaError_t e = gemv_launcher(r)(p, c.NT, child_mode, gs, grid, block, c.smem,
                                            (cudaStream_t)stream, (flags & MQ_PDL) != 0);
     return cuda_status(e, "mq_gemv");
 }

@@ -7,74 +7,100 @@
 #include "matq_common.cuh"
 #include "matq_internal.h"
 
+#include <algorithm>
+
 namespace mq {
 
 // ---------------------------------------------------------------------------
-// K1: codes (N, K) uint8 with `nbits` significant bits -> MSB-first planes.
-// One thread per (row tile, step, lane, word); each writes nbits words.
-__global__ void k_pack_planes(const uint8_t* __restrict__ codes, long long ldc, int N, int K,
-                              int nbits, uint32_t* __restrict__ planes, long long plane_stride,
-                              int n_rt, int nsteps) {
-    const long long total = (long long)n_rt * nsteps * 128;
+// K1: codes (N, K) uint8 with `nbits` significant bits -> MSB-first planes in
+// the step-interleaved blob.  One thread per (row tile, step, lane, word).
+__global__ void k_pack_planes(const uint8_t* __restrict__ codes, long long ldc, Layout L, int nbits,
+                              uint32_t* __restrict__ blob) {
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
         const long long blk = idx >> 7;
-        const int st = (int)(blk % nsteps), rt = (int)(blk / nsteps);
+        const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
         uint32_t words[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
         for (int bit = 0; bit < 32; ++bit) {
             int ro, co;
             word_bit_pos(lane, w, bit, ro, co);
             const int row = rt * kTileRows + ro, col = st * kStepCols + co;
-            const uint32_t q = (row < N && col < K) ? codes[(long long)row * ldc + col] : 0u;
+            const uint32_t q = (row < L.N && col < L.K) ? codes[(long long)row * ldc + col] : 0u;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (j < nbits) words[j] |= ((q >> (nbits - 1 - j)) & 1u) << bit;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-            if (j < nbits) planes[j * plane_stride + idx] = words[j];
+            if (j < nbits) blob[L.plane_word(rt, st, j, lane, w)] = words[j];
     }
 }
 
-// scales (N, ng) row-major (QuantGrid.scales, grid.py:293) -> tiled
-// [Np/16][ngp][16]; padding entries are 0 (their activations are 0 too).
-__global__ void k_tile_scales(const float* __restrict__ scales, int N, int ng, int ngp, int Np,
-                              float* __restrict__ ts) {
-    const long long total = (long long)Np * ngp;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int r16 = (int)(idx & 15);
-        const long long rest = idx >> 4;
-        const int grp = (int)(rest % ngp), rt = (int)(rest / ngp);
-        const int row = rt * 16 + r16;
-        ts[idx] = (row < N && grp < ng) ? scales[(long long)row * ng + grp] : 0.0f;
+// Group scales (N, ng) row-major (QuantGrid.scales, grid.py:293) -> the
+// blob's per-step scale blocks (spg > 0) and/or the tiled array
+// [Np/16][ngp][16] (generic group sizes).  Padding entries are 0.
+__global__ void k_pack_scales(const float* __restrict__ scales, Layout L, int ng,
+                              uint32_t* __restrict__ blob, float* __restrict__ ts) {
+    if (blob && L.spg > 0) {
+        const long long total = (long long)L.n_rt * L.nsteps * L.spg * 16;
+        for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+             idx += (long long)gridDim.x * blockDim.x) {
+            const int r16 = (int)(idx & 15);
+            const long long rest = idx >> 4;
+            const int gi = (int)(rest % L.spg);
+            const long long blk = rest / L.spg;
+            const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
+            const int row = rt * 16 + r16;
+            const int grp = (st * kStepCols + gi * min(L.G, kStepCols)) / L.G;
+            const float v = (row < L.N && grp < ng) ? scales[(long long)row * ng + grp] : 0.0f;
+            blob[L.block(rt, st) + gi * 16 + r16] = __float_as_uint(v);
+        }
     }
+    if (ts) {
+        const long long total = (long long)L.Np * L.ngp;
+        for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+             idx += (long long)gridDim.x * blockDim.x) {
+            const int r16 = (int)(idx & 15);
+            const long long rest = idx >> 4;
+            const int grp = (int)(rest % L.ngp), rt = (int)(rest / L.ngp);
+            const int row = rt * 16 + r16;
+            ts[idx] = (row < L.N && grp < ng) ? scales[(long long)row * ng + grp] : 0.0f;
+        }
+    }
+}
+
+__device__ __forceinline__ float layout_scale(const Layout& L, const uint32_t* blob, const float* ts,
+                                              int rt, int st, int r16, int col_in_step) {
+    if (L.spg > 0) return __uint_as_float(blob[L.scale_word(rt, st, r16, col_in_step)]);
+    const int grp = (st * kStepCols + col_in_step) / L.G;
+    return ts[((long long)rt * L.ngp + grp) * 16 + r16];
 }
 
 // ---------------------------------------------------------------------------
-// K2a: planes -> r-bit sliced codes (N, K) via the bitsliced slice K3 uses.
+// K2a: blob -> r-bit sliced codes (N, K) via the bitsliced slice K3 uses.
 template <int R, bool CHILD>
-__global__ void k_slice_codes(const uint32_t* __restrict__ planes, long long plane_stride, int N,
-                              int K, int n_rt, int nsteps, uint8_t* __restrict__ out, long long ldo) {
+__global__ void k_slice_codes(const uint32_t* __restrict__ blob, Layout L, uint8_t* __restrict__ out,
+                              long long ldo) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
-    const long long total = (long long)n_rt * nsteps * 128;
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
         const long long blk = idx >> 7;
-        const int st = (int)(blk % nsteps), rt = (int)(blk / nsteps);
+        const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
         uint32_t T[NPL];
 #pragma unroll
-        for (int j = 0; j < NPL; ++j) T[j] = planes[j * plane_stride + idx];
+        for (int j = 0; j < NPL; ++j) T[j] = blob[L.plane_word(rt, st, j, lane, w)];
         uint32_t S[R];
         slice_loaded<R, CHILD>(T, S);
         for (int bit = 0; bit < 32; ++bit) {
             int ro, co;
             word_bit_pos(lane, w, bit, ro, co);
             const int row = rt * kTileRows + ro, col = st * kStepCols + co;
-            if (row >= N || col >= K) continue;
+            if (row >= L.N || col >= L.K) continue;
             uint32_t q = 0;
 #pragma unroll
             for (int j = 0; j < R; ++j) q |= ((S[j] >> bit) & 1u) << (R - 1 - j);
@@ -83,26 +109,25 @@ __global__ void k_slice_codes(const uint32_t* __restrict__ planes, long long pla
     }
 }
 
-// K2b: planes -> dequantised weights through the exact K3 decode path
+// K2b: blob -> dequantised weights through the exact K3 decode path
 // (bitsliced slice + transpose network + bf16 magic conversion).
 //   vals (int8, optional): s - 2^(r-1) as decoded in bf16 registers
 //   W (fp32, optional): (s - z) * (scale * out_scale), one fp32 rounding --
 //   the same arithmetic as PackedLayer.dense_f32 (matmul.py:232-237).
 template <int R, bool CHILD>
-__global__ void k_decode_dense(const uint32_t* __restrict__ planes, long long plane_stride,
-                               const float* __restrict__ tscales, int ngp, int G, float out_scale,
-                               int N, int K, int n_rt, int nsteps, int8_t* __restrict__ vals,
+__global__ void k_decode_dense(const uint32_t* __restrict__ blob, const float* __restrict__ ts,
+                               Layout L, float out_scale, int8_t* __restrict__ vals,
                                float* __restrict__ W, long long ldw) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
-    const long long total = (long long)n_rt * nsteps * 128;
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
         const long long blk = idx >> 7;
-        const int st = (int)(blk % nsteps), rt = (int)(blk / nsteps);
+        const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
         uint32_t T[NPL];
 #pragma unroll
-        for (int j = 0; j < NPL; ++j) T[j] = planes[j * plane_stride + idx];
+        for (int j = 0; j < NPL; ++j) T[j] = blob[L.plane_word(rt, st, j, lane, w)];
         uint32_t S[R];
         slice_loaded<R, CHILD>(T, S);
         uint32_t A[16];
@@ -114,33 +139,36 @@ __global__ void k_decode_dense(const uint32_t* __restrict__ planes, long long pl
                 int ro, co;
                 word_bit_pos(lane, w, p + 16 * h, ro, co);
                 const int row = rt * kTileRows + ro, col = st * kStepCols + co;
-                if (row >= N || col >= K) continue;
+                if (row >= L.N || col >= L.K) continue;
                 const float v = bf16_to_f32((uint16_t)(A[p] >> (16 * h)));
                 if (vals) vals[(long long)row * ldw + col] = (int8_t)v;
-                if (W) {
-                    const float sc = tscales[((long long)rt * ngp + col / G) * 16 + ro] * out_scale;
-                    W[(long long)row * ldw + col] = v * sc;
-                }
+                if (W) W[(long long)row * ldw + col] = v * (layout_scale(L, blob, ts, rt, st, ro, co) * out_scale);
             }
         }
     }
 }
 
-// K2c: mode C child materialisation: parent planes -> r sliced planes.
+// K2c: mode C child materialisation: parent blob -> r-plane child blob
+// (scale blocks copied, planes sliced).
 template <int R>
-__global__ void k_materialize_child(const uint32_t* __restrict__ planes, long long plane_stride,
-                                    long long nwords, uint32_t* __restrict__ child,
-                                    long long child_stride) {
+__global__ void k_materialize_child(const uint32_t* __restrict__ blob, Layout Lp, Layout Lc,
+                                    uint32_t* __restrict__ child) {
+    const long long nwords = (long long)Lp.n_rt * Lp.nsteps * 128;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < nwords;
          idx += (long long)gridDim.x * blockDim.x) {
+        const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
+        const long long blk = idx >> 7;
+        const int st = (int)(blk % Lp.nsteps), rt = (int)(blk / Lp.nsteps);
         constexpr int NPL = PlaneCount<R, false>::value;
         uint32_t T[NPL];
 #pragma unroll
-        for (int j = 0; j < NPL; ++j) T[j] = planes[j * plane_stride + idx];
+        for (int j = 0; j < NPL; ++j) T[j] = blob[Lp.plane_word(rt, st, j, lane, w)];
         uint32_t S[R];
         slice_loaded<R, false>(T, S);
 #pragma unroll
-        for (int j = 0; j < R; ++j) child[j * child_stride + idx] = S[j];
+        for (int j = 0; j < R; ++j) child[Lc.plane_word(rt, st, j, lane, w)] = S[j];
+        if (lane * 4 + w < 16 * Lp.spg)  // copy the step's scale block
+            child[Lc.block(rt, st) + lane * 4 + w] = blob[Lp.block(rt, st) + lane * 4 + w];
     }
 }
 
@@ -267,54 +295,46 @@ static inline int grid_for(long long n, int block = 256) {
     return (int)g;
 }
 
-cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits,
-                               uint32_t* planes, cudaStream_t s) {
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long total = (long long)n_rt * nsteps * 128;
-    k_pack_planes<<<grid_for(total), 256, 0, s>>>(codes, ldc, N, K, nbits, planes, total, n_rt,
-                                                  nsteps);
+cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, const Layout& L, int nbits,
+                               uint32_t* blob, cudaStream_t s) {
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
+    k_pack_planes<<<grid_for(total), 256, 0, s>>>(codes, ldc, L, nbits, blob);
     return cudaGetLastError();
 }
 
-cudaError_t launch_tile_scales(const float* scales, int N, int ng, int ngp, float* ts,
+cudaError_t launch_pack_scales(const float* scales, const Layout& L, int ng, uint32_t* blob, float* ts,
                                cudaStream_t s) {
-    const int Np = pad16(N);
-    k_tile_scales<<<grid_for((long long)Np * ngp), 256, 0, s>>>(scales, N, ng, ngp, Np, ts);
+    const long long total = std::max((long long)L.n_rt * L.nsteps * L.spg * 16, (long long)L.Np * L.ngp);
+    k_pack_scales<<<grid_for(total), 256, 0, s>>>(scales, L, ng, blob, ts);
     return cudaGetLastError();
 }
 
 template <bool CHILD>
-static cudaError_t slice_codes_dispatch(int r, const uint32_t* planes, long long ps, int N, int K,
-                                        int n_rt, int nsteps, uint8_t* out, long long ldo,
-                                        cudaStream_t s) {
-    const long long total = (long long)n_rt * nsteps * 128;
-    const int gr = grid_for(total);
+static cudaError_t slice_codes_dispatch(int r, const uint32_t* blob, const Layout& L, uint8_t* out,
+                                        long long ldo, cudaStream_t s) {
+    const int gr = grid_for((long long)L.n_rt * L.nsteps * 128);
     switch (r) {
-        case 2: k_slice_codes<2, CHILD><<<gr, 256, 0, s>>>(planes, ps, N, K, n_rt, nsteps, out, ldo); break;
-        case 3: k_slice_codes<3, CHILD><<<gr, 256, 0, s>>>(planes, ps, N, K, n_rt, nsteps, out, ldo); break;
-        case 4: k_slice_codes<4, CHILD><<<gr, 256, 0, s>>>(planes, ps, N, K, n_rt, nsteps, out, ldo); break;
-        case 6: k_slice_codes<6, CHILD><<<gr, 256, 0, s>>>(planes, ps, N, K, n_rt, nsteps, out, ldo); break;
-        case 8: k_slice_codes<8, CHILD><<<gr, 256, 0, s>>>(planes, ps, N, K, n_rt, nsteps, out, ldo); break;
+        case 2: k_slice_codes<2, CHILD><<<gr, 256, 0, s>>>(blob, L, out, ldo); break;
+        case 3: k_slice_codes<3, CHILD><<<gr, 256, 0, s>>>(blob, L, out, ldo); break;
+        case 4: k_slice_codes<4, CHILD><<<gr, 256, 0, s>>>(blob, L, out, ldo); break;
+        case 6: k_slice_codes<6, CHILD><<<gr, 256, 0, s>>>(blob, L, out, ldo); break;
+        case 8: k_slice_codes<8, CHILD><<<gr, 256, 0, s>>>(blob, L, out, ldo); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_slice_codes(int r, bool child, const uint32_t* planes, int N, int K,
-                               uint8_t* out, long long ldo, cudaStream_t s) {
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long ps = (long long)n_rt * nsteps * 128;
-    return child ? slice_codes_dispatch<true>(r, planes, ps, N, K, n_rt, nsteps, out, ldo, s)
-                 : slice_codes_dispatch<false>(r, planes, ps, N, K, n_rt, nsteps, out, ldo, s);
+cudaError_t launch_slice_codes(int r, bool child, const uint32_t* blob, const Layout& L, uint8_t* out,
+                               long long ldo, cudaStream_t s) {
+    return child ? slice_codes_dispatch<true>(r, blob, L, out, ldo, s)
+                 : slice_codes_dispatch<false>(r, blob, L, out, ldo, s);
 }
 
 template <bool CHILD>
-static cudaError_t decode_dispatch(int r, const uint32_t* planes, long long ps, const float* ts,
-                                   int ngp, int G, float os, int N, int K, int n_rt, int nsteps,
-                                   int8_t* vals, float* W, long long ldw, cudaStream_t s) {
-    const long long total = (long long)n_rt * nsteps * 128;
-    const int gr = grid_for(total);
-#define MQ_DD(R_) k_decode_dense<R_, CHILD><<<gr, 256, 0, s>>>(planes, ps, ts, ngp, G, os, N, K, n_rt, nsteps, vals, W, ldw)
+static cudaError_t decode_dispatch(int r, const uint32_t* blob, const float* ts, const Layout& L,
+                                   float os, int8_t* vals, float* W, long long ldw, cudaStream_t s) {
+    const int gr = grid_for((long long)L.n_rt * L.nsteps * 128);
+#define MQ_DD(R_) k_decode_dense<R_, CHILD><<<gr, 256, 0, s>>>(blob, ts, L, os, vals, W, ldw)
     switch (r) {
         case 2: MQ_DD(2); break;
         case 3: MQ_DD(3); break;
@@ -327,29 +347,22 @@ static cudaError_t decode_dispatch(int r, const uint32_t* planes, long long ps, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_decode_dense(int r, bool child, const uint32_t* planes, const float* ts, int G,
-                                float out_scale, int N, int K, int8_t* vals, float* W,
+cudaError_t launch_decode_dense(int r, bool child, const uint32_t* blob, const float* ts,
+                                const Layout& L, float out_scale, int8_t* vals, float* W,
                                 long long ldw, cudaStream_t s) {
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long ps = (long long)n_rt * nsteps * 128;
-    const int ngp = cdiv(pad256(K), G);
-    return child ? decode_dispatch<true>(r, planes, ps, ts, ngp, G, out_scale, N, K, n_rt, nsteps,
-                                         vals, W, ldw, s)
-                 : decode_dispatch<false>(r, planes, ps, ts, ngp, G, out_scale, N, K, n_rt, nsteps,
-                                          vals, W, ldw, s);
+    return child ? decode_dispatch<true>(r, blob, ts, L, out_scale, vals, W, ldw, s)
+                 : decode_dispatch<false>(r, blob, ts, L, out_scale, vals, W, ldw, s);
 }
 
-cudaError_t launch_materialize_child(int r, const uint32_t* planes, int N, int K, uint32_t* child,
+cudaError_t launch_materialize_child(int r, const uint32_t* blob, const Layout& Lp, uint32_t* child,
                                      cudaStream_t s) {
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long nw = (long long)n_rt * nsteps * 128;
-    const int gr = grid_for(nw);
+    const Layout Lc = Layout::make(Lp.N, Lp.K, Lp.G, r);
+    const int gr = grid_for((long long)Lp.n_rt * Lp.nsteps * 128);
     switch (r) {
-        case 2: k_materialize_child<2><<<gr, 256, 0, s>>>(planes, nw, nw, child, nw); break;
-        case 3: k_materialize_child<3><<<gr, 256, 0, s>>>(planes, nw, nw, child, nw); break;
-        case 4: k_materialize_child<4><<<gr, 256, 0, s>>>(planes, nw, nw, child, nw); break;
-        case 6: k_materialize_child<6><<<gr, 256, 0, s>>>(planes, nw, nw, child, nw); break;
-        case 8: k_materialize_child<8><<<gr, 256, 0, s>>>(planes, nw, nw, child, nw); break;
+        case 2: k_materialize_child<2><<<gr, 256, 0, s>>>(blob, Lp, Lc, child); break;
+        case 3: k_materialize_child<3><<<gr, 256, 0, s>>>(blob, Lp, Lc, child); break;
+        case 4: k_materialize_child<4><<<gr, 256, 0, s>>>(blob, Lp, Lc, child); break;
+        case 6: k_materialize_child<6><<<gr, 256, 0, s>>>(blob, Lp, Lc, child); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

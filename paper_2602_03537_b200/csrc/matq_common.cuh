@@ -40,6 +40,40 @@ __host__ __device__ __forceinline__ void word_bit_pos(int lane, int w, int bit, 
     col = 64 * w + 16 * s + 8 * (q >> 1) + 2 * t + h;
 }
 
+// Step-interleaved blob layout.  For every (row tile, step):
+//   [scale block: spg groups x 16 rows fp32][plane 0 slab]...[plane P-1 slab]
+// with one slab = 32 lanes x 4 words.  A slice-r GEMV step reads the first
+// scale_words + (r+1) slabs -- one contiguous bulk copy.  spg = 256/G for
+// G in {32, 64, 128}, 1 when G is a multiple of 256 (the step's group), and
+// 0 for other group sizes (then a separate tiled scale array [Np/16][ngp][16]
+// is used).
+struct Layout {
+    int N, K, Np, Kp, n_rt, nsteps, nplanes, G, spg, ngp;
+    long long step_words;  // words per (row tile, step) block
+    __host__ __device__ static Layout make(int N, int K, int G, int nplanes) {
+        Layout L{};
+        L.N = N; L.K = K; L.G = G; L.nplanes = nplanes;
+        L.Np = pad16(N); L.Kp = pad256(K);
+        L.n_rt = L.Np / 16; L.nsteps = L.Kp / 256;
+        L.spg = (G > 0 && 256 % G == 0 && G % 32 == 0) ? 256 / G : ((G > 0 && G % 256 == 0) ? 1 : 0);
+        L.ngp = G > 0 ? cdiv(L.Kp, G) : 0;
+        L.step_words = 16LL * L.spg + 128LL * nplanes;
+        return L;
+    }
+    __host__ __device__ long long total_words() const { return (long long)n_rt * nsteps * step_words; }
+    __host__ __device__ long long block(int rt, int st) const {
+        return ((long long)rt * nsteps + st) * step_words;
+    }
+    __host__ __device__ long long plane_word(int rt, int st, int plane, int lane, int w) const {
+        return block(rt, st) + 16LL * spg + 128LL * plane + lane * 4 + w;
+    }
+    // scale of (row-in-tile r16, column col) inside the step's scale block
+    __host__ __device__ long long scale_word(int rt, int st, int r16, int col_in_step) const {
+        const int gi = spg > 1 ? col_in_step / G : 0;
+        return block(rt, st) + gi * 16 + r16;
+    }
+};
+
 // ----------------------------------------------------------------------------
 // bf16 constants (exact small dyadic values), computed at compile time.
 __host__ __device__ constexpr uint32_t bf16_bits(int num, int sh) {  // num * 2^-sh

@@ -31,9 +31,10 @@
 namespace mq {
 
 struct GemvParams {
-    const uint32_t* planes;   // P8 planes (parent) or child planes
-    long long plane_stride;   // uint32 words between consecutive planes
-    const float* tscales;     // tiled scales [Np/16][ngp][16]
+    const uint32_t* blob;     // step-interleaved blob (parent: 8 planes, child: r planes)
+    long long step_words;     // words per (row tile, step) block
+    int sb_words;             // scale-block words at the head of each block (16 * spg)
+    const float* tscales;     // tiled scales [Np/16][ngp][16] (generic G only)
     const void* X;            // bf16 [B][ldx] or fp32 [B][ldx]
     void* Y;                  // bf16 [B][ldy] or fp32 [B][ldy]
     float* ws;                // fp32 [S][B][Np] when S > 1
@@ -50,8 +51,11 @@ struct GemvParams {
     int xs_stride;            // smem X row stride (elements)
     int xs_bytes;             // smem bytes of the X staging area (16-aligned)
     int stages;               // per-warp TMA ring depth (<= 8)
-    int debug;                // profiling only: 1 = skip decode, 2 = skip weight loads
 };
+
+#ifndef MQ_GEMV_DEBUG
+#define MQ_GEMV_DEBUG 0  // profiling builds: 1 = skip decode, 2 = skip weight loads
+#endif
 
 constexpr int kMaxWarps = 16;
 
@@ -59,8 +63,8 @@ template <int R, int NT, bool CHILD, int GS>
 __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(const GemvParams p) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512;
-    constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;
-    constexpr uint32_t kStageBytes = NPL * kSlab + kScaleBytes;
+    constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;   // 2 groups x 16 rows, head of block
+    constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
 
@@ -70,7 +74,8 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     const int kc = blockIdx.x % p.S, j = blockIdx.x / p.S;
     const int chunk0 = kc * p.cs;
     const int ns = max(0, min(chunk0 + p.cs, p.nsteps) - chunk0);
-    const int rt_first = j * nwarps + warp;
+    // row tiles dealt warp-major across the chunk's CTAs, so every SM gets work
+    const int rt_first = warp * p.ctas_per_chunk + j;
     const int rt_stride = p.ctas_per_chunk * nwarps;
     const int n_units = (rt_first < p.n_rt && ns > 0) ? (p.n_rt - 1 - rt_first) / rt_stride + 1 : 0;
     const int total = n_units * ns;  // flattened (unit, step) sequence of this warp
@@ -88,24 +93,27 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         fence_mbar_init();
     }
     __syncwarp();
-    auto issue = [&](int f, int stage) {  // lane 0 only
-        const int m = f / ns, st = chunk0 + (f - m * ns);
-        const int rt = rt_first + m * rt_stride;
-        const uint32_t bar = my_bar0 + 8 * stage;
-        const uint32_t dst = my_ring0 + stage * kStageBytes;
-        const uint32_t* src = p.planes + ((long long)rt * p.nsteps + st) * 128;
+    // One bulk copy per step: [scales][planes 0..NPL-1] are contiguous at the
+    // head of the (rt, st) block.  The issue cursor advances incrementally.
+    const uint32_t skip_words = (uint32_t)(p.sb_words - kScaleBytes / 4);  // scale words not needed
+    const uint32_t* issue_ptr = p.blob + ((long long)rt_first * p.nsteps + chunk0) * p.step_words + skip_words;
+    int issue_li = 0, issue_stage = 0;
+    const long long unit_jump = ((long long)rt_stride * p.nsteps - ns) * p.step_words;
+    auto issue_next = [&]() {  // lane 0 only
+        const uint32_t bar = my_bar0 + 8 * issue_stage;
         mbar_expect_tx(bar, kStageBytes);
-#pragma unroll
-        for (int jj = 0; jj < NPL; ++jj)
-            bulk_g2s(dst + jj * kSlab, src + jj * p.plane_stride, kSlab, bar, policy);
-        if constexpr (GS == 128)
-            bulk_g2s(dst + NPL * kSlab, p.tscales + ((long long)rt * p.ngp + 2 * st) * 16,
-                     kScaleBytes, bar, policy);
+        bulk_g2s(my_ring0 + issue_stage * kStageBytes, issue_ptr, kStageBytes, bar, policy);
+        issue_ptr += p.step_words;
+        if (++issue_li == ns) {
+            issue_li = 0;
+            issue_ptr += unit_jump;
+        }
+        if (++issue_stage == D) issue_stage = 0;
     };
     // Weights do not depend on the previous kernel: fill the ring before
     // waiting on the programmatic dependency (X, workspace, Y).
-    if (lane == 0 && !(p.debug & 2))
-        for (int i = 0; i < D && i < total; ++i) issue(i, i);
+    if (lane == 0 && !(MQ_GEMV_DEBUG & 2))
+        for (int i = 0; i < D && i < total; ++i) issue_next();
     pdl_launch_dependents();
     pdl_wait();
 
@@ -190,7 +198,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
 #pragma unroll
             for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
             uint32_t A[16];
-            if (p.debug & 1) {
+            if (MQ_GEMV_DEBUG & 1) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) A[q] = T[q % NPL] & 0x3F3F3F3Fu;
             } else {
@@ -331,11 +339,11 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         if (lane == 0) p.tickets[rt] = 0;
     };
 
+    int li = 0, stage = 0, rt = rt_first;
+    uint32_t parity = 0;
 #pragma unroll 1
     for (int f = 0; f < total; ++f) {
-        const int m = f / ns, li = f - m * ns;
         const int st = chunk0 + li;
-        const int rt = rt_first + m * rt_stride;
         if (li == 0) {
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
@@ -347,26 +355,33 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                 next_bound = (cur_grp + 1) * p.G;
             }
         }
-        const int stage = f % D;
-        if (!(p.debug & 2)) mbar_wait(my_bar0 + 8 * stage, (uint32_t)((f / D) & 1));
+        if (!(MQ_GEMV_DEBUG & 2)) mbar_wait(my_bar0 + 8 * stage, parity);
         const uint32_t src = my_ring0 + stage * kStageBytes;
-        uint4 buf[NPL];
-#pragma unroll
-        for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + jj * kSlab + lane * 16);
         float sc[4];
         if constexpr (GS == 128) {
-            sc[0] = lds32f(src + NPL * kSlab + g * 4);
-            sc[1] = lds32f(src + NPL * kSlab + (g + 8) * 4);
-            sc[2] = lds32f(src + NPL * kSlab + (16 + g) * 4);
-            sc[3] = lds32f(src + NPL * kSlab + (24 + g) * 4);
+            sc[0] = lds32f(src + g * 4);
+            sc[1] = lds32f(src + (g + 8) * 4);
+            sc[2] = lds32f(src + (16 + g) * 4);
+            sc[3] = lds32f(src + (24 + g) * 4);
         }
+        uint4 buf[NPL];
+#pragma unroll
+        for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
         __syncwarp();
-        if (lane == 0 && f + D < total && !(p.debug & 2)) {
+        if (lane == 0 && f + D < total && !(MQ_GEMV_DEBUG & 2)) {
             fence_proxy_async_smem();
-            issue(f + D, stage);
+            issue_next();
         }
         process(buf, sc, st);
-        if (li == ns - 1) finalize(rt);
+        if (++li == ns) {
+            finalize(rt);
+            li = 0;
+            rt += rt_stride;
+        }
+        if (++stage == D) {
+            stage = 0;
+            parity ^= 1u;
+        }
     }
 }
 

@@ -3,18 +3,20 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "matq_common.cuh"
+
 namespace mq {
 
-cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, int N, int K, int nbits,
-                               uint32_t* planes, cudaStream_t s);
-cudaError_t launch_tile_scales(const float* scales, int N, int ng, int ngp, float* ts,
+cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, const Layout& L, int nbits,
+                               uint32_t* blob, cudaStream_t s);
+cudaError_t launch_pack_scales(const float* scales, const Layout& L, int ng, uint32_t* blob, float* ts,
                                cudaStream_t s);
-cudaError_t launch_slice_codes(int r, bool child, const uint32_t* planes, int N, int K,
-                               uint8_t* out, long long ldo, cudaStream_t s);
-cudaError_t launch_decode_dense(int r, bool child, const uint32_t* planes, const float* ts, int G,
-                                float out_scale, int N, int K, int8_t* vals, float* W,
+cudaError_t launch_slice_codes(int r, bool child, const uint32_t* blob, const Layout& L, uint8_t* out,
+                               long long ldo, cudaStream_t s);
+cudaError_t launch_decode_dense(int r, bool child, const uint32_t* blob, const float* ts,
+                                const Layout& L, float out_scale, int8_t* vals, float* W,
                                 long long ldw, cudaStream_t s);
-cudaError_t launch_materialize_child(int r, const uint32_t* planes, int N, int K, uint32_t* child,
+cudaError_t launch_materialize_child(int r, const uint32_t* blob, const Layout& Lp, uint32_t* child,
                                      cudaStream_t s);
 cudaError_t launch_slice_elementwise(const uint8_t* q, long long n, int c, int r, int on_master,
                                      uint8_t* out, int* err, cudaStream_t s);

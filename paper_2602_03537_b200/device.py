@@ -1,11 +1,11 @@
-"""Device-resident bit-plane weights (the P8 layout) and the GEMV entry.
+"""Device-resident bit-plane weights (the step-interleaved blob) and the GEMV.
 
-A ``PlaneTensor`` owns the MSB-first bit planes of one (N, K) layer in HBM
-plus its tiled fp32 group scales.  A parent (``nbits = c``,
-normally the int8 parent with c = 8) serves every slice r <= c without
-repacking: slice r reads planes 0..r (mode P).  A child (``nbits = r``)
-holds an already-sliced r-bit code (mode C) and streams exactly r/8 of the
-parent's bytes.
+A ``PlaneTensor`` owns one (N, K) layer in HBM: per (16-row tile, 256-column
+step) a block of [group scales][MSB-first bit-plane slabs].  A
+parent (``nplanes = c``, normally the int8 parent with c = 8) serves every
+slice r <= c without repacking: slice r reads the scales and planes 0..r of
+each block (mode P).  A child (``nplanes = r``) holds an already-sliced r-bit
+code (mode C) and streams exactly r/8 of the parent's plane bytes.
 
 Everything here is a thin shell over libmatq (include/matq.h); there is no
 CPU compute path.
@@ -66,23 +66,31 @@ def reserve_workspace(nbytes: int, stream=None) -> None:
 
 
 class PlaneTensor:
-    """Bit planes + tiled scales of one layer on the current CUDA device."""
+    """Bit-plane blob (+ tiled scales when G != 128) of one layer on the GPU.
 
-    def __init__(self, planes: torch.Tensor, tscales: torch.Tensor, N: int, K: int, G: int,
-                 nbits: int, is_child: bool, scales_are_effective: bool):
-        self.planes = planes
+    ``nplanes`` is the number of stored planes: the master bit-width c of a
+    parent (8 for the int8 parent), or r for an r-bit child.  ``master_bits``
+    is the grid the scales live on; ``out_scale(r)`` = 2^(master_bits - r)
+    unless the stored scales are already effective (a reference-style child).
+    """
+
+    def __init__(self, blob: torch.Tensor, tscales: torch.Tensor | None, N: int, K: int, G: int,
+                 nplanes: int, master_bits: int, scales_are_effective: bool):
+        self.blob = blob
         self.tscales = tscales
         self.N, self.K, self.G = int(N), int(K), int(G)
-        self.nbits = int(nbits)
-        self.is_child = bool(is_child)
+        self.nplanes = int(nplanes)
+        self.master_bits = int(master_bits)
         self.scales_are_effective = bool(scales_are_effective)
 
     # -- construction ------------------------------------------------------
     @classmethod
-    def from_codes(cls, codes, nbits: int, scales, group_size: int, is_child: bool = False,
+    def from_codes(cls, codes, nbits: int, scales, group_size: int,
                    scales_are_effective: bool = False) -> "PlaneTensor":
-        """K1 on device: (N, K) codes with ``nbits`` bits -> MSB-first planes."""
+        """K1 on device: (N, K) codes with ``nbits`` bits + (N, ng) scales -> blob."""
         _lib.require_cuda()
+        if group_size < 32 or group_size % 32:
+            raise ValueError("group size must be a multiple of 32")
         c_d = _as_device_u8(codes)
         if c_d.dim() != 2:
             raise ValueError("codes must be a matrix")
@@ -91,14 +99,14 @@ class PlaneTensor:
         ng = -(-K // group_size)
         if tuple(s_d.shape) != (N, ng):
             raise ValueError("scales shape %s != (%d, %d)" % (tuple(s_d.shape), N, ng))
-        nplane_bytes = _lib.lib().mq_planes_bytes(N, K, nbits)
-        planes = torch.empty(nplane_bytes // 4, dtype=torch.int32, device="cuda")
-        ts = torch.empty(_lib.lib().mq_tscales_bytes(N, K, group_size) // 4, dtype=torch.float32,
-                         device="cuda")
-        sp = _lib.stream_ptr()
-        _lib.call("mq_pack_planes", _lib.ptr(c_d), K, N, K, nbits, _lib.ptr(planes), sp)
-        _lib.call("mq_tile_scales", _lib.ptr(s_d), N, K, group_size, _lib.ptr(ts), sp)
-        return cls(planes, ts, N, K, group_size, nbits, is_child, scales_are_effective)
+        L = _lib.lib()
+        blob = torch.empty(L.mq_blob_bytes(N, K, group_size, nbits) // 4, dtype=torch.int32, device="cuda")
+        ts = None
+        if group_size != 128:
+            ts = torch.empty(L.mq_tscales_bytes(N, K, group_size) // 4, dtype=torch.float32, device="cuda")
+        _lib.call("mq_pack_blob", _lib.ptr(c_d), K, N, K, nbits, _lib.ptr(s_d), group_size,
+                  _lib.ptr(blob), _lib.ptr(ts), _lib.stream_ptr())
+        return cls(blob, ts, N, K, group_size, nbits, nbits, scales_are_effective)
 
     @classmethod
     def random_parent(cls, N: int, K: int, group_size: int = 128, seed: int = 0,
@@ -123,67 +131,64 @@ class PlaneTensor:
 
     @property
     def nbytes(self) -> int:
-        return self.planes.numel() * 4 + self.tscales.numel() * 4
+        return self.blob.numel() * 4 + (0 if self.tscales is None else self.tscales.numel() * 4)
 
-    def _mode(self, r: int) -> tuple[int, float]:
-        """(flags, out_scale) to read slice r from these planes."""
+    def _check(self, r: int) -> float:
+        """Validate slice r for this blob; returns the output scale."""
         if r not in LADDER:
             raise ValueError("unsupported bits")
-        if self.is_child:
-            if r != self.nbits:
-                raise ValueError("a %d-bit child cannot serve %d bits" % (self.nbits, r))
-            return _lib.MQ_CHILD, 1.0
-        if r > self.nbits:
-            raise ValueError("cannot slice %d bits out of %d" % (r, self.nbits))
-        flags = _lib.MQ_CHILD if r == self.nbits else 0
-        scale = 1.0 if self.scales_are_effective else float(1 << (self.nbits - r))
-        return flags, scale
+        if r > self.nplanes:
+            raise ValueError("cannot slice %d bits out of %d" % (r, self.nplanes))
+        if r != self.nplanes and r + 1 > self.nplanes:
+            raise ValueError("a %d-plane blob cannot serve %d bits" % (self.nplanes, r))
+        return 1.0 if self.scales_are_effective else float(1 << (self.master_bits - r))
 
     def planes_read(self, r: int) -> int:
         """Planes a slice-r GEMV streams (r+1 in mode P, r in mode C / identity)."""
-        flags, _ = self._mode(r)
-        return r if flags & _lib.MQ_CHILD else r + 1
+        self._check(r)
+        return r if r == self.nplanes else r + 1
 
     # -- K2: slice / decode ------------------------------------------------
     def slice_codes(self, r: int) -> torch.Tensor:
-        flags, _ = self._mode(r)
+        self._check(r)
         out = torch.empty((self.N, self.K), dtype=torch.uint8, device="cuda")
-        _lib.call("mq_slice", _lib.ptr(self.planes), self.N, self.K, r, int(bool(flags & _lib.MQ_CHILD)),
+        _lib.call("mq_slice", _lib.ptr(self.blob), self.N, self.K, self.G, self.nplanes, r,
                   _lib.ptr(out), self.K, _lib.stream_ptr())
         return out
 
     def decode(self, r: int, values: bool = False) -> torch.Tensor:
         """fp32 dequantised weights (or int8 s - z) through the GEMV register path."""
-        flags, scale = self._mode(r)
-        child = int(bool(flags & _lib.MQ_CHILD))
+        scale = self._check(r)
         sp = _lib.stream_ptr()
         if values:
             out = torch.empty((self.N, self.K), dtype=torch.int8, device="cuda")
-            _lib.call("mq_dequant", _lib.ptr(self.planes), None, self.N, self.K, self.G, r, child,
-                      scale, _lib.ptr(out), None, self.K, sp)
+            _lib.call("mq_dequant", _lib.ptr(self.blob), _lib.ptr(self.tscales), self.N, self.K,
+                      self.G, self.nplanes, r, scale, _lib.ptr(out), None, self.K, sp)
         else:
             out = torch.empty((self.N, self.K), dtype=torch.float32, device="cuda")
-            _lib.call("mq_dequant", _lib.ptr(self.planes), _lib.ptr(self.tscales), self.N, self.K,
-                      self.G, r, child, scale, None, _lib.ptr(out), self.K, sp)
+            _lib.call("mq_dequant", _lib.ptr(self.blob), _lib.ptr(self.tscales), self.N, self.K,
+                      self.G, self.nplanes, r, scale, None, _lib.ptr(out), self.K, sp)
         return out
 
     def materialize_child(self, r: int) -> "PlaneTensor":
-        """Mode C: an r-plane child sliced once from this parent (K2c)."""
-        flags, scale = self._mode(r)
-        if flags & _lib.MQ_CHILD:
+        """Mode C: an r-plane child sliced once from this 8-plane parent (K2c)."""
+        self._check(r)
+        if r == self.nplanes:
             return self
-        child = torch.empty(_lib.lib().mq_planes_bytes(self.N, self.K, r) // 4, dtype=torch.int32,
-                            device="cuda")
-        _lib.call("mq_materialize_child", _lib.ptr(self.planes), self.N, self.K, r, _lib.ptr(child),
-                  _lib.stream_ptr())
-        ts = self.tscales if scale == 1.0 else self.tscales * scale  # exact: power of two
-        return PlaneTensor(child, ts, self.N, self.K, self.G, r, True, True)
+        if self.nplanes != 8:
+            raise ValueError("children are materialised from an 8-plane parent")
+        child = torch.empty(_lib.lib().mq_blob_bytes(self.N, self.K, self.G, r) // 4,
+                            dtype=torch.int32, device="cuda")
+        _lib.call("mq_materialize_child", _lib.ptr(self.blob), self.N, self.K, self.G, r,
+                  _lib.ptr(child), _lib.stream_ptr())
+        return PlaneTensor(child, self.tscales, self.N, self.K, self.G, r, self.master_bits,
+                           self.scales_are_effective)
 
     # -- K3 ----------------------------------------------------------------
     def gemv(self, X: torch.Tensor, r: int, out: torch.Tensor | None = None,
              out_dtype: torch.dtype | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
         """Y = X @ dequant(slice_r).T for 1 <= B <= 32 rows (16 for fp32 X)."""
-        flags, scale = self._mode(r)
+        scale = self._check(r)
         if X.dim() != 2 or X.shape[1] != self.K:
             raise ValueError("activations must be (batch, %d)" % self.K)
         if not X.is_cuda:
@@ -191,6 +196,7 @@ class PlaneTensor:
         if X.stride(1) != 1:
             X = X.contiguous()
         B = X.shape[0]
+        flags = 0
         if X.dtype == torch.float32:
             flags |= _lib.MQ_X_F32
         elif X.dtype != torch.bfloat16:
@@ -202,16 +208,16 @@ class PlaneTensor:
             flags |= _lib.MQ_Y_F32
         elif out.dtype != torch.bfloat16:
             raise ValueError("output must be bfloat16 or float32")
-        if out.stride(1) != 1 or out.shape != (B, self.N):
+        if out.stride(1) != 1 or tuple(out.shape) != (B, self.N):
             raise ValueError("bad output tensor")
         if pdl:
             flags |= _lib.MQ_PDL
         sp = _lib.stream_ptr(stream)
         need = _lib.lib().mq_gemv_workspace_bytes(self.N, self.K, B, flags)
         ws = WORKSPACES.get(need, sp)
-        _lib.call("mq_gemv", _lib.ptr(self.planes), _lib.ptr(self.tscales), _lib.ptr(X), X.stride(0),
-                  _lib.ptr(out), out.stride(0), B, self.N, self.K, self.G, r, scale, flags,
-                  _lib.ptr(ws), 0 if ws is None else ws.numel(), sp)
+        _lib.call("mq_gemv", _lib.ptr(self.blob), _lib.ptr(self.tscales), _lib.ptr(X), X.stride(0),
+                  _lib.ptr(out), out.stride(0), B, self.N, self.K, self.G, self.nplanes, r, scale,
+                  flags, _lib.ptr(ws), 0 if ws is None else ws.numel(), sp)
         return out
 
     def workspace_bytes(self, B: int, x_f32: bool = False) -> int:

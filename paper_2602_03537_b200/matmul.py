@@ -83,8 +83,7 @@ class PackedLayer:
                   _bits=layer.bits, _shape=tuple(layer.codes.shape))
         if packed is None:
             out._planes = PlaneTensor.from_codes(layer.codes, layer.bits, layer.scales,
-                                                 layer.group_size, is_child=True,
-                                                 scales_are_effective=True)
+                                                 layer.group_size, scales_are_effective=True)
         return out
 
     @classmethod
@@ -109,7 +108,7 @@ class PackedLayer:
                 raise MatmulError("layer has no packed codes")
             codes = unpack_device(to_canonical(self.packed))
             self._planes = PlaneTensor.from_codes(codes, self.bits, self.scales, self.group_size,
-                                                  is_child=True, scales_are_effective=True)
+                                                  scales_are_effective=True)
             self._planes_key = key
         return self._planes
 

@@ -30,23 +30,23 @@ static int slice_ref(int q, int r) {  // slicing.py:67-84 with c = 8
     return v > (1 << r) - 1 ? (1 << r) - 1 : v;
 }
 
-// host restatement of k_pack_planes (matq_aux.cu)
+// host restatement of k_pack_planes (matq_aux.cu), step-interleaved blob
 static void pack_planes(const std::vector<uint8_t>& codes, int N, int K, int nbits,
-                        std::vector<uint32_t>& planes) {
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long total = (long long)n_rt * nsteps * 128;
-    planes.assign((size_t)total * nbits, 0u);
+                        std::vector<uint32_t>& blob, Layout& L) {
+    L = Layout::make(N, K, 128, nbits);
+    blob.assign((size_t)L.total_words(), 0u);
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
     for (long long idx = 0; idx < total; ++idx) {
         const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
         const long long blk = idx >> 7;
-        const int st = (int)(blk % nsteps), rt = (int)(blk / nsteps);
+        const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
         for (int bit = 0; bit < 32; ++bit) {
             int ro, co;
             word_bit_pos(lane, w, bit, ro, co);
             const int row = rt * 16 + ro, col = st * 256 + co;
             const uint32_t q = (row < N && col < K) ? codes[(size_t)row * K + col] : 0u;
             for (int j = 0; j < nbits; ++j)
-                planes[(size_t)j * total + idx] |= ((q >> (nbits - 1 - j)) & 1u) << bit;
+                blob[(size_t)L.plane_word(rt, st, j, lane, w)] |= ((q >> (nbits - 1 - j)) & 1u) << bit;
         }
     }
 }
@@ -61,16 +61,16 @@ static long long check(const std::vector<uint8_t>& parent, int N, int K) {
         nbits = R;
     }
     std::vector<uint32_t> planes;
-    pack_planes(src, N, K, nbits, planes);
-    const int n_rt = pad16(N) / 16, nsteps = pad256(K) / 256;
-    const long long total = (long long)n_rt * nsteps * 128;
+    Layout L;
+    pack_planes(src, N, K, nbits, planes, L);
+    const long long total = (long long)L.n_rt * L.nsteps * 128;
     long long bad = 0;
     for (long long idx = 0; idx < total; ++idx) {
         const int w = (int)(idx & 3), lane = (int)((idx >> 2) & 31);
         const long long blk = idx >> 7;
-        const int st = (int)(blk % nsteps), rt = (int)(blk / nsteps);
+        const int st = (int)(blk % L.nsteps), rt = (int)(blk / L.nsteps);
         uint32_t T[NPL];
-        for (int j = 0; j < NPL; ++j) T[j] = planes[(size_t)j * total + idx];
+        for (int j = 0; j < NPL; ++j) T[j] = planes[(size_t)L.plane_word(rt, st, j, lane, w)];
         uint32_t S[R];
         slice_loaded<R, CHILD>(T, S);
         uint32_t A[16];

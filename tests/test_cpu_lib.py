@@ -19,7 +19,7 @@ def test_library_exports_every_declared_symbol():
     from paper_2602_03537_b200 import _lib
 
     syms = _header_symbols()
-    assert len(syms) >= 19
+    assert len(syms) >= 18
     out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
                          text=True, check=True).stdout
     exported = set(re.findall(r"\sT\s(mq_\w+)", out))
@@ -47,8 +47,10 @@ def test_host_layout_queries():
     Np, Kp, ngp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
     assert L.mq_layout_dims(40, 600, 128, ctypes.byref(Np), ctypes.byref(Kp), ctypes.byref(ngp)) == 0
     assert (Np.value, Kp.value, ngp.value) == (48, 768, 6)
-    assert L.mq_planes_bytes(4096, 4096, 8) == 4096 * 4096
-    assert L.mq_planes_bytes(4096, 4096, 3) == 3 * 4096 * 4096 // 8
+    # blob = planes + one fp32 scale per (row, group) embedded per step (G = 128)
+    assert L.mq_blob_bytes(4096, 4096, 128, 8) == 4096 * 4096 + 4096 * 32 * 4
+    assert L.mq_blob_bytes(4096, 4096, 128, 3) == 3 * 4096 * 4096 // 8 + 4096 * 32 * 4
+    assert L.mq_blob_bytes(4096, 4096, 96, 8) == 4096 * 4096  # no embedded scales
     assert L.mq_tscales_bytes(4096, 4096, 128) == 4096 * 32 * 4
     assert L.mq_layout_dims(0, 10, 128, None, None, None) == _lib.MQ_ERR_INVALID
     # workspace query is host-only
