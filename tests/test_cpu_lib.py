@@ -64,9 +64,9 @@ def test_invalid_arguments_fail_before_cuda():
 
     L = _lib.lib()
     # unsupported bits / group size are rejected by validation, no device touched
-    st = L.mq_gemv(1, 1, 1, 64, 1, 64, 1, 64, 64, 128, 5, 1.0, 0, None, 0, None)
+    st = L.mq_gemv(1, 1, 1, 64, 1, 64, 1, 64, 64, 128, 8, 5, 1.0, 0, None, 0, None)
     assert st == _lib.MQ_ERR_INVALID and "unsupported bits" in _lib.last_error()
-    st = L.mq_gemv(1, 1, 1, 64, 1, 64, 1, 64, 64, 48, 4, 1.0, 0, None, 0, None)
+    st = L.mq_gemv(1, 1, 1, 64, 1, 64, 1, 64, 64, 48, 8, 4, 1.0, 0, None, 0, None)
     assert st == _lib.MQ_ERR_INVALID and "multiple of 32" in _lib.last_error()
     st = L.mq_slice_elementwise(None, 0, 3, 4, 0, None, None, None)
     assert st == _lib.MQ_ERR_INVALID and "cannot slice 4 bits out of 3" in _lib.last_error()
