@@ -46,7 +46,7 @@ int sm_count() {
 struct GemvConfig {
     int NT, S, cs, grid, nwarps, stages;
     size_t smem;
-    int xs_stride, xs_bytes;
+    int xs_stride, xs_bytes, xcopy_stride, cs_off;
 };
 
 constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA
@@ -62,7 +62,9 @@ int env_int(const char* name, int dflt) {
     return (v && *v) ? atoi(v) : dflt;
 }
 
-GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
+GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
+    // activation copies for zero-point folding (matq_common.cuh ZeroPoint<R>)
+    const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     GemvConfig c{};
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
@@ -76,7 +78,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
         if (force_s && S != std::min(force_s, nsteps)) continue;
         const int cs = mq::cdiv(nsteps, S);
         if (mq::cdiv(nsteps, cs) != S && !force_s) continue;  // would leave an empty chunk
-        const size_t xs = (size_t)Bx * (cs * 256 + 8) * 2;
+        const size_t xs = (size_t)ncopy * Bx * (cs * 256 + 8) * 2;
         if (xs > kXsMax && cs > 1) continue;
         int cpc = sms / S;
         if (cpc < 1) break;
@@ -91,7 +93,10 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128) {
         }
     }
     c.xs_stride = c.cs * 256 + 8;
-    c.xs_bytes = (int)(((size_t)Bx * c.xs_stride * 2 + 15) & ~(size_t)15);
+    c.xcopy_stride = Bx * c.xs_stride;
+    c.cs_off = (int)(((size_t)ncopy * c.xcopy_stride * 2 + 15) & ~(size_t)15);
+    const size_t zc_bytes = (g128 && r != 8) ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
+    c.xs_bytes = (int)((c.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
     const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
     int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (c.nwarps * stage));
@@ -215,7 +220,7 @@ size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
     if (N < 1 || K < 1 || B < 1) return 0;
     const int Bx = (flags & MQ_X_F32) ? 2 * B : B;
     if (Bx > 32) return 0;
-    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, 8, true), B);
+    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, 8, true, 4), B);
 }
 
 int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, void* Y, int ldy,
@@ -235,7 +240,7 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
 
     const bool child_mode = nplanes == r;
     const int npl = (child_mode || r == 8) ? r : r + 1;
-    const GemvConfig c = choose_gemv_config(N, K, Bx, npl, G == 128);
+    const GemvConfig c = choose_gemv_config(N, K, Bx, npl, G == 128, r);
     const size_t need = gemv_ws_bytes(N, c, B);
     if (need > workspace_bytes || (need && !workspace))
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
@@ -273,6 +278,8 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     p.x_f32 = xf32 ? 1 : 0;
     p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
     p.xs_stride = c.xs_stride;
+    p.xcopy_stride = c.xcopy_stride;
+    p.cs_off = c.cs_off;
     p.xs_bytes = c.xs_bytes;
     p.stages = c.stages;
     const dim3 grid(c.grid, 1, 1), block(32 * c.nwarps, 1, 1);

@@ -187,6 +187,21 @@ MQ_HD uint32_t field_bf16(uint32_t w) {
     return hfma2(v, mul, add);
 }
 
+// Field of R bits at offset O, magic-encoded only: bf16 128 + field * 2^O.
+// The GEMV folds the 2^-O into a pre-scaled activation copy and the
+// (128 * 2^-O + z) zero point into a per-group constant (zp_off<R> below).
+template <int R, int O>
+MQ_HD uint32_t field_raw(uint32_t w) {
+    static_assert(O + R <= 7, "field must sit inside the bf16 mantissa");
+    constexpr uint32_t m = ((1u << R) - 1u) << O;
+    return lop3<kAndOr>(w, x2(m), 0x43004300u);
+}
+template <int R, int O, bool RAW>
+MQ_HD uint32_t field_out(uint32_t w) {
+    if constexpr (RAW) return field_raw<R, O>(w);
+    else return field_bf16<R, O>(w);
+}
+
 // 8-bit field at offset 0 (bit 7 would land in the bf16 exponent):
 // (low7 | 0x4300) - (bit7 ? 128 : 256) = code - 128, exact.
 MQ_HD uint32_t field8_bf16(uint32_t w) {
@@ -250,7 +265,7 @@ MQ_HD void transpose_planes(uint32_t (&P)[NP]) {
 // steps: A[p] holds weights at bit positions p (low half) and p + 16 (high
 // half) as exact bf16 (s - 2^(R-1)).  S[0..R-1] are the sliced planes, MSB
 // first.
-template <int R>
+template <int R, bool RAW = false>
 MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
     if constexpr (R == 2) {
         uint32_t P[2] = {S[1], S[0]};
@@ -259,14 +274,14 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
             const uint32_t w0 = P[i], w6 = shr<6>(P[i]), w12 = shr<12>(P[i]);
-            A[0 + i] = field_bf16<2, 0>(w0);
-            A[2 + i] = field_bf16<2, 2>(w0);
-            A[4 + i] = field_bf16<2, 4>(w0);
-            A[6 + i] = field_bf16<2, 0>(w6);
-            A[8 + i] = field_bf16<2, 2>(w6);
-            A[10 + i] = field_bf16<2, 4>(w6);
-            A[12 + i] = field_bf16<2, 0>(w12);
-            A[14 + i] = field_bf16<2, 2>(w12);
+            A[0 + i] = field_out<2, 0, RAW>(w0);
+            A[2 + i] = field_out<2, 2, RAW>(w0);
+            A[4 + i] = field_out<2, 4, RAW>(w0);
+            A[6 + i] = field_out<2, 0, RAW>(w6);
+            A[8 + i] = field_out<2, 2, RAW>(w6);
+            A[10 + i] = field_out<2, 4, RAW>(w6);
+            A[12 + i] = field_out<2, 0, RAW>(w12);
+            A[14 + i] = field_out<2, 2, RAW>(w12);
         }
     } else if constexpr (R == 3 || R == 4) {
         uint32_t P[4];
@@ -279,15 +294,15 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
             const uint32_t w = P[i];
             if constexpr (R == 3) {
                 const uint32_t w8 = shr<8>(w);
-                A[0 + i] = field_bf16<3, 0>(w);
-                A[4 + i] = field_bf16<3, 4>(w);
-                A[8 + i] = field_bf16<3, 0>(w8);
-                A[12 + i] = field_bf16<3, 4>(w8);
+                A[0 + i] = field_out<3, 0, RAW>(w);
+                A[4 + i] = field_out<3, 4, RAW>(w);
+                A[8 + i] = field_out<3, 0, RAW>(w8);
+                A[12 + i] = field_out<3, 4, RAW>(w8);
             } else {
-                A[0 + i] = field_bf16<4, 0>(w);
-                A[4 + i] = field_bf16<4, 3>(shr<1>(w));
-                A[8 + i] = field_bf16<4, 0>(shr<8>(w));
-                A[12 + i] = field_bf16<4, 3>(shr<9>(w));
+                A[0 + i] = field_out<4, 0, RAW>(w);
+                A[4 + i] = field_out<4, 3, RAW>(shr<1>(w));
+                A[8 + i] = field_out<4, 0, RAW>(shr<8>(w));
+                A[12 + i] = field_out<4, 3, RAW>(shr<9>(w));
             }
         }
     } else {
@@ -300,14 +315,46 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             if constexpr (R == 6) {
-                A[0 + i] = field_bf16<6, 0>(P[i]);
-                A[8 + i] = field_bf16<6, 0>(shr<8>(P[i]));
+                A[0 + i] = field_out<6, 0, RAW>(P[i]);
+                A[8 + i] = field_out<6, 0, RAW>(shr<8>(P[i]));
             } else {
                 A[0 + i] = field8_bf16(P[i]);
                 A[8 + i] = field8_bf16(shr<8>(P[i]));
             }
         }
     }
+}
+
+// Zero-point folding for the raw decode (R in {2,3,4,6}).  decode_word<R, true>
+// leaves A[4s+q] = bf16(128 + s_code * 2^o) with o = kOff[s][q >> 1] (the field
+// offset of k16 step s, 8-column half q >> 1).  The GEMV multiplies that half
+// by an activation copy scaled by 2^-o, so the MMA returns
+//   sum (s_code - z) x + sum (128 * 2^-o + z) x,
+// and subtracts the second term, computed per scale group by the same MMA
+// chain on the all-zero-code A fragment kZeroA (so zero-code rows are exactly
+// 0, as in the reference, test_matmul.py:61-66).
+template <int R>
+__host__ __device__ constexpr int zp_off(int s, int h) {
+    // R = 2: W_i fields n = 2s + h at offsets 0,2,4 | 0 (>>6),2,4 | 0 (>>12),2
+    // R = 3: nibble n = s at offsets 0,4 | 0 (>>8),4      R = 4: 0, 3 (>>1) | 0 (>>8), 3 (>>9)
+    // R = 6, 8: byte fields at offset 0
+    return R == 2 ? ((2 * s + h) % 3 == 0 ? 0 : ((2 * s + h) % 3 == 1 ? 2 : 4))
+         : R == 3 ? ((s & 1) ? 4 : 0)
+         : R == 4 ? ((s & 1) ? 3 : 0)
+         : 0;
+}
+// distinct offsets -> activation copy index (copy c is x * 2^-zp_copy_off(R, c))
+__host__ __device__ constexpr int zp_copy_of(int R, int o) {
+    return o == 0 ? 0 : (R == 2 ? (o == 2 ? 1 : 2) : 1);
+}
+__host__ __device__ constexpr int zp_ncopies(int R) { return R == 2 ? 3 : (R == 3 || R == 4 ? 2 : 1); }
+__host__ __device__ constexpr int zp_copy_off(int R, int c) {
+    return c == 0 ? 0 : (R == 2 ? (c == 1 ? 2 : 4) : (R == 3 ? 4 : 3));
+}
+// A register (s, q) of the all-zero-code fragment: 128 + z * 2^o, both halves
+template <int R>
+__host__ __device__ constexpr uint32_t zp_zero_a(int s, int q) {
+    return x2(bf16_bits(128 + ((1 << (R - 1)) << zp_off<R>(s, q >> 1)), 0));
 }
 
 // Loaded planes -> sliced planes.  CHILD: planes already hold the r-bit code

@@ -49,6 +49,8 @@ struct GemvParams {
     int x_f32;                // X is fp32 (split into hi + lo bf16 rows)
     int y_f32;                // Y is fp32
     int xs_stride;            // smem X row stride (elements)
+    int xcopy_stride;         // elements between activation copies (zero-point folding)
+    int cs_off;               // smem byte offset of the per-group zero-point constants
     int xs_bytes;             // smem bytes of the X staging area (16-aligned)
     int stages;               // per-warp TMA ring depth (<= 8)
 };
@@ -65,6 +67,9 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     constexpr uint32_t kSlab = 512;
     constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;   // 2 groups x 16 rows, head of block
     constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
+    // zero-point folding (zp_off<R>, matq_common.cuh): raw magic-encoded A + scaled activation copies
+    constexpr bool ZP = (GS == 128) && (R != 8) && !(MQ_GEMV_DEBUG & 1);
+    constexpr int NCOPY = ZP ? zp_ncopies(R) : 1;
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
 
@@ -118,8 +123,19 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     pdl_wait();
 
     // ---- stage X[:, chunk columns] into shared memory as bf16 rows ----------
+    // copy c (ZP only) holds x * 2^-zp_copy_off(R, c): exact power-of-two scaling.
     const int Kc = p.cs * kStepCols;
     const int col_base = chunk0 * kStepCols;
+    auto put = [&](int row, int c, uint16_t v) {
+        xs[row * p.xs_stride + c] = v;
+        if constexpr (NCOPY > 1) {
+#pragma unroll
+            for (int cp = 1; cp < NCOPY; ++cp) {
+                const float f = bf16_to_f32(v) * (1.0f / (float)(1 << zp_copy_off(R, cp)));
+                xs[cp * p.xcopy_stride + row * p.xs_stride + c] = f32_to_bf16_rn(f);
+            }
+        }
+    };
     if (!p.x_f32) {
         const uint16_t* X = reinterpret_cast<const uint16_t*>(p.X);
         const bool vec = ((p.ldx & 7) == 0) && ((p.K & 7) == 0) &&
@@ -132,12 +148,24 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                 uint4 v = make_uint4(0, 0, 0, 0);
                 if (col < p.K) v = __ldg(reinterpret_cast<const uint4*>(X + (long long)b * p.ldx + col));
                 *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
+                if constexpr (NCOPY > 1) {
+                    const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+                    for (int cp = 1; cp < NCOPY; ++cp) {
+                        uint4 o;
+                        uint16_t* ho = reinterpret_cast<uint16_t*>(&o);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            ho[e] = f32_to_bf16_rn(bf16_to_f32(hv[e]) * (1.0f / (float)(1 << zp_copy_off(R, cp))));
+                        *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = o;
+                    }
+                }
             }
         } else {
             for (int idx = threadIdx.x; idx < p.B * Kc; idx += blockDim.x) {
                 const int b = idx / Kc, c = idx - b * Kc;
                 const int col = col_base + c;
-                xs[b * p.xs_stride + c] = col < p.K ? X[(long long)b * p.ldx + col] : (uint16_t)0;
+                put(b, c, col < p.K ? X[(long long)b * p.ldx + col] : (uint16_t)0);
             }
         }
     } else {
@@ -150,8 +178,8 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             const float x = col < p.K ? X[(long long)b * p.ldx + col] : 0.0f;
             const uint16_t hi = f32_to_bf16_rn(x);
             const uint16_t lo = f32_to_bf16_rn(x - bf16_to_f32(hi));
-            xs[(2 * b) * p.xs_stride + c] = hi;
-            xs[(2 * b + 1) * p.xs_stride + c] = lo;
+            put(2 * b, c, hi);
+            put(2 * b + 1, c, lo);
         }
     }
     __syncthreads();
@@ -159,13 +187,64 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     // ldmatrix row addresses: matrix mi = lane >> 3 covers k offset 8*mi of a
     // 32-column pair of k16 steps; row n = nt*8 + (lane & 7) (rows >= Bx read
     // row 0: their outputs are discarded).
+    // With ZP, matrix mi = (k16 step s = 2*s2 + (mi >> 1), half mi & 1) reads the
+    // activation copy matching that half's field offset.
     const uint32_t xs_saddr = smem_addr(xs);
-    uint32_t xrow_addr[NT];
+    uint32_t xrow_addr[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) {
         int n = nt * 8 + (lane & 7);
         if (n >= p.Bx) n = 0;
-        xrow_addr[nt] = xs_saddr + (uint32_t)(n * p.xs_stride + 8 * (lane >> 3)) * 2u;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const int mi = lane >> 3;
+            int cp = 0;
+            if constexpr (ZP) {
+                const int sx = 2 * s2 + (mi >> 1), hx = mi & 1;
+                cp = zp_copy_of(R, zp_off<R>(sx, hx));
+            }
+            xrow_addr[nt][s2] =
+                xs_saddr + (uint32_t)(cp * p.xcopy_stride + n * p.xs_stride + 8 * mi) * 2u;
+        }
+    }
+    // Per-group zero-point constants: the same MMA chain as a group of the
+    // main loop, on the all-zero-code fragment, once per CTA.
+    float* zc = reinterpret_cast<float*>(smem + p.cs_off);
+    if constexpr (ZP) {
+        const int ngc = 2 * p.cs;
+        for (int gi = warp; gi < ngc; gi += nwarps) {
+            float cacc[NT][4];
+#pragma unroll
+            for (int w2 = 0; w2 < 2; ++w2)
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    uint32_t bf[NT][4];
+                    const uint32_t xcol = (uint32_t)(gi * 128 + 64 * w2 + 32 * s2);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) ldmatrix_x4(bf[nt], xrow_addr[nt][s2] + xcol * 2u);
+#pragma unroll
+                    for (int sh = 0; sh < 2; ++sh) {
+                        const int s = 2 * s2 + sh;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            if (w2 == 0 && s == 0)
+                                mma_zero(cacc[nt], zp_zero_a<R>(s, 0), zp_zero_a<R>(s, 1), zp_zero_a<R>(s, 2),
+                                         zp_zero_a<R>(s, 3), bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                            else
+                                mma_acc(cacc[nt], zp_zero_a<R>(s, 0), zp_zero_a<R>(s, 1), zp_zero_a<R>(s, 2),
+                                        zp_zero_a<R>(s, 3), bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                        }
+                    }
+                }
+            if (g == 0) {
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    zc[gi * (NT * 8) + nt * 8 + 2 * t] = cacc[nt][0];
+                    zc[gi * (NT * 8) + nt * 8 + 2 * t + 1] = cacc[nt][1];
+                }
+            }
+        }
+        __syncthreads();
     }
 
     float tot[NT][4];
@@ -204,14 +283,14 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             } else {
                 uint32_t S[R];
                 slice_loaded<R, CHILD>(T, S);
-                decode_word<R>(S, A);
+                decode_word<R, ZP>(S, A);
             }
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
                 uint32_t bf[NT][4];
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
-                    ldmatrix_x4(bf[nt], xrow_addr[nt] + (xcol + 64 * w + 32 * s2) * 2u);
+                    ldmatrix_x4(bf[nt], xrow_addr[nt][s2] + (xcol + 64 * w + 32 * s2) * 2u);
 #pragma unroll
                 for (int sh = 0; sh < 2; ++sh) {
                     const int s = 2 * s2 + sh;
@@ -244,10 +323,19 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                     const float s_lo = sc[(w >> 1) * 2], s_hi = sc[(w >> 1) * 2 + 1];
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
-                        tot[nt][0] = fmaf(s_lo, acc[nt][0], tot[nt][0]);
-                        tot[nt][1] = fmaf(s_lo, acc[nt][1], tot[nt][1]);
-                        tot[nt][2] = fmaf(s_hi, acc[nt][2], tot[nt][2]);
-                        tot[nt][3] = fmaf(s_hi, acc[nt][3], tot[nt][3]);
+                        if constexpr (ZP) {
+                            const float* zp = zc + ((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t;
+                            const float c0 = zp[0], c1 = zp[1];
+                            tot[nt][0] = fmaf(s_lo, acc[nt][0] - c0, tot[nt][0]);
+                            tot[nt][1] = fmaf(s_lo, acc[nt][1] - c1, tot[nt][1]);
+                            tot[nt][2] = fmaf(s_hi, acc[nt][2] - c0, tot[nt][2]);
+                            tot[nt][3] = fmaf(s_hi, acc[nt][3] - c1, tot[nt][3]);
+                        } else {
+                            tot[nt][0] = fmaf(s_lo, acc[nt][0], tot[nt][0]);
+                            tot[nt][1] = fmaf(s_lo, acc[nt][1], tot[nt][1]);
+                            tot[nt][2] = fmaf(s_hi, acc[nt][2], tot[nt][2]);
+                            tot[nt][3] = fmaf(s_hi, acc[nt][3], tot[nt][3]);
+                        }
                     }
                 }
             }

@@ -73,8 +73,9 @@ static long long check(const std::vector<uint8_t>& parent, int N, int K) {
         for (int j = 0; j < NPL; ++j) T[j] = planes[(size_t)L.plane_word(rt, st, j, lane, w)];
         uint32_t S[R];
         slice_loaded<R, CHILD>(T, S);
-        uint32_t A[16];
+        uint32_t A[16], Araw[16];
         decode_word<R>(S, A);
+        decode_word<R, true>(S, Araw);
         const int g = lane >> 2, t = lane & 3;
         for (int s = 0; s < 4; ++s)
             for (int q = 0; q < 4; ++q)
@@ -88,6 +89,15 @@ static long long check(const std::vector<uint8_t>& parent, int N, int K) {
                         want = slice_ref(parent[(size_t)row * K + col], R) - (1 << (R - 1));
                     else
                         want = (CHILD ? 0 : slice_ref(0, R)) - (1 << (R - 1));  // pad code 0
+                    if (R != 8) {  // raw (zero-point folded) encoding: 128 + s * 2^o
+                        const float raw = host_bf16(Araw[4 * s + q] >> (16 * h));
+                        const int o = zp_off<R>(s, q >> 1);
+                        const float dec = (raw - 128.0f) / (float)(1 << o) - (float)(1 << (R - 1));
+                        if (dec != (float)want) {
+                            if (bad < 5) std::printf("RAW R=%d row=%d col=%d got %g want %d\n", R, row, col, dec, want);
+                            ++bad;
+                        }
+                    }
                     if (v != (float)want) {
                         if (bad < 5)
                             std::printf("R=%d child=%d row=%d col=%d got %g want %d\n", R, (int)CHILD,
