@@ -14,7 +14,8 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmatq.so")
+# MQ_LIB_PATH: load an alternative build (tuning experiments only)
+LIB_PATH = os.environ.get("MQ_LIB_PATH") or os.path.join(HERE, "libmatq.so")
 
 MQ_OK = 0
 MQ_ERR_INVALID = 1

@@ -162,17 +162,34 @@ MQ_HD uint32_t shl(uint32_t x) {
     return x << S;
 #endif
 }
-template <int S>
-MQ_HD uint32_t shr(uint32_t x) {
+// Right shifts.  Measured on B200 (scripts/micro/op_rate.cu): LOP3, SHF, PRMT
+// and HFMA2 retire 2 warp-instr/cycle/SM, IMAD.HI only 1.  MQ_SHR_MODE picks
+// the implementation for the network (shr) and field extraction (shr_x):
+// 0 = all IMAD.HI, 1 = all SHF, 2 = IMAD.HI in the network + SHF/PRMT in extraction.
+#ifndef MQ_SHR_MODE
+#define MQ_SHR_MODE 1
+#endif
+template <int S, bool IMAD>
+MQ_HD uint32_t shr_impl(uint32_t x) {
     static_assert(S > 0 && S < 32, "shift");
 #ifdef __CUDA_ARCH__
     uint32_t d;
-    asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - S)));
+    if constexpr (IMAD) {
+        asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - S)));
+    } else if constexpr (S == 8) {
+        asm("prmt.b32 %0, %1, 0, 0x4321;" : "=r"(d) : "r"(x));  // bytes >> 8, zero-fill
+    } else {
+        asm("shr.b32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(S));
+    }
     return d;
 #else
     return x >> S;
 #endif
 }
+template <int S>
+MQ_HD uint32_t shr(uint32_t x) { return shr_impl<S, MQ_SHR_MODE != 1>(x); }
+template <int S>
+MQ_HD uint32_t shr_x(uint32_t x) { return shr_impl<S, MQ_SHR_MODE == 0>(x); }
 
 // Field of R bits at bit offset O of both 16-bit halves of w -> bf16x2 of
 // (field - 2^(R-1)), exact.  (w & mask) | 0x4300 is bf16 128 + field*2^O; one
@@ -273,7 +290,7 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         // W_i field n (offset 2n) <-> position 2n + i
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
-            const uint32_t w0 = P[i], w6 = shr<6>(P[i]), w12 = shr<12>(P[i]);
+            const uint32_t w0 = P[i], w6 = shr_x<6>(P[i]), w12 = shr_x<12>(P[i]);
             A[0 + i] = field_out<2, 0, RAW>(w0);
             A[2 + i] = field_out<2, 2, RAW>(w0);
             A[4 + i] = field_out<2, 4, RAW>(w0);
@@ -293,16 +310,16 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         for (int i = 0; i < 4; ++i) {
             const uint32_t w = P[i];
             if constexpr (R == 3) {
-                const uint32_t w8 = shr<8>(w);
+                const uint32_t w8 = shr_x<8>(w);
                 A[0 + i] = field_out<3, 0, RAW>(w);
                 A[4 + i] = field_out<3, 4, RAW>(w);
                 A[8 + i] = field_out<3, 0, RAW>(w8);
                 A[12 + i] = field_out<3, 4, RAW>(w8);
             } else {
                 A[0 + i] = field_out<4, 0, RAW>(w);
-                A[4 + i] = field_out<4, 3, RAW>(shr<1>(w));
-                A[8 + i] = field_out<4, 0, RAW>(shr<8>(w));
-                A[12 + i] = field_out<4, 3, RAW>(shr<9>(w));
+                A[4 + i] = field_out<4, 3, RAW>(shr_x<1>(w));
+                A[8 + i] = field_out<4, 0, RAW>(shr_x<8>(w));
+                A[12 + i] = field_out<4, 3, RAW>(shr_x<9>(w));
             }
         }
     } else {
@@ -316,10 +333,10 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
         for (int i = 0; i < 8; ++i) {
             if constexpr (R == 6) {
                 A[0 + i] = field_out<6, 0, RAW>(P[i]);
-                A[8 + i] = field_out<6, 0, RAW>(shr<8>(P[i]));
+                A[8 + i] = field_out<6, 0, RAW>(shr_x<8>(P[i]));
             } else {
                 A[0 + i] = field8_bf16(P[i]);
-                A[8 + i] = field8_bf16(shr<8>(P[i]));
+                A[8 + i] = field8_bf16(shr_x<8>(P[i]));
             }
         }
     }

@@ -59,7 +59,10 @@ struct GemvParams {
 #define MQ_GEMV_DEBUG 0  // profiling builds: 1 = skip decode, 2 = skip weight loads
 #endif
 
-constexpr int kMaxWarps = 16;
+#ifndef MQ_GEMV_MAX_WARPS
+#define MQ_GEMV_MAX_WARPS 16
+#endif
+constexpr int kMaxWarps = MQ_GEMV_MAX_WARPS;
 
 template <int R, int NT, bool CHILD, int GS>
 __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(const GemvParams p) {
