@@ -314,6 +314,34 @@ def main():
     except Exception:
         pass
 
+    # per-layer-kind breakdown: one CUDA graph of the 32 same-kind launches (PDL)
+    kinds = {}
+    for kind in ("qkv", "o", "gate_up", "down"):
+        pts = [pt for _, k2, pt in stack.layers if k2 == kind]
+        xin = {"qkv": stack.x, "o": stack.bufs["qkv"][:, :pts[0].K], "gate_up": stack.bufs["o"],
+               "down": stack.bufs["gate_up"][:, :pts[0].K]}[kind]
+        outk = {"qkv": stack.bufs["qkv"], "o": stack.bufs["o"], "gate_up": stack.bufs["gate_up"],
+                "down": stack.x}[kind]
+        with torch.cuda.stream(stack.stream):
+            for pt in pts:
+                pt.gemv(xin, r, out=outk, pdl=True, stream=stack.stream)
+        stack.stream.synchronize()
+        gk = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gk, stream=stack.stream):
+            for pt in pts:
+                pt.gemv(xin, r, out=outk, pdl=True, stream=stack.stream)
+        with torch.cuda.stream(stack.stream):
+            gk.replay()
+        def replay_k(g=gk):
+            with torch.cuda.stream(stack.stream):
+                g.replay()
+
+        secs = time_steps(replay_k, 5) / 5 / len(pts)
+        nb = algorithmic_bytes(pts[0].N, pts[0].K, args.batch, r, pts[0].planes_read(r), 128)
+        kinds[kind] = {"us": secs * 1e6, "GBps": nb / secs / 1e9, "frac": nb / secs / 1e9 / peak,
+                       "N": pts[0].N, "K": pts[0].K}
+        del gk
+
     # mode C (materialised children) for the headline r
     mode_c = None
     if r < 8 and world == 1 and not args.no_sweep:
@@ -368,6 +396,7 @@ def main():
                               "stack_frac": v["bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9 / peak}
                      for b, v in results.items()},
         "mode_c_tok_s": mode_c,
+        "per_kind_r%d" % args.bits: kinds,
         "bytes_per_token": bytes_tok,
         "e2e": {"value": args.batch * args.steps / e2e_secs, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
