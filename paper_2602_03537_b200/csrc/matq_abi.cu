@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstring>
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
 
@@ -45,33 +46,46 @@ int sm_count() {
 
 struct GemvConfig {
     int NT, S, cs, grid, nwarps, stages;
+    int stream;  // stream-K assignment
+    long long T;
+    int W, slots;  // stream-K warps, max contributors per row tile
     size_t smem;
     int xs_stride, xs_bytes, xcopy_stride, cs_off;
 };
 
-constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA
+constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA (chunked mode)
+constexpr size_t kXsStream = 100 * 1024;    // full-K staging allowed for stream-K
 constexpr size_t kSmemFullSm = 220 * 1024;
 
-// Decomposition.  One CTA of 8 independent warps per SM.  The
-// K range is cut into S chunks of cs steps; chunk kc is owned by grid/S CTAs
-// whose warps take row tiles round-robin.  S is chosen to minimise the
-// critical path in steps (units per warp x cs) plus a small per-chunk fixup
-// cost, subject to the staged activation chunk fitting kXsMax.
 int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
     return (v && *v) ? atoi(v) : dflt;
 }
 
+int streamk_warp_of(long long u, long long T, int W) { return (int)(((u + 1) * W - 1) / T); }
+
+// Decomposition.  One CTA of `nwarps` independent warps per
+// SM.  The cost of a configuration is the critical path in steps on the most
+// loaded SM sub-partition (4 per SM, warp w on SMSP w % 4), since the decode
+// is issue-bound per SMSP; a split tile adds a fixup (partials + ticket).
+//   chunked (mode 0): K cut into S chunks of cs steps, row tiles dealt
+//     warp-major; every tile of an S > 1 split needs the fixup;
+//   stream-K: each warp owns a balanced contiguous range of the flattened
+//     (row tile, step) space; only tiles cut by a range boundary are fixed up.
+//     Needs the whole K range of X staged.
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
-    // activation copies for zero-point folding (matq_common.cuh ZeroPoint<R>)
-    const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     GemvConfig c{};
+    const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
-    // tuning overrides (scripts/sweep_gemv.py): MQ_GEMV_WARPS, MQ_GEMV_SPLIT, MQ_GEMV_STAGES
-    c.nwarps = std::max(1, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
+    // tuning overrides (scripts/sweep_gemv.py): MQ_GEMV_WARPS, MQ_GEMV_SPLIT, MQ_GEMV_STAGES,
+    // MQ_GEMV_STREAM (0 = never, 1 = force when it fits)
+    c.nwarps = std::max(4, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
+    c.nwarps &= ~3;
+    const int per_smsp = c.nwarps / 4;
     const int force_s = env_int("MQ_GEMV_SPLIT", 0);
-    const double fixup = 2.0;  // a split-K tile costs ~2 steps (partials, ticket, reduction)
+    const int force_stream = env_int("MQ_GEMV_STREAM", -1);
+    const double fixup = 1.0;
     const int sms = sm_count();
     double best = 1e30;
     for (int S = 1; S <= std::min(nsteps, 64); ++S) {
@@ -83,15 +97,50 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
         int cpc = sms / S;
         if (cpc < 1) break;
         cpc = std::min(cpc, n_rt);  // at least one row tile per CTA
-        const int units_per_warp = mq::cdiv(n_rt, cpc * c.nwarps);
-        const double cost = (double)units_per_warp * (cs + (S > 1 ? fixup : 0.0));
+        const int rt_stride = cpc * c.nwarps;
+        int max_units = 0;  // most units on one SMSP of any CTA
+        for (int j = 0; j < cpc; ++j)
+            for (int k = 0; k < 4; ++k) {
+                int u = 0;
+                for (int w = k; w < c.nwarps; w += 4) {
+                    const int first = w * cpc + j;
+                    if (first < n_rt) u += (n_rt - 1 - first) / rt_stride + 1;
+                }
+                max_units = std::max(max_units, u);
+            }
+        const double cost = (double)max_units * (cs + (S > 1 ? fixup : 0.0));
         if (cost < best - 1e-9) {
             best = cost;
             c.S = S;
             c.cs = cs;
             c.grid = cpc * S;
+            c.stream = 0;
         }
     }
+    const size_t xs_full = (size_t)ncopy * Bx * (nsteps * 256 + 8) * 2;
+    if (force_stream != 0 && !force_s && xs_full <= kXsStream && nsteps > 1) {
+        const long long T = (long long)n_rt * nsteps;
+        const int W = sms * c.nwarps;
+        const double q = std::ceil((double)T / W);
+        const double cost = per_smsp * (q + 2 * fixup * (q < nsteps ? 1.0 : 0.5));
+        if (cost < best || force_stream == 1) {
+            best = cost;
+            c.stream = 1;
+            c.S = 1;
+            c.cs = nsteps;
+            c.grid = sms;
+            c.T = T;
+            c.W = W;
+            int slots = 1;
+            for (int rt = 0; rt < n_rt; ++rt) {
+                const int fw = streamk_warp_of((long long)rt * nsteps, T, W);
+                const int lw = streamk_warp_of((long long)rt * nsteps + nsteps - 1, T, W);
+                slots = std::max(slots, lw - fw + 1);
+            }
+            c.slots = slots;
+        }
+    }
+    if (!c.stream) c.slots = c.S;
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
     c.cs_off = (int)(((size_t)ncopy * c.xcopy_stride * 2 + 15) & ~(size_t)15);
@@ -112,8 +161,8 @@ constexpr size_t kTicketBytes = 64 * 1024;
 constexpr int kMaxTickets = (int)(kTicketBytes / sizeof(int));
 
 size_t gemv_ws_bytes(int N, const GemvConfig& c, int B) {
-    if (c.S <= 1) return 0;
-    return kTicketBytes + (size_t)c.S * B * mq::pad16(N) * sizeof(float);
+    if (c.slots <= 1) return 0;
+    return kTicketBytes + (size_t)c.slots * B * mq::pad16(N) * sizeof(float);
 }
 
 mq::GemvLaunchFn gemv_launcher(int r) {
@@ -220,7 +269,13 @@ size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
     if (N < 1 || K < 1 || B < 1) return 0;
     const int Bx = (flags & MQ_X_F32) ? 2 * B : B;
     if (Bx > 32) return 0;
-    return gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, 8, true, 4), B);
+    // the largest requirement over every bit-width / mode / group-size path
+    size_t need = 0;
+    for (int r : {2, 3, 4, 6, 8})
+        for (int npl : {r, std::min(8, r + 1)})
+            for (bool g128 : {true, false})
+                need = std::max(need, gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, npl, g128, r), B));
+    return need;
 }
 
 int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, void* Y, int ldy,
@@ -275,6 +330,9 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     p.S = c.S;
     p.cs = c.cs;
     p.ctas_per_chunk = c.grid / c.S;
+    p.stream = c.stream;
+    p.T = c.T;
+    p.W = c.W;
     p.x_f32 = xf32 ? 1 : 0;
     p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
     p.xs_stride = c.xs_stride;

@@ -159,6 +159,28 @@ def test_shared_workspace_across_shapes_and_batches(mq):
                 assert rel_err(got, want) <= 1e-4, (pt.shape, B)
 
 
+@pytest.mark.parametrize("mode", ["stream", "chunked"])
+def test_gemv_forced_decompositions(mq, mode, monkeypatch):
+    """Stream-K (multi-contributor tiles) and chunked split-K, forced via the
+    tuning overrides, on shapes where tiles split across many warps."""
+    if mode == "stream":
+        monkeypatch.setenv("MQ_GEMV_STREAM", "1")
+    else:
+        monkeypatch.setenv("MQ_GEMV_STREAM", "0")
+        monkeypatch.setenv("MQ_GEMV_SPLIT", "3")
+    for n, k, B in ((40, 600, 1), (256, 4096, 5), (64, 14336, 16), (1000, 2048, 2)):
+        codes, scales = _parent(n, k, seed=n + k + B)
+        pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
+        mq.reserve_workspace(pt.workspace_bytes(B) * 4)
+        X = _x_bf16(B, k, seed=B)
+        Xd = torch.from_numpy(X).cuda().to(torch.bfloat16)
+        for r in LADDER:
+            want = O.parent_matmul_ref(codes, scales, 128, r, X)
+            for _ in range(2):
+                got = pt.gemv(Xd, r, out_dtype=torch.float32).cpu().numpy()
+                assert rel_err(got, want) <= 1e-4, (mode, n, k, B, r)
+
+
 def test_gemv_mode_c_matches_mode_p(mq):
     codes, scales = _parent(128, 2048, seed=31)
     pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
