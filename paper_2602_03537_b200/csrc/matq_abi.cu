@@ -6,7 +6,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <tuple>
 
 #include "../../include/matq.h"
 #include "matq_gemv.cuh"
@@ -85,7 +87,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
     const int per_smsp = c.nwarps / 4;
     const int force_s = env_int("MQ_GEMV_SPLIT", 0);
     const int force_stream = env_int("MQ_GEMV_STREAM", -1);
-    const double fixup = 1.0;
+    const double fixup = 1.0, stream_fixup = 3.0;  // measured: a stream-K split costs ~3 steps
     const int sms = sm_count();
     double best = 1e30;
     for (int S = 1; S <= std::min(nsteps, 64); ++S) {
@@ -98,16 +100,13 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
         if (cpc < 1) break;
         cpc = std::min(cpc, n_rt);  // at least one row tile per CTA
         const int rt_stride = cpc * c.nwarps;
-        int max_units = 0;  // most units on one SMSP of any CTA
-        for (int j = 0; j < cpc; ++j)
-            for (int k = 0; k < 4; ++k) {
-                int u = 0;
-                for (int w = k; w < c.nwarps; w += 4) {
-                    const int first = w * cpc + j;
-                    if (first < n_rt) u += (n_rt - 1 - first) / rt_stride + 1;
-                }
-                max_units = std::max(max_units, u);
-            }
+        // most units on one SMSP: CTA 0, SMSP 0 (warps 0, 4, 8, ... take the
+        // lowest tile indices, and a warp's unit count is non-increasing in it)
+        int max_units = 0;
+        for (int w = 0; w < c.nwarps; w += 4) {
+            const int first = w * cpc;
+            if (first < n_rt) max_units += (n_rt - 1 - first) / rt_stride + 1;
+        }
         const double cost = (double)max_units * (cs + (S > 1 ? fixup : 0.0));
         if (cost < best - 1e-9) {
             best = cost;
@@ -118,11 +117,15 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
         }
     }
     const size_t xs_full = (size_t)ncopy * Bx * (nsteps * 256 + 8) * 2;
-    if (force_stream != 0 && !force_s && xs_full <= kXsStream && nsteps > 1) {
-        const long long T = (long long)n_rt * nsteps;
+    const long long T_all = (long long)n_rt * nsteps;
+    // stream-K needs every warp to own >= 1 step (contributors of a tile are
+    // then consecutive warps)
+    if (force_stream != 0 && !force_s && xs_full <= kXsStream && nsteps > 1 &&
+        T_all >= (long long)sms * c.nwarps) {
+        const long long T = T_all;
         const int W = sms * c.nwarps;
         const double q = std::ceil((double)T / W);
-        const double cost = per_smsp * (q + 2 * fixup * (q < nsteps ? 1.0 : 0.5));
+        const double cost = per_smsp * (q + 2 * stream_fixup);
         if (cost < best || force_stream == 1) {
             best = cost;
             c.stream = 1;
@@ -163,6 +166,30 @@ constexpr int kMaxTickets = (int)(kTicketBytes / sizeof(int));
 size_t gemv_ws_bytes(int N, const GemvConfig& c, int B) {
     if (c.slots <= 1) return 0;
     return kTicketBytes + (size_t)c.slots * B * mq::pad16(N) * sizeof(float);
+}
+
+// Configurations are pure functions of (shape, batch, path, overrides): cache them.
+struct CfgKey {
+    int N, K, Bx, npl, g128, r, w, s, st, sk;
+    bool operator<(const CfgKey& o) const {
+        return std::tie(N, K, Bx, npl, g128, r, w, s, st, sk) <
+               std::tie(o.N, o.K, o.Bx, o.npl, o.g128, o.r, o.w, o.s, o.st, o.sk);
+    }
+};
+GemvConfig cached_config(int N, int K, int Bx, int npl, bool g128, int r) {
+    static std::mutex mu;
+    static std::map<CfgKey, GemvConfig> cache;
+    const CfgKey key{N, K, Bx, npl, (int)g128, r, env_int("MQ_GEMV_WARPS", 0), env_int("MQ_GEMV_SPLIT", 0),
+                     env_int("MQ_GEMV_STAGES", 0), env_int("MQ_GEMV_STREAM", -1)};
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    const GemvConfig c = choose_gemv_config(N, K, Bx, npl, g128, r);
+    std::lock_guard<std::mutex> lk(mu);
+    cache[key] = c;
+    return c;
 }
 
 mq::GemvLaunchFn gemv_launcher(int r) {
@@ -274,7 +301,7 @@ size_t mq_gemv_workspace_bytes(int N, int K, int B, int flags) {
     for (int r : {2, 3, 4, 6, 8})
         for (int npl : {r, std::min(8, r + 1)})
             for (bool g128 : {true, false})
-                need = std::max(need, gemv_ws_bytes(N, choose_gemv_config(N, K, Bx, npl, g128, r), B));
+                need = std::max(need, gemv_ws_bytes(N, cached_config(N, K, Bx, npl, g128, r), B));
     return need;
 }
 
@@ -295,7 +322,7 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
 
     const bool child_mode = nplanes == r;
     const int npl = (child_mode || r == 8) ? r : r + 1;
-    const GemvConfig c = choose_gemv_config(N, K, Bx, npl, G == 128, r);
+    const GemvConfig c = cached_config(N, K, Bx, npl, G == 128, r);
     const size_t need = gemv_ws_bytes(N, c, B);
     if (need > workspace_bytes || (need && !workspace))
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);

@@ -59,6 +59,16 @@ class _Workspaces:
 
 
 WORKSPACES = _Workspaces()
+_WS_NEED: dict[tuple[int, int, int, int], int] = {}
+
+
+def gemv_workspace_bytes(N: int, K: int, B: int, flags: int) -> int:
+    """Cached mq_gemv_workspace_bytes (the launch path calls it every GEMV)."""
+    key = (N, K, B, flags & _lib.MQ_X_F32)
+    v = _WS_NEED.get(key)
+    if v is None:
+        v = _WS_NEED[key] = _lib.lib().mq_gemv_workspace_bytes(N, K, B, flags)
+    return v
 
 
 def reserve_workspace(nbytes: int, stream=None) -> None:
@@ -213,7 +223,7 @@ class PlaneTensor:
         if pdl:
             flags |= _lib.MQ_PDL
         sp = _lib.stream_ptr(stream)
-        need = _lib.lib().mq_gemv_workspace_bytes(self.N, self.K, B, flags)
+        need = gemv_workspace_bytes(self.N, self.K, B, flags)
         ws = WORKSPACES.get(need, sp)
         _lib.call("mq_gemv", _lib.ptr(self.blob), _lib.ptr(self.tscales), _lib.ptr(X), X.stride(0),
                   _lib.ptr(out), out.stride(0), B, self.N, self.K, self.G, self.nplanes, r, scale,

@@ -41,6 +41,7 @@ def main():
     splits = os.environ.get("SPLITS", "0").split(",")
     shapes = os.environ.get("SHAPES", "qkv,o,gate_up,down").split(",")
     debugs = os.environ.get("DEBUGS", "0").split(",")
+    streams = os.environ.get("STREAMS", "-1").split(",")
     res = []
     for name in shapes:
         N, K = SHAPES[name]
@@ -49,13 +50,14 @@ def main():
             X = torch.randn(B, K, device="cuda").to(torch.bfloat16)
             out = torch.empty(B, N, device="cuda", dtype=torch.bfloat16)
             mq.reserve_workspace(max(pt.workspace_bytes(B) for pt in pts) * 64 + (1 << 22))
-            for r, w, d, s, dbg in itertools.product(bits, warps, stages, splits, debugs):
+            for r, w, d, s, dbg, sk in itertools.product(bits, warps, stages, splits, debugs, streams):
                 os.environ["MQ_GEMV_WARPS"], os.environ["MQ_GEMV_STAGES"] = w, d
                 os.environ["MQ_GEMV_SPLIT"], os.environ["MQ_GEMV_DEBUG"] = s, dbg
+                os.environ["MQ_GEMV_STREAM"] = sk
                 us = time_cfg(pts, X, out, r)
                 gb = algorithmic_bytes(N, K, B, r, pts[0].planes_read(r)) / (us * 1e-6) / 1e9
                 rec = {"layer": name, "N": N, "K": K, "B": B, "r": r, "warps": int(w), "stages": int(d),
-                       "split": int(s), "debug": int(dbg), "us": round(us, 2), "GBps": round(gb, 1)}
+                       "split": int(s), "debug": int(dbg), "stream": int(sk), "us": round(us, 2), "GBps": round(gb, 1)}
                 res.append(rec)
                 print(json.dumps(rec), flush=True)
         del pts

@@ -168,7 +168,7 @@ def test_gemv_forced_decompositions(mq, mode, monkeypatch):
     else:
         monkeypatch.setenv("MQ_GEMV_STREAM", "0")
         monkeypatch.setenv("MQ_GEMV_SPLIT", "3")
-    for n, k, B in ((40, 600, 1), (256, 4096, 5), (64, 14336, 16), (1000, 2048, 2)):
+    for n, k, B in ((40, 600, 1), (256, 4096, 5), (4096, 4096, 1), (2048, 14336, 3), (4000, 4352, 16)):
         codes, scales = _parent(n, k, seed=n + k + B)
         pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
         mq.reserve_workspace(pt.workspace_bytes(B) * 4)
