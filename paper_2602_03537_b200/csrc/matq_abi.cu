@@ -75,7 +75,8 @@ int streamk_warp_of(long long u, long long T, int W) { return (int)(((u + 1) * W
 //   stream-K: each warp owns a balanced contiguous range of the flattened
 //     (row tile, step) space; only tiles cut by a range boundary are fixed up.
 //     Needs the whole K range of X staged.
-GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
+GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
+                              bool honour_overrides = true) {
     GemvConfig c{};
     const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
@@ -85,8 +86,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
     c.nwarps = std::max(4, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
     c.nwarps &= ~3;
     const int per_smsp = c.nwarps / 4;
-    const int force_s = env_int("MQ_GEMV_SPLIT", 0);
-    const int force_stream = env_int("MQ_GEMV_STREAM", -1);
+    const int force_s = honour_overrides ? env_int("MQ_GEMV_SPLIT", 0) : 0;
+    const int force_stream = honour_overrides ? env_int("MQ_GEMV_STREAM", -1) : -1;
     const double fixup = 1.0, stream_fixup = 3.0;  // measured: a stream-K split costs ~3 steps
     const int sms = sm_count();
     double best = 1e30;
@@ -143,6 +144,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r) {
             c.slots = slots;
         }
     }
+    if (c.S == 0)  // overrides admitted no configuration: ignore them
+        return choose_gemv_config(N, K, Bx, npl, g128, r, false);
     if (!c.stream) c.slots = c.S;
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
