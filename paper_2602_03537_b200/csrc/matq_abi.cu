@@ -48,15 +48,12 @@ int sm_count() {
 
 struct GemvConfig {
     int NT, S, cs, grid, nwarps, stages;
-    int stream;  // stream-K assignment
-    long long T;
-    int W, slots;  // stream-K warps, max contributors per row tile
+    int slots;  // partial-sum slots per row tile (= S)
     size_t smem;
     int xs_stride, xs_bytes, xcopy_stride, cs_off;
 };
 
 constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA (chunked mode)
-constexpr size_t kXsStream = 100 * 1024;    // full-K staging allowed for stream-K
 constexpr size_t kSmemFullSm = 220 * 1024;
 
 int env_int(const char* name, int dflt) {
@@ -64,17 +61,14 @@ int env_int(const char* name, int dflt) {
     return (v && *v) ? atoi(v) : dflt;
 }
 
-int streamk_warp_of(long long u, long long T, int W) { return (int)(((u + 1) * W - 1) / T); }
-
 // Decomposition.  One CTA of `nwarps` independent warps per
 // SM.  The cost of a configuration is the critical path in steps on the most
 // loaded SM sub-partition (4 per SM, warp w on SMSP w % 4), since the decode
 // is issue-bound per SMSP; a split tile adds a fixup (partials + ticket).
-//   chunked (mode 0): K cut into S chunks of cs steps, row tiles dealt
-//     warp-major; every tile of an S > 1 split needs the fixup;
-//   stream-K: each warp owns a balanced contiguous range of the flattened
-//     (row tile, step) space; only tiles cut by a range boundary are fixed up.
-//     Needs the whole K range of X staged.
+// K is cut into S chunks of cs steps, row tiles dealt warp-major; every tile
+// of an S > 1 split needs the fixup.  (A stream-K assignment -- balanced
+// contiguous per-warp ranges -- was measured and lost to the fixups; see
+// DESIGN.md 4.)
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
                               bool honour_overrides = true) {
     GemvConfig c{};
@@ -85,10 +79,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     // MQ_GEMV_STREAM (0 = never, 1 = force when it fits)
     c.nwarps = std::max(4, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
     c.nwarps &= ~3;
-    const int per_smsp = c.nwarps / 4;
     const int force_s = honour_overrides ? env_int("MQ_GEMV_SPLIT", 0) : 0;
-    const int force_stream = honour_overrides ? env_int("MQ_GEMV_STREAM", -1) : -1;
-    const double fixup = 1.0, stream_fixup = 3.0;  // measured: a stream-K split costs ~3 steps
+    const double fixup = 2.0;  // measured: a split-K tile costs ~2 steps (partials, ticket, reduction)
     const int sms = sm_count();
     double best = 1e30;
     for (int S = 1; S <= std::min(nsteps, 64); ++S) {
@@ -114,39 +106,11 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
             c.S = S;
             c.cs = cs;
             c.grid = cpc * S;
-            c.stream = 0;
-        }
-    }
-    const size_t xs_full = (size_t)ncopy * Bx * (nsteps * 256 + 8) * 2;
-    const long long T_all = (long long)n_rt * nsteps;
-    // stream-K needs every warp to own >= 1 step (contributors of a tile are
-    // then consecutive warps)
-    if (force_stream != 0 && !force_s && xs_full <= kXsStream && nsteps > 1 &&
-        T_all >= (long long)sms * c.nwarps) {
-        const long long T = T_all;
-        const int W = sms * c.nwarps;
-        const double q = std::ceil((double)T / W);
-        const double cost = per_smsp * (q + 2 * stream_fixup);
-        if (cost < best || force_stream == 1) {
-            best = cost;
-            c.stream = 1;
-            c.S = 1;
-            c.cs = nsteps;
-            c.grid = sms;
-            c.T = T;
-            c.W = W;
-            int slots = 1;
-            for (int rt = 0; rt < n_rt; ++rt) {
-                const int fw = streamk_warp_of((long long)rt * nsteps, T, W);
-                const int lw = streamk_warp_of((long long)rt * nsteps + nsteps - 1, T, W);
-                slots = std::max(slots, lw - fw + 1);
-            }
-            c.slots = slots;
         }
     }
     if (c.S == 0)  // overrides admitted no configuration: ignore them
         return choose_gemv_config(N, K, Bx, npl, g128, r, false);
-    if (!c.stream) c.slots = c.S;
+    c.slots = c.S;
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
     c.cs_off = (int)(((size_t)ncopy * c.xcopy_stride * 2 + 15) & ~(size_t)15);
@@ -183,7 +147,7 @@ GemvConfig cached_config(int N, int K, int Bx, int npl, bool g128, int r) {
     static std::mutex mu;
     static std::map<CfgKey, GemvConfig> cache;
     const CfgKey key{N, K, Bx, npl, (int)g128, r, env_int("MQ_GEMV_WARPS", 0), env_int("MQ_GEMV_SPLIT", 0),
-                     env_int("MQ_GEMV_STAGES", 0), env_int("MQ_GEMV_STREAM", -1)};
+                     env_int("MQ_GEMV_STAGES", 0), 0};
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
@@ -360,9 +324,6 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     p.S = c.S;
     p.cs = c.cs;
     p.ctas_per_chunk = c.grid / c.S;
-    p.stream = c.stream;
-    p.T = c.T;
-    p.W = c.W;
     p.x_f32 = xf32 ? 1 : 0;
     p.y_f32 = (flags & MQ_Y_F32) ? 1 : 0;
     p.xs_stride = c.xs_stride;

@@ -44,11 +44,8 @@ struct GemvParams {
     int B;                    // logical batch rows
     int Bx;                   // activation rows in the mma N dim (2B when x_f32)
     int N, Np, K, Kp, G, ngp, nsteps, n_rt;
-    int S, cs;                // K chunks, steps per chunk (mode 0)
+    int S, cs;                // K chunks, steps per chunk
     int ctas_per_chunk;       // gridDim.x / S
-    int stream;               // 1: stream-K -- warp gw owns steps [gw*T/W, (gw+1)*T/W)
-    long long T;              // stream-K: total steps n_rt * nsteps
-    int W;                    // stream-K: warps in the grid
     int x_f32;                // X is fp32 (split into hi + lo bf16 rows)
     int y_f32;                // Y is fp32
     int xs_stride;            // smem X row stride (elements)
@@ -82,26 +79,14 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     const int nwarps = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, t = lane & 3;
-    // Work assignment.  Mode 0 (chunked): CTAs with blockIdx % S == kc own K
-    // chunk kc and deal row tiles warp-major, so every SM gets work.
-    // Stream-K: warp gw owns the flattened (row tile, step) range
-    // [gw*T/W, (gw+1)*T/W) -- balanced to one step, and contiguous in the blob.
-    const int kc = p.stream ? 0 : blockIdx.x % p.S, j = p.stream ? 0 : blockIdx.x / p.S;
+    const int kc = blockIdx.x % p.S, j = blockIdx.x / p.S;
     const int chunk0 = kc * p.cs;
     const int ns = max(0, min(chunk0 + p.cs, p.nsteps) - chunk0);
-    const int gw = blockIdx.x * nwarps + warp;
-    const long long u0 = p.stream ? (long long)gw * p.T / p.W : 0;
-    int rt_first = warp * p.ctas_per_chunk + j, st_first = chunk0;
+    // row tiles dealt warp-major across the chunk's CTAs, so every SM gets work
+    const int rt_first = warp * p.ctas_per_chunk + j;
     const int rt_stride = p.ctas_per_chunk * nwarps;
-    int total;
-    if (p.stream) {
-        total = (int)((long long)(gw + 1) * p.T / p.W - u0);
-        rt_first = (int)(u0 / p.nsteps);
-        st_first = (int)(u0 - (long long)rt_first * p.nsteps);
-    } else {
-        const int n_units = (rt_first < p.n_rt && ns > 0) ? (p.n_rt - 1 - rt_first) / rt_stride + 1 : 0;
-        total = n_units * ns;  // flattened (unit, step) sequence of this warp
-    }
+    const int n_units = (rt_first < p.n_rt && ns > 0) ? (p.n_rt - 1 - rt_first) / rt_stride + 1 : 0;
+    const int total = n_units * ns;  // flattened (unit, step) sequence of this warp
 
     // ---- per-warp TMA ring --------------------------------------------------
     const int D = p.stages;
@@ -119,16 +104,15 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     // One bulk copy per step: [scales][planes 0..NPL-1] are contiguous at the
     // head of the (rt, st) block.  The issue cursor advances incrementally.
     const uint32_t skip_words = (uint32_t)(p.sb_words - kScaleBytes / 4);  // scale words not needed
-    const uint32_t* issue_ptr = p.blob + ((long long)rt_first * p.nsteps + st_first) * p.step_words + skip_words;
+    const uint32_t* issue_ptr = p.blob + ((long long)rt_first * p.nsteps + chunk0) * p.step_words + skip_words;
     int issue_li = 0, issue_stage = 0;
-    const long long unit_jump = p.stream ? 0 : ((long long)rt_stride * p.nsteps - ns) * p.step_words;
-    const int issue_ns = p.stream ? (1 << 30) : ns;
+    const long long unit_jump = ((long long)rt_stride * p.nsteps - ns) * p.step_words;
     auto issue_next = [&]() {  // lane 0 only
         const uint32_t bar = my_bar0 + 8 * issue_stage;
         mbar_expect_tx(bar, kStageBytes);
         bulk_g2s(my_ring0 + issue_stage * kStageBytes, issue_ptr, kStageBytes, bar, policy);
         issue_ptr += p.step_words;
-        if (++issue_li == issue_ns) {
+        if (++issue_li == ns) {
             issue_li = 0;
             issue_ptr += unit_jump;
         }
@@ -370,9 +354,6 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         else
             reinterpret_cast<uint16_t*>(p.Y)[(long long)b * p.ldy + row] = f32_to_bf16_rn(v);
     };
-    // Stream-K fixup bookkeeping: the warp owning step u is
-    // floor(((u+1) W - 1) / T); a tile's contributors are consecutive warps.
-    auto warp_of = [&](long long u) -> int { return (int)(((u + 1) * p.W - 1) / p.T); };
     auto finalize = [&](int rt) {
         if constexpr (GS == 0) flush_generic();
         const int r0 = rt * kTileRows + g;
@@ -395,15 +376,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                 bcol[nt][1] = 1 << 30;  // no second column
             }
         }
-        // contributors of this tile: the S chunk owners (mode 0), or the
-        // consecutive stream-K warps whose ranges intersect it
-        int slot = kc, nparts = p.S;
-        if (p.stream) {
-            const int fw = warp_of((long long)rt * p.nsteps), lw = warp_of((long long)rt * p.nsteps + p.nsteps - 1);
-            slot = gw - fw;
-            nparts = lw - fw + 1;
-        }
-        if (nparts == 1) {
+        if (p.S == 1) {
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -423,13 +396,13 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                 for (int c = 0; c < 2; ++c) {
                     const int row = r0 + 8 * h, b = bcol[nt][c];
                     if (b < p.B && row < p.N)
-                        p.ws[((long long)slot * p.B + b) * p.Np + row] = v[nt][h][c];
+                        p.ws[((long long)kc * p.B + b) * p.Np + row] = v[nt][h][c];
                 }
         // publish: warp barrier orders all lanes' partials before lane 0's
         // release-RMW on the tile ticket; the last arriver acquires.
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = (atom_add_acq_rel(p.tickets + rt, 1) == nparts - 1);
+        if (lane == 0) last = (atom_add_acq_rel(p.tickets + rt, 1) == p.S - 1);
         last = __shfl_sync(0xffffffffu, last, 0);
         if (!last) return;
 #pragma unroll
@@ -444,12 +417,12 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                         const long long cstride = (long long)p.B * p.Np;
                         float s = 0.0f;
                         int q = 0;
-                        for (; q + 4 <= nparts; q += 4) {  // independent loads, ordered sum
+                        for (; q + 4 <= p.S; q += 4) {  // independent loads, ordered sum
                             const float a0 = __ldcg(wp + q * cstride), a1 = __ldcg(wp + (q + 1) * cstride);
                             const float a2 = __ldcg(wp + (q + 2) * cstride), a3 = __ldcg(wp + (q + 3) * cstride);
                             s += a0; s += a1; s += a2; s += a3;
                         }
-                        for (; q < nparts; ++q) s += __ldcg(wp + q * cstride);
+                        for (; q < p.S; ++q) s += __ldcg(wp + q * cstride);
                         store_y(b, row, s);
                     }
                 }
@@ -457,11 +430,11 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         if (lane == 0) p.tickets[rt] = 0;
     };
 
-    int li = 0, stage = 0, rt = rt_first, st = st_first;
+    int li = 0, stage = 0, rt = rt_first;
     uint32_t parity = 0;
-    const int st_last = p.stream ? p.nsteps - 1 : chunk0 + ns - 1;
 #pragma unroll 1
     for (int f = 0; f < total; ++f) {
+        const int st = chunk0 + li;
         if (li == 0) {
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
@@ -491,19 +464,10 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             issue_next();
         }
         process(buf, sc, st);
-        ++li;
-        if (st == st_last || f == total - 1) {
+        if (++li == ns) {
             finalize(rt);
             li = 0;
-            if (p.stream) {
-                ++rt;
-                st = 0;
-            } else {
-                rt += rt_stride;
-                st = chunk0;
-            }
-        } else {
-            ++st;
+            rt += rt_stride;
         }
         if (++stage == D) {
             stage = 0;

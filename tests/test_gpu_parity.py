@@ -159,15 +159,11 @@ def test_shared_workspace_across_shapes_and_batches(mq):
                 assert rel_err(got, want) <= 1e-4, (pt.shape, B)
 
 
-@pytest.mark.parametrize("mode", ["stream", "chunked"])
-def test_gemv_forced_decompositions(mq, mode, monkeypatch):
-    """Stream-K (multi-contributor tiles) and chunked split-K, forced via the
-    tuning overrides, on shapes where tiles split across many warps."""
-    if mode == "stream":
-        monkeypatch.setenv("MQ_GEMV_STREAM", "1")
-    else:
-        monkeypatch.setenv("MQ_GEMV_STREAM", "0")
-        monkeypatch.setenv("MQ_GEMV_SPLIT", "3")
+@pytest.mark.parametrize("split", ["3", "5"])
+def test_gemv_forced_decompositions(mq, split, monkeypatch):
+    """Chunked split-K forced via the tuning override (uneven chunks, tickets
+    with several contributors), including configurations it cannot honour."""
+    monkeypatch.setenv("MQ_GEMV_SPLIT", split)
     for n, k, B in ((40, 600, 1), (256, 4096, 5), (4096, 4096, 1), (2048, 14336, 3), (4000, 4352, 16)):
         codes, scales = _parent(n, k, seed=n + k + B)
         pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
