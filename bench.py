@@ -110,8 +110,8 @@ class CpuReference:
     as kernels/_core.pyx:24-64 drives it), rows spread over `threads` host
     threads (the kernel walks rows independently, packed_kernels.c:88; ctypes
     releases the GIL).  r in {6,8}: the reference has no packed kernel
-    (matmul.py:223-224); its bench baseline, a dense fp32 GEMV on the
-    dequantised child (matmul.py:332-333), is used instead.
+    (matmul.py:55-56); its bench baseline, a dense fp32 GEMV on the
+    dequantised child (matmul.py:164-165), is used instead.
     Preparation (slice + pack) is untimed, as in the reference bench.
     """
 

@@ -20,7 +20,7 @@
  *     MQ_ERR_CODE_RANGE, as the reference validates synchronously.
  *   - Return value: MQ_OK or an MQ_ERR_* status; mq_last_error() gives a
  *     thread-local message (replaces the reference's Python-side exception
- *     texts, matmul.py:106-109, slicing.py:58-64, which the Python layer
+ *     texts, matmul.py:106-109, slicing.py:22-28, which the Python layer
  *     keeps verbatim).
  *
  * Device layout: a "blob" of uint32 blocks, one per (16-row
@@ -75,7 +75,7 @@ MQ_API size_t mq_tscales_bytes(int N, int K, int G);
 
 /* K1: codes (N, K) uint8 with `nbits` significant bits (8 for the int8
  * parent, r for a child) + group scales (N, ceil(K/G)) fp32 row-major
- * (QuantGrid.scales, grid.py:293) -> blob (+ tscales, required when
+ * (QuantGrid.scales, grid.py:75) -> blob (+ tscales, required when
  * G != 128).  Replaces the reference's child packer pack() (packing.py:81-110)
  * and its raw-byte parent storage (checkpoint.py:66-75) with one device
  * layout. */
@@ -84,14 +84,14 @@ MQ_API int mq_pack_blob(const uint8_t* codes, long long ldc, int N, int K, int n
 
 /* K2a: r-bit sliced codes (N, K) uint8 from a blob of `nplanes` planes, with
  * the bitsliced slice the GEMV uses (nplanes == r: the blob is a child).
- * Replaces slice_to_code over a layer (slicing.py:87-90, slice_layer
+ * Replaces slice_to_code over a layer (slicing.py:51-54, slice_layer
  * :158-171). */
 MQ_API int mq_slice(const uint32_t* blob, int N, int K, int G, int nplanes, int r,
                     uint8_t* codes_out, long long ldo, void* stream);
 
 /* K2b: decode through the exact GEMV register path.  vals_out (optional):
  * int8 s - 2^(r-1); w_out (optional): fp32 (s - z) * scale * out_scale, i.e.
- * PackedLayer.dense_f32 (matmul.py:232-237) when out_scale = 2^(c-r). */
+ * PackedLayer.dense_f32 (matmul.py:64-69) when out_scale = 2^(c-r). */
 MQ_API int mq_dequant(const uint32_t* blob, const float* tscales, int N, int K, int G, int nplanes,
                       int r, float out_scale, int8_t* vals_out, float* w_out, long long ldw,
                       void* stream);
@@ -119,21 +119,21 @@ MQ_API int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, in
 
 /* ---- format-layer helpers behind the drop-in Python API --------------- */
 
-/* slice_code / slice_to_code (slicing.py:67-90) over n codes at master
+/* slice_code / slice_to_code (slicing.py:31-54) over n codes at master
  * bit-width c; err_dev: one device int of scratch.  Synchronises. */
 MQ_API int mq_slice_elementwise(const uint8_t* q, long long n, int c, int r, int on_master,
                          uint8_t* out, int* err_dev, void* stream);
 
-/* dequant (grid.py:346-367) in float64.  Synchronises. */
+/* dequant (grid.py:128-149) in float64.  Synchronises. */
 MQ_API int mq_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int ng, int G, int c,
                    int r, double* out, int* err_dev, void* stream);
 
-/* dequant_value (grid.py:346-358): out[i] = scale[i] * (2^(c-r) * (q[i] - 2^(r-1)))
+/* dequant_value (grid.py:128-140): out[i] = scale[i] * (2^(c-r) * (q[i] - 2^(r-1)))
  * with a per-element float64 scale.  Synchronises. */
 MQ_API int mq_dequant_value_f64(const uint8_t* q, const double* scale, long long n, int c, int r,
                                 double* out, int* err_dev, void* stream);
 
-/* matmul_ref (matmul.py:253-260), bit-exact float32 k-ascending. */
+/* matmul_ref (matmul.py:85-92), bit-exact float32 k-ascending. */
 MQ_API int mq_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y, void* stream);
 
 /* The reference's child bit-plane layout (packing.py:81-126).  Synchronises. */

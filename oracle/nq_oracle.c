@@ -13,7 +13,7 @@
  * test_grid.py:83-93 in the reference tree).
  *
  * Build with -ffp-contract=off: matmul_ref's numpy loop rounds the product
- * and the sum separately (matmul.py:258-259), an FMA would not.
+ * and the sum separately (matmul.py:90-91), an FMA would not.
  */
 #include <stdint.h>
 #include <stddef.h>
@@ -23,7 +23,7 @@
 #define OQ_BAD_ARGS 1
 #define OQ_CODE_RANGE 2
 
-/* slicing.py:58-64 (_check_slice_args): 2 <= c <= 8, r <= c, r >= 2. */
+/* slicing.py:22-28 (_check_slice_args): 2 <= c <= 8, r <= c, r >= 2. */
 int oq_check_slice_args(int c, int r) {
     if (c < 2 || c > 8) return OQ_BAD_ARGS;
     if (r > c) return OQ_BAD_ARGS;
@@ -31,8 +31,8 @@ int oq_check_slice_args(int c, int r) {
     return OQ_OK;
 }
 
-/* slicing.py:67-84 (slice_code): min((q + 2^(k-1)) >> k, 2^r - 1) << k with
- * k = c - r; identity when k == 0.  slicing.py:87-90 (slice_to_code) drops
+/* slicing.py:31-48 (slice_code): min((q + 2^(k-1)) >> k, 2^r - 1) << k with
+ * k = c - r; identity when k == 0.  slicing.py:51-54 (slice_to_code) drops
  * the final << k.  `on_master` selects slice_code (1) or slice_to_code (0). */
 int oq_slice(const uint8_t* q, int64_t n, int c, int r, int on_master, uint8_t* out) {
     int st = oq_check_slice_args(c, r);
@@ -40,7 +40,7 @@ int oq_slice(const uint8_t* q, int64_t n, int c, int r, int on_master, uint8_t* 
     const int k = c - r;
     const int qmax = (1 << c) - 1;
     for (int64_t i = 0; i < n; i++)
-        if (q[i] > qmax) return OQ_CODE_RANGE; /* slicing.py:75-76 */
+        if (q[i] > qmax) return OQ_CODE_RANGE; /* slicing.py:39-40 */
     for (int64_t i = 0; i < n; i++) {
         int v = q[i];
         if (k > 0) {
@@ -53,15 +53,15 @@ int oq_slice(const uint8_t* q, int64_t n, int c, int r, int on_master, uint8_t* 
     return OQ_OK;
 }
 
-/* slicing.py:163 (slice_layer scales): scales * float32(2^(c-r)), exact. */
+/* slicing.py:127 (slice_layer scales): scales * float32(2^(c-r)), exact. */
 void oq_scale_eff(const float* scales, int64_t n, int c, int r, float* out) {
     const float f = (float)(1 << (c - r));
     for (int64_t i = 0; i < n; i++) out[i] = scales[i] * f;
 }
 
-/* grid.py:346-358 (dequant_value) + grid.py:361-367 (dequant): float64
+/* grid.py:128-140 (dequant_value) + grid.py:143-149 (dequant): float64
  * scale * (2^(c-r) * (code - 2^(r-1))), scale expanded per column by
- * grid.py:313-316 (column_scales, col // G).  codes (N,K) r-bit, scales
+ * grid.py:95-98 (column_scales, col // G).  codes (N,K) r-bit, scales
  * (N, ng) fp32 master-grid scales, out (N,K) float64. */
 int oq_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int ng,
                    int G, int c, int r, double* out) {
@@ -71,16 +71,16 @@ int oq_dequant_f64(const uint8_t* codes, int N, int K, const float* scales, int 
     for (int i = 0; i < N; i++)
         for (int j = 0; j < K; j++) {
             int q = codes[(size_t)i * K + j];
-            if (q > (1 << r) - 1) return OQ_CODE_RANGE; /* grid.py:353-354 */
+            if (q > (1 << r) - 1) return OQ_CODE_RANGE; /* grid.py:135-136 */
             double s = (double)scales[(size_t)i * ng + j / G];
             out[(size_t)i * K + j] = s * (double)(step * ((int64_t)q - zr));
         }
     return OQ_OK;
 }
 
-/* matmul.py:232-237 (PackedLayer.dense_f32): (float32(code) - float32(z)) *
+/* matmul.py:64-69 (PackedLayer.dense_f32): (float32(code) - float32(z)) *
  * scales_eff[:, col // G], one float32 rounding.  scales_eff are the child's
- * effective scales (slicing.py:163). */
+ * effective scales (slicing.py:127). */
 void oq_dense_f32(const uint8_t* codes, int N, int K, const float* scales_eff, int ng,
                   int G, int r, float* W) {
     const float z = (float)(1 << (r - 1));
@@ -91,7 +91,7 @@ void oq_dense_f32(const uint8_t* codes, int N, int K, const float* scales_eff, i
         }
 }
 
-/* matmul.py:253-260 (matmul_ref): Y = 0; for k ascending:
+/* matmul.py:85-92 (matmul_ref): Y = 0; for k ascending:
  * Y += X[:, k][:, None] * Wd[:, k][None, :]  -- float32 product, then
  * float32 add, in that order (no FMA). */
 void oq_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y) {
@@ -109,9 +109,9 @@ void oq_matmul_ref(const float* X, int B, int K, const float* W, int N, float* Y
 }
 
 /* Dense float32 GEMV/GEMM, one thread: the reference bench's baseline
- * `X @ Wd.T` under threadpool_limits(1) (matmul.py:332-333).  Row-dot order
+ * `X @ Wd.T` under threadpool_limits(1) (matmul.py:164-165).  Row-dot order
  * (BLAS-like); used only as the CPU timing baseline for r in {6, 8}, which
- * have no packed kernel in the reference (matmul.py:223-224). */
+ * have no packed kernel in the reference (matmul.py:55-56). */
 void oq_dense_gemm_f32(const float* X, int B, int K, const float* W, int N, float* Y) {
     for (int b = 0; b < B; b++) {
         const float* xb = X + (size_t)b * K;
@@ -176,10 +176,10 @@ void oq_unpack_child(const uint64_t* base, const uint32_t* b2, const uint32_t* b
 
 /* Composite used by tests/bench: parent codes (N,K) at c bits + master-grid
  * scales (N, ng) -> r-bit child -> dense_f32 -> matmul_ref.  This is the
- * chain slice_layer (slicing.py:158-171) -> PackedLayer.from_sliced
- * (matmul.py:221-230; pack/unpack are lossless, packing.py:113-126) ->
- * matmul_ref (matmul.py:253-260); for r in {6, 8}, which PackedLayer rejects
- * (matmul.py:223-224), it is the same formula applied directly. */
+ * chain slice_layer (slicing.py:122-135) -> PackedLayer.from_sliced
+ * (matmul.py:53-62; pack/unpack are lossless, packing.py:113-126) ->
+ * matmul_ref (matmul.py:85-92); for r in {6, 8}, which PackedLayer rejects
+ * (matmul.py:55-56), it is the same formula applied directly. */
 int oq_parent_matmul_ref(const uint8_t* parent, int N, int K, const float* scales, int ng,
                          int G, int c, int r, const float* X, int B,
                          uint8_t* child_scratch, float* scale_scratch, float* W_scratch,

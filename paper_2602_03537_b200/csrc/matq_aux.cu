@@ -39,7 +39,7 @@ __global__ void k_pack_planes(const uint8_t* __restrict__ codes, long long ldc, 
     }
 }
 
-// Group scales (N, ng) row-major (QuantGrid.scales, grid.py:293) -> the
+// Group scales (N, ng) row-major (QuantGrid.scales, grid.py:75) -> the
 // blob's per-step scale blocks (spg > 0) and/or the tiled array
 // [Np/16][ngp][16] (generic group sizes).  Padding entries are 0.
 __global__ void k_pack_scales(const float* __restrict__ scales, Layout L, int ng,
@@ -113,7 +113,7 @@ __global__ void k_slice_codes(const uint32_t* __restrict__ blob, Layout L, uint8
 // (bitsliced slice + transpose network + bf16 magic conversion).
 //   vals (int8, optional): s - 2^(r-1) as decoded in bf16 registers
 //   W (fp32, optional): (s - z) * (scale * out_scale), one fp32 rounding --
-//   the same arithmetic as PackedLayer.dense_f32 (matmul.py:232-237).
+//   the same arithmetic as PackedLayer.dense_f32 (matmul.py:64-69).
 template <int R, bool CHILD>
 __global__ void k_decode_dense(const uint32_t* __restrict__ blob, const float* __restrict__ ts,
                                Layout L, float out_scale, int8_t* __restrict__ vals,
@@ -173,7 +173,7 @@ __global__ void k_materialize_child(const uint32_t* __restrict__ blob, Layout Lp
 }
 
 // ---------------------------------------------------------------------------
-// Elementwise slice_code / slice_to_code (slicing.py:67-90) for any 2<=c<=8.
+// Elementwise slice_code / slice_to_code (slicing.py:31-54) for any 2<=c<=8.
 __global__ void k_slice_elementwise(const uint8_t* __restrict__ q, long long n, int c, int r,
                                     int on_master, uint8_t* __restrict__ out, int* err) {
     const int k = c - r, qmax = (1 << c) - 1;
@@ -192,7 +192,7 @@ __global__ void k_slice_elementwise(const uint8_t* __restrict__ q, long long n, 
     }
 }
 
-// grid.py:346-367 (dequant_value / dequant) in float64:
+// grid.py:128-149 (dequant_value / dequant) in float64:
 // scale[row, col // G] * (2^(c-r) * (code - 2^(r-1))).
 __global__ void k_dequant_f64(const uint8_t* __restrict__ codes, int N, int K,
                               const float* __restrict__ scales, int ng, int G, int c, int r,
@@ -212,7 +212,7 @@ __global__ void k_dequant_f64(const uint8_t* __restrict__ codes, int N, int K,
     }
 }
 
-// grid.py:346-358 dequant_value with a per-element float64 scale.
+// grid.py:128-140 dequant_value with a per-element float64 scale.
 __global__ void k_dequant_value_f64(const uint8_t* __restrict__ q, const double* __restrict__ scale,
                                     long long n, int c, int r, double* __restrict__ out, int* err) {
     const long long step = 1ll << (c - r), zr = 1ll << (r - 1);
@@ -227,7 +227,7 @@ __global__ void k_dequant_value_f64(const uint8_t* __restrict__ q, const double*
     }
 }
 
-// matmul.py:253-260 matmul_ref, bit-exact on device: float32 product then
+// matmul.py:85-92 matmul_ref, bit-exact on device: float32 product then
 // float32 add, k ascending (explicit _rn intrinsics forbid FMA contraction).
 __global__ void k_matmul_ref(const float* __restrict__ X, int B, int K,
                              const float* __restrict__ W, int N, float* __restrict__ Y) {

@@ -228,7 +228,7 @@ MQ_HD uint32_t field8_bf16(uint32_t w) {
 }
 
 // ----------------------------------------------------------------------------
-// Bitsliced rounding slice (slicing.py:67-84), 32 weights per instruction.
+// Bitsliced rounding slice (slicing.py:31-48), 32 weights per instruction.
 // T[0..R-1] = top R code bits (T[0] = MSB), T[R] = the rounding bit k-1.
 //   carry = T[R] & ~(T[0] & ... & T[R-1])      (clamp: no carry into all-ones)
 //   S = T + carry  (ripple from the LSB; cannot overflow because of the clamp)

@@ -13,7 +13,7 @@ validation and messages; the compute runs on the B200 through libmatq:
   float32 k-ascending, bit-identical to the reference's numpy loop.
 
 Bit-widths: the reference's PackedLayer accepts r in {2, 3, 4}
-(matmul.py:223-224); here any r on the ladder {2, 3, 4, 6, 8} works, and
+(matmul.py:55-56); here any r on the ladder {2, 3, 4, 6, 8} works, and
 ``PackedLayer.from_parent`` serves every r from one resident int8 parent
 without repacking (mode P).
 """
@@ -75,7 +75,7 @@ class PackedLayer:
 
     @classmethod
     def from_sliced(cls, layer: SlicedLayer) -> "PackedLayer":
-        """matmul.py:221-230; r in {6, 8} is accepted as well (no reference format)."""
+        """matmul.py:53-62; r in {6, 8} is accepted as well (no reference format)."""
         if layer.bits not in LADDER:
             raise MatmulError("unsupported bits")
         packed = pack(layer.codes, layer.bits) if layer.bits <= 4 else None
@@ -113,7 +113,7 @@ class PackedLayer:
         return self._planes
 
     def dense_f32(self) -> np.ndarray:
-        """(codes - z) * scales[:, col // G] in float32 (matmul.py:232-237), on device."""
+        """(codes - z) * scales[:, col // G] in float32 (matmul.py:64-69), on device."""
         return self.device().decode(self.bits).cpu().numpy()
 
 
@@ -133,7 +133,7 @@ class MatmulTask:
 
 
 def matmul_ref(task: MatmulTask) -> np.ndarray:
-    """Dense reference: float32, k-ascending (matmul.py:253-260); exact on device."""
+    """Dense reference: float32, k-ascending (matmul.py:85-92); exact on device."""
     _lib.require_cuda()
     W = task.layer.device().decode(task.layer.bits)
     X = torch.from_numpy(task.X).cuda()
@@ -225,7 +225,7 @@ def bench(m: int, k: int, batch: int, bits: int, reps: int = 7, group_size: int 
 
     Same record keys as the reference.  Activations and outputs stay on the
     device (bf16); ``gbps`` counts the weight payload + X + Y like the
-    reference (matmul.py:335-336, scales excluded).
+    reference (matmul.py:167-168, scales excluded).
     """
     if reps < 3:
         raise MatmulError("reps must be >= 3")

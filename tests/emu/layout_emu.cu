@@ -6,7 +6,7 @@
 // produced by slice_loaded + decode_word hold exactly s_r(q) - 2^(r-1) for
 // the weight the mma.m16n8k16 A-fragment layout assigns to that register
 // slot (PTX ISA: a0/a1 row g cols 2t,2t+1; a2/a3 row g+8; a4..a7 cols +8).
-// s_r is the reference rounding slice (slicing.py:67-84).
+// s_r is the reference rounding slice (slicing.py:31-48).
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -23,7 +23,7 @@ static uint32_t xrand() {
     return rng_state;
 }
 
-static int slice_ref(int q, int r) {  // slicing.py:67-84 with c = 8
+static int slice_ref(int q, int r) {  // slicing.py:31-48 with c = 8
     const int k = 8 - r;
     if (k == 0) return q;
     int v = (q + (1 << (k - 1))) >> k;

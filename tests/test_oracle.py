@@ -49,7 +49,7 @@ def test_slice_tables_exhaustive(golden):
             deq = O.dequant_f64(low[None, :], np.full((1, 1), 0.37, np.float32),
                                 low.size, c, r)[0]
             # reference dequant_value uses the float64 scale 0.37, the oracle the
-            # float32 grid scale (grid.py:300): compare the integer multipliers
+            # float32 grid scale (grid.py:82): compare the integer multipliers
             mult = deq / np.float64(np.float32(0.37))
             want = t["deq_c%d_r%d" % (c, r)] / 0.37
             assert np.allclose(mult, want, rtol=0, atol=1e-9)
