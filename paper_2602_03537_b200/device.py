@@ -13,6 +13,8 @@ CPU compute path.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -62,9 +64,16 @@ WORKSPACES = _Workspaces()
 _WS_NEED: dict[tuple[int, int, int, int], int] = {}
 
 
+def _tuning_env() -> tuple:
+    e = os.environ
+    return (e.get("MQ_GEMV_SPLIT"), e.get("MQ_GEMV_WARPS"), e.get("MQ_GEMV_STAGES"),
+            e.get("MQ_GEMV_STREAM"))
+
+
 def gemv_workspace_bytes(N: int, K: int, B: int, flags: int) -> int:
     """Cached mq_gemv_workspace_bytes (the launch path calls it every GEMV)."""
-    key = (N, K, B, flags & _lib.MQ_X_F32)
+    # the C side honours tuning overrides (MQ_GEMV_*) that change the split
+    key = (N, K, B, flags & _lib.MQ_X_F32, _tuning_env())
     v = _WS_NEED.get(key)
     if v is None:
         v = _WS_NEED[key] = _lib.lib().mq_gemv_workspace_bytes(N, K, B, flags)
