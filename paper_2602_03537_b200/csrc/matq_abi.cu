@@ -338,6 +338,27 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     return cuda_status(e, "mq_gemv");
 }
 
+int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int B, int N, int K,
+            int G, int nplanes, int r, float out_scale, int flags, void* stream) {
+    if (!blob || !X || !Y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (nplanes < r || nplanes > 8 || (nplanes != r && nplanes < r + 1))
+        return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", r, nplanes);
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (G != 128) return fail(MQ_ERR_INVALID, "mq_gemm needs group size 128 (got %d)", G);
+    if (N < 1 || K < 1 || B < 1) return fail(MQ_ERR_INVALID, "bad shape B=%d N=%d K=%d", B, N, K);
+    if (ldx < K || ldy < N) return fail(MQ_ERR_INVALID, "bad leading dimension");
+    if (flags & MQ_X_F32) return fail(MQ_ERR_INVALID, "mq_gemm takes bf16 activations");
+    if ((ldx & 7) || (reinterpret_cast<uintptr_t>(X) & 15))
+        return fail(MQ_ERR_INVALID, "activations must be 16-byte aligned with ldx %% 8 == 0");
+    const mq::Layout L = mq::Layout::make(N, K, G, nplanes);
+    const char* why = "";
+    const cudaError_t e = mq::launch_gemm(blob, L, X, ldx, Y, ldy, B, r, nplanes == r, out_scale,
+                                          (flags & MQ_Y_F32) != 0, sm_count(), (cudaStream_t)stream,
+                                          (flags & MQ_PDL) != 0, &why);
+    if (e != cudaSuccess && *why) return fail(MQ_ERR_CUDA, "mq_gemm: %s", why);
+    return cuda_status(e, "mq_gemm");
+}
+
 static int sync_and_check(cudaError_t launch, int* err_dev, cudaStream_t s, const char* where,
                           const char* range_msg) {
     if (launch != cudaSuccess) return cuda_status(launch, where);

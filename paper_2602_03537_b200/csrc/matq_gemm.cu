@@ -1,0 +1,122 @@
+// matq_gemm.cu -- K4 launcher: TMA tensor map for the activations, tile
+// grid, template dispatch over (r, child, token tile).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "matq_gemm.cuh"
+#include "matq_internal.h"
+
+namespace mq {
+
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+template <int R, bool CHILD, int BN>
+cudaError_t launch_bn(const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t stream,
+                      bool pdl) {
+    auto kern = k_gemm<R, CHILD, BN>;
+    static bool attr_set = false;
+    constexpr int smem = (int)GemmSmem<BN>::kBytes;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    if (pdl) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, map, p);
+}
+
+template <int R, bool CHILD>
+cudaError_t launch_rc(int bn, const CUtensorMap& map, const GemmParams& p, int grid,
+                      cudaStream_t stream, bool pdl) {
+    if (bn == 64) return launch_bn<R, CHILD, 64>(map, p, grid, stream, pdl);
+    return launch_bn<R, CHILD, 128>(map, p, grid, stream, pdl);
+}
+
+}  // namespace
+
+int gemm_token_tile(int B) { return B <= 64 ? 64 : 128; }
+
+size_t gemm_smem_bytes(int bn) {
+    return bn == 64 ? GemmSmem<64>::kBytes : GemmSmem<128>::kBytes;
+}
+
+cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
+                        int ldy, int B, int r, bool child, float out_scale, bool y_f32, int sms,
+                        cudaStream_t stream, bool pdl, const char** why) {
+    auto enc = encode_fn();
+    if (enc == nullptr) {
+        *why = "cuTensorMapEncodeTiled unavailable";
+        return cudaErrorNotSupported;
+    }
+    const int bn = gemm_token_tile(B);
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)B};
+    const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)bn};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        *why = "cuTensorMapEncodeTiled rejected the activation tensor";
+        return cudaErrorInvalidValue;
+    }
+    GemmParams p{};
+    p.blob = blob;
+    p.step_words = L.step_words;
+    p.sb_words = 16 * L.spg;
+    p.Y = Y;
+    p.ldy = ldy;
+    p.B = B;
+    p.N = L.N;
+    p.K = L.K;
+    p.nsteps = L.nsteps;
+    p.n_rt = L.n_rt;
+    p.n_bt = cdiv(B, bn);
+    p.n_tiles = cdiv(L.N, kGemmBM) * p.n_bt;
+    p.out_scale = out_scale;
+    p.y_f32 = y_f32 ? 1 : 0;
+    const int grid = std::min(p.n_tiles, sms);
+    const bool ch = child && r < 8;
+    switch (r) {
+        case 2: return ch ? launch_rc<2, true>(bn, map, p, grid, stream, pdl)
+                          : launch_rc<2, false>(bn, map, p, grid, stream, pdl);
+        case 3: return ch ? launch_rc<3, true>(bn, map, p, grid, stream, pdl)
+                          : launch_rc<3, false>(bn, map, p, grid, stream, pdl);
+        case 4: return ch ? launch_rc<4, true>(bn, map, p, grid, stream, pdl)
+                          : launch_rc<4, false>(bn, map, p, grid, stream, pdl);
+        case 6: return ch ? launch_rc<6, true>(bn, map, p, grid, stream, pdl)
+                          : launch_rc<6, false>(bn, map, p, grid, stream, pdl);
+        case 8: return launch_rc<8, false>(bn, map, p, grid, stream, pdl);
+    }
+    *why = "unsupported bit-width";
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace mq

@@ -33,4 +33,8 @@ cudaError_t launch_unpack_ref_layout(const unsigned long long* base, const uint3
                                      const uint32_t* b3, int N, int K, uint8_t* codes,
                                      cudaStream_t s);
 
+cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
+                        int ldy, int B, int r, bool child, float out_scale, bool y_f32, int sms,
+                        cudaStream_t stream, bool pdl, const char** why);
+
 }  // namespace mq

@@ -22,6 +22,8 @@ from . import _lib
 
 LADDER = (2, 3, 4, 6, 8)
 MAX_GEMV_ROWS = 32
+# K3 serves B <= GEMV_MAX_ROWS; K4 (tcgen05) serves larger bf16 batches.
+GEMV_MAX_ROWS = 32
 
 
 def _as_device_u8(codes) -> torch.Tensor:
@@ -237,6 +239,62 @@ class PlaneTensor:
         _lib.call("mq_gemv", _lib.ptr(self.blob), _lib.ptr(self.tscales), _lib.ptr(X), X.stride(0),
                   _lib.ptr(out), out.stride(0), B, self.N, self.K, self.G, self.nplanes, r, scale,
                   flags, _lib.ptr(ws), 0 if ws is None else ws.numel(), sp)
+        return out
+
+    # -- K4 ----------------------------------------------------------------
+    def gemm(self, X: torch.Tensor, r: int, out: torch.Tensor | None = None,
+             out_dtype: torch.dtype | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
+        """Y = X @ dequant(slice_r).T on the tcgen05 tensor cores (prefill, any B).
+
+        X: bf16 (B, K), rows 16-byte aligned.  The dequantised weight is
+        rounded to bf16 once (scale * (s - z)); accumulation is fp32.
+        """
+        scale = self._check(r)
+        if self.G != 128:
+            raise ValueError("the tensor-core path needs group size 128")
+        if X.dim() != 2 or X.shape[1] != self.K:
+            raise ValueError("activations must be (batch, %d)" % self.K)
+        if not X.is_cuda or X.dtype != torch.bfloat16:
+            raise ValueError("activations must be a bfloat16 CUDA tensor")
+        if X.stride(1) != 1 or X.stride(0) % 8 or X.data_ptr() % 16:
+            X = X.contiguous()
+            if self.K % 8:
+                raise ValueError("K must be a multiple of 8 for the tensor-core path")
+        B = X.shape[0]
+        if out is None:
+            out = torch.empty((B, self.N), dtype=out_dtype or torch.bfloat16, device=X.device)
+        flags = 0
+        if out.dtype == torch.float32:
+            flags |= _lib.MQ_Y_F32
+        elif out.dtype != torch.bfloat16:
+            raise ValueError("output must be bfloat16 or float32")
+        if out.stride(1) != 1 or tuple(out.shape) != (B, self.N):
+            raise ValueError("bad output tensor")
+        if pdl:
+            flags |= _lib.MQ_PDL
+        _lib.call("mq_gemm", _lib.ptr(self.blob), _lib.ptr(X), X.stride(0), _lib.ptr(out),
+                  out.stride(0), B, self.N, self.K, self.G, self.nplanes, r, scale, flags,
+                  _lib.stream_ptr(stream))
+        return out
+
+    def linear(self, X: torch.Tensor, r: int, out: torch.Tensor | None = None,
+               out_dtype: torch.dtype | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
+        """Dispatch by batch: K3 (GEMV) up to GEMV_MAX_ROWS rows, K4 (tcgen05 GEMM) above.
+
+        fp32 activations or G != 128 stay on K3 (in 32/16-row chunks), which keeps
+        the reference API's 1e-4 agreement (hi + lo bf16 split of fp32 X).
+        """
+        B = X.shape[0]
+        if B <= GEMV_MAX_ROWS and not (X.dtype == torch.float32 and B > 16):
+            return self.gemv(X, r, out=out, out_dtype=out_dtype, pdl=pdl, stream=stream)
+        if X.dtype == torch.bfloat16 and self.G == 128:
+            return self.gemm(X, r, out=out, out_dtype=out_dtype, pdl=pdl, stream=stream)
+        cap = 16 if X.dtype == torch.float32 else MAX_GEMV_ROWS
+        if out is None:
+            od = out_dtype or (torch.float32 if X.dtype == torch.float32 else torch.bfloat16)
+            out = torch.empty((B, self.N), dtype=od, device=X.device)
+        for lo in range(0, B, cap):
+            self.gemv(X[lo:lo + cap], r, out=out[lo:lo + cap], pdl=pdl, stream=stream)
         return out
 
     def workspace_bytes(self, B: int, x_f32: bool = False) -> int:

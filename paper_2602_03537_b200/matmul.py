@@ -153,19 +153,10 @@ def _validate(layer: PackedLayer) -> None:
 
 def matmul_packed_device(layer: PackedLayer, X: torch.Tensor, out: torch.Tensor | None = None,
                          out_dtype: torch.dtype | None = None) -> torch.Tensor:
-    """Device-in / device-out packed matmul; rows beyond 32 run in 32-row chunks."""
+    """Device-in / device-out packed matmul: K3 for B <= 32, K4 (tcgen05) for
+    larger bf16 batches, K3 in chunks for fp32 activations."""
     _validate(layer)
-    pt = layer.device()
-    B = X.shape[0]
-    cap = 16 if X.dtype == torch.float32 else 32
-    if B <= cap:
-        return pt.gemv(X, layer.bits, out=out, out_dtype=out_dtype)
-    if out is None:
-        od = out_dtype or (torch.float32 if X.dtype == torch.float32 else torch.bfloat16)
-        out = torch.empty((B, pt.N), dtype=od, device=X.device)
-    for lo in range(0, B, cap):
-        pt.gemv(X[lo:lo + cap], layer.bits, out=out[lo:lo + cap])
-    return out
+    return layer.device().linear(X, layer.bits, out=out, out_dtype=out_dtype)
 
 
 def matmul_packed(task: MatmulTask, force_fallback: bool = False) -> np.ndarray:

@@ -342,3 +342,99 @@ def test_reference_matmul_suite_semantics(mq):
         mq.random_task(4, 32, 1, 5)
     recs = mq.bench(256, 512, 2, 4, reps=5)
     assert recs[0]["backend"] == "cuda-sm100" and len(recs[0]["samples_ns"]) == 5
+
+
+# ------------------------------------------------------------ K4 (tcgen05) --
+def _k4_weights(codes, scales, r, G=128):
+    """The weights K4 multiplies: bf16(bf16(scale * 2^(8-r)) * (s_r - 2^(r-1))).
+
+    Both roundings are single IEEE round-to-nearest-even steps of exact fp32
+    values (a bf16 times an integer below 2^8 fits fp32 exactly), so this
+    reproduces the device's mul.rn.bf16x2 bit for bit."""
+    s = O.slice_codes(codes, 8, r).astype(np.float32) - float(1 << (r - 1))
+    seff = round_bf16(scales.astype(np.float32) * np.float32(1 << (8 - r)))
+    cols = np.arange(codes.shape[1]) // G
+    return round_bf16(seff[:, cols] * s)
+
+
+@pytest.mark.parametrize("n,k,B", [(128, 1024, 64), (200, 640, 100), (384, 2048, 300),
+                                   (136, 4096, 33), (1024, 5120, 129)])
+def test_gemm_vs_oracle(mq, n, k, B):
+    """K4 against (a) an exact emulation of its bf16 weight rounding (only the
+    fp32 accumulation order differs) and (b) the reference's dequantise-then-
+    matmul oracle, within the stated bf16 tolerance."""
+    codes, scales = _parent(n, k, seed=n + k + B)
+    pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
+    X = _x_bf16(B, k, seed=B)
+    Xd = torch.from_numpy(X).cuda().to(torch.bfloat16)
+    for r in LADDER:
+        got32 = pt.gemm(Xd, r, out_dtype=torch.float32).cpu().numpy()
+        emu = X.astype(np.float64) @ _k4_weights(codes, scales, r).astype(np.float64).T
+        assert rel_err(got32, emu) <= 2e-5, ("emulated", n, k, B, r)
+        want = O.parent_matmul_ref(codes, scales, 128, r, X)
+        assert rel_err(got32, want) <= 5e-3, ("oracle fp32 out", n, k, B, r)
+        got16 = pt.gemm(Xd, r).float().cpu().numpy()
+        assert rel_err(got16, want) <= 1e-2, ("oracle bf16 out", n, k, B, r)
+
+
+def test_gemm_child_and_zero_rows(mq):
+    codes, scales = _parent(256, 1024, seed=77)
+    codes[5] = 128  # parent code 128 slices to the zero code at every r
+    pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
+    X = torch.from_numpy(_x_bf16(96, 1024, seed=3)).cuda().to(torch.bfloat16)
+    for r in (2, 3, 4, 6):
+        yp = pt.gemm(X, r, out_dtype=torch.float32)
+        yc = pt.materialize_child(r).gemm(X, r, out_dtype=torch.float32)
+        assert torch.equal(yp, yc)
+        assert (yp[:, 5] == 0).all()
+
+
+def test_gemm_strided_io_graph_and_pdl(mq):
+    codes, scales = _parent(512, 2048, seed=9)
+    pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
+    big = torch.from_numpy(_x_bf16(80, 2304, seed=5)).cuda().to(torch.bfloat16)
+    X = big[:, 128:128 + 2048]  # row stride 2304, 16-byte aligned
+    ref = pt.gemm(X.contiguous(), 4).clone()
+    outbuf = torch.zeros((80, 600), dtype=torch.bfloat16, device="cuda")
+    out = outbuf[:, :512]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        pt.gemm(X, 4, out=out, pdl=True, stream=s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            pt.gemm(X, 4, out=out, pdl=True, stream=s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    assert (outbuf[:, 512:] == 0).all()
+
+
+def test_gemm_qwen_shapes_vs_fp32_torch(mq):
+    """Qwen3-14B layer shapes (BASELINE config 4) at prefill batches: against
+    an fp32 torch product of the exactly decoded weights (tf32 off)."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for (n, k) in ((7168, 5120), (5120, 17408)):
+        pt = mq.PlaneTensor.random_parent(n, k, seed=n)
+        g = torch.Generator(device="cuda").manual_seed(2)
+        for B in (64, 256, 1024):
+            X = torch.randn(B, k, device="cuda", generator=g).to(torch.bfloat16)
+            for r in (4, 8):
+                W = pt.decode(r)
+                want = X.float() @ W.T
+                got = pt.gemm(X, r, out_dtype=torch.float32)
+                assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 5e-3, (n, k, B, r)
+                # batch rows are independent of the token tile they land in
+                half = pt.gemm(X[: B // 2].contiguous(), r, out_dtype=torch.float32)
+                assert torch.equal(half, got[: B // 2])
+
+
+def test_linear_dispatch(mq):
+    codes, scales = _parent(256, 1024, seed=12)
+    pt = mq.PlaneTensor.from_codes(codes, 8, scales, 128)
+    X = torch.from_numpy(_x_bf16(48, 1024, seed=2)).cuda()
+    y_gemm = pt.linear(X.to(torch.bfloat16), 4, out_dtype=torch.float32)
+    assert torch.equal(y_gemm, pt.gemm(X.to(torch.bfloat16), 4, out_dtype=torch.float32))
+    y32 = pt.linear(X, 4)  # fp32 activations: chunked K3, reference API accuracy
+    want = O.parent_matmul_ref(codes, scales, 128, 4, X.cpu().numpy())
+    assert rel_err(y32.cpu().numpy(), want) <= 1e-4
