@@ -121,11 +121,16 @@ MQ_API int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, in
  * tcgen05 tensor cores: the decode warps slice + dequantise the blob into
  * shared memory as bf16 scale * (s - 2^(r-1)) and tcgen05.mma accumulates in
  * fp32 (TMEM).  X is bf16 (B, K), 16-byte aligned, ldx % 8 == 0; Y bf16 or
- * fp32 (MQ_Y_F32).  G must be 128.  No workspace.  Replaces the reference's
- * blocked batch path nq_gemm (packed_kernels.h:25-27) as driven by
- * _core.pyx:53-63 for batch >= 8. */
+ * fp32 (MQ_Y_F32).  G must be 128.  `workspace` (zero-filled once, shared
+ * with mq_gemv: same ticket convention) must hold
+ * mq_gemm_workspace_bytes(N, K, B, flags) bytes -- nonzero only when the
+ * tiles cannot fill the GPU and K is split across CTAs (deterministic
+ * in-order reduction).  Replaces the reference's blocked batch path nq_gemm
+ * (packed_kernels.h:25-27) as driven by _core.pyx:53-63 for batch >= 8. */
+MQ_API size_t mq_gemm_workspace_bytes(int N, int K, int B, int flags);
 MQ_API int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int B, int N,
-                   int K, int G, int nplanes, int r, float out_scale, int flags, void* stream);
+                   int K, int G, int nplanes, int r, float out_scale, int flags, void* workspace,
+                   size_t workspace_bytes, void* stream);
 
 /* ---- format-layer helpers behind the drop-in Python API --------------- */
 

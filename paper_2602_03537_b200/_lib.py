@@ -54,7 +54,8 @@ _SIGS = {
     "mq_materialize_child": ([_vp, _i, _i, _i, _i, _vp, _vp], _i),
     "mq_gemv_workspace_bytes": ([_i, _i, _i, _i], _sz),
     "mq_gemv": ([_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
-    "mq_gemm": ([_vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp], _i),
+    "mq_gemm_workspace_bytes": ([_i, _i, _i, _i], _sz),
+    "mq_gemm": ([_vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
     "mq_slice_elementwise": ([_vp, _ll, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_f64": ([_vp, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_value_f64": ([_vp, _vp, _ll, _i, _i, _vp, _vp, _vp], _i),

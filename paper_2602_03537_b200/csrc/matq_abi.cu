@@ -338,8 +338,15 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     return cuda_status(e, "mq_gemv");
 }
 
+size_t mq_gemm_workspace_bytes(int N, int K, int B, int flags) {
+    (void)flags;
+    if (N < 1 || K < 1 || B < 1) return 0;
+    return mq::gemm_ws_bytes(mq::choose_gemm_config(N, K, B, sm_count()));
+}
+
 int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int B, int N, int K,
-            int G, int nplanes, int r, float out_scale, int flags, void* stream) {
+            int G, int nplanes, int r, float out_scale, int flags, void* workspace,
+            size_t workspace_bytes, void* stream) {
     if (!blob || !X || !Y) return fail(MQ_ERR_INVALID, "null pointer");
     if (nplanes < r || nplanes > 8 || (nplanes != r && nplanes < r + 1))
         return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", r, nplanes);
@@ -350,10 +357,16 @@ int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int 
     if (flags & MQ_X_F32) return fail(MQ_ERR_INVALID, "mq_gemm takes bf16 activations");
     if ((ldx & 7) || (reinterpret_cast<uintptr_t>(X) & 15))
         return fail(MQ_ERR_INVALID, "activations must be 16-byte aligned with ldx %% 8 == 0");
+    const mq::GemmConfig c = mq::choose_gemm_config(N, K, B, sm_count());
+    const size_t need = mq::gemm_ws_bytes(c);
+    if (need > workspace_bytes || (need && !workspace))
+        return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);
+    if (need && c.n_tiles > (int)(mq::kGemmTicketBytes / sizeof(int)))
+        return fail(MQ_ERR_INVALID, "too many tiles for split-K");
     const mq::Layout L = mq::Layout::make(N, K, G, nplanes);
     const char* why = "";
     const cudaError_t e = mq::launch_gemm(blob, L, X, ldx, Y, ldy, B, r, nplanes == r, out_scale,
-                                          (flags & MQ_Y_F32) != 0, sm_count(), (cudaStream_t)stream,
+                                          (flags & MQ_Y_F32) != 0, c, workspace, (cudaStream_t)stream,
                                           (flags & MQ_PDL) != 0, &why);
     if (e != cudaSuccess && *why) return fail(MQ_ERR_CUDA, "mq_gemm: %s", why);
     return cuda_status(e, "mq_gemm");

@@ -30,7 +30,7 @@ cudaError_t launch_bn(const CUtensorMap& map, const GemmParams& p, int grid, cud
                       bool pdl) {
     auto kern = k_gemm<R, CHILD, BN>;
     static bool attr_set = false;
-    constexpr int smem = (int)GemmSmem<BN>::kBytes;
+    constexpr int smem = (int)GemmSmem<BN, PlaneCount<R, CHILD>::value>::kBytes;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
@@ -55,30 +55,54 @@ template <int R, bool CHILD>
 cudaError_t launch_rc(int bn, const CUtensorMap& map, const GemmParams& p, int grid,
                       cudaStream_t stream, bool pdl) {
     if (bn == 64) return launch_bn<R, CHILD, 64>(map, p, grid, stream, pdl);
-    return launch_bn<R, CHILD, 128>(map, p, grid, stream, pdl);
+    if (bn == 128) return launch_bn<R, CHILD, 128>(map, p, grid, stream, pdl);
+    return launch_bn<R, CHILD, 256>(map, p, grid, stream, pdl);
 }
 
 }  // namespace
 
-int gemm_token_tile(int B) { return B <= 64 ? 64 : 128; }
+GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
+    GemmConfig c{};
+    c.bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
+    const int n_bt = cdiv(B, c.bn);
+    c.n_tiles = cdiv(N, kGemmBM) * n_bt;
+    const int nsteps = pad256(K) / 256;
+    // K splits only when the tiles leave SMs idle: minimise the busiest CTA's
+    // steps (+ ~4 steps of partial write / in-order reduction per split tile).
+    double best = 1e30;
+    for (int S = 1; S <= std::min(8, nsteps); ++S) {
+        const int cs = cdiv(nsteps, S);
+        if (cdiv(nsteps, cs) != S) continue;
+        const int units = c.n_tiles * S;
+        const double cost = (double)cdiv(units, sms) * (cs + (S > 1 ? 4.0 : 0.0));
+        if (cost < best - 1e-9) {
+            best = cost;
+            c.S = S;
+            c.cs = cs;
+        }
+    }
+    c.grid = std::min(c.n_tiles * c.S, sms);
+    return c;
+}
 
-size_t gemm_smem_bytes(int bn) {
-    return bn == 64 ? GemmSmem<64>::kBytes : GemmSmem<128>::kBytes;
+size_t gemm_ws_bytes(const GemmConfig& c) {
+    if (c.S <= 1) return 0;
+    return kGemmTicketBytes + (size_t)c.n_tiles * c.S * c.bn * kGemmBM * sizeof(float);
 }
 
 cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
-                        int ldy, int B, int r, bool child, float out_scale, bool y_f32, int sms,
-                        cudaStream_t stream, bool pdl, const char** why) {
+                        int ldy, int B, int r, bool child, float out_scale, bool y_f32,
+                        const GemmConfig& c, void* ws, cudaStream_t stream, bool pdl,
+                        const char** why) {
     auto enc = encode_fn();
     if (enc == nullptr) {
         *why = "cuTensorMapEncodeTiled unavailable";
         return cudaErrorNotSupported;
     }
-    const int bn = gemm_token_tile(B);
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)B};
     const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-    const cuuint32_t box[2] = {64, (cuuint32_t)bn};
+    const cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)c.bn};
     const cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -90,7 +114,7 @@ cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, in
     GemmParams p{};
     p.blob = blob;
     p.step_words = L.step_words;
-    p.sb_words = 16 * L.spg;
+    p.skip_words = 16 * L.spg - 32;
     p.Y = Y;
     p.ldy = ldy;
     p.B = B;
@@ -98,12 +122,18 @@ cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, in
     p.K = L.K;
     p.nsteps = L.nsteps;
     p.n_rt = L.n_rt;
-    p.n_bt = cdiv(B, bn);
-    p.n_tiles = cdiv(L.N, kGemmBM) * p.n_bt;
+    p.n_bt = cdiv(B, c.bn);
+    p.n_tiles = c.n_tiles;
+    p.S = c.S;
+    p.cs = c.cs;
+    if (c.S > 1) {
+        p.tickets = reinterpret_cast<int*>(ws);
+        p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kGemmTicketBytes);
+    }
     p.out_scale = out_scale;
     p.y_f32 = y_f32 ? 1 : 0;
-    const int grid = std::min(p.n_tiles, sms);
     const bool ch = child && r < 8;
+    const int bn = c.bn, grid = c.grid;
     switch (r) {
         case 2: return ch ? launch_rc<2, true>(bn, map, p, grid, stream, pdl)
                           : launch_rc<2, false>(bn, map, p, grid, stream, pdl);

@@ -6,21 +6,24 @@
 // (packed_kernels.c:177-210, driven in chunks of 16 rows by
 // kernels/_core.pyx:53-63).
 //
-// One persistent CTA per SM, 16 warps, output tiles of 128 weight rows x BN
-// tokens, K consumed 128 columns (one scale group) per pipeline stage:
-//   warp 0      TMA producer: X tile [BN tokens][128 k] bf16, two 64-column
-//               SWIZZLE_128B boxes per stage (tensor map, zero fill past B / K)
-//   warp 1      TMEM allocator + MMA issuer: 8 x tcgen05.mma.kind::f16
-//               (M=128, N=BN, K=16) per stage into a double-buffered fp32
-//               accumulator in TMEM; tcgen05.commit frees the stage
-//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 columns, bf16/fp32 store
-//   warps 8-15  decode producers, one 16-row tile each: stream the P8 blob
-//               (r+1 planes + group scales) straight from HBM, slice + decode
-//               bitsliced exactly as K3 does, multiply by the group scale
-//               (bf16x2), and stmatrix the mma-fragment-ordered registers into
-//               the K-major SWIZZLE_128B A operand.
-// The dequantised weight is rounded to bf16 once (scale * (s - z)); the
-// products and the K reduction run in fp32 on the tensor core.
+// Persistent CTAs (one per SM, 16 warps).  Work unit = (output tile of 128
+// weight rows x BN tokens, K split).  Pipelines:
+//   raw ring    warp 2 (one lane) bulk-copies, per 256-column step, the eight
+//               16-row P8 blocks of the tile ([group scales][r+1 plane slabs],
+//               each contiguous) into shared memory (TMA, mbarrier complete_tx)
+//   operand     per 64-column stage: A = 128 x 64 bf16 weights, B = BN x 64
+//   stages      bf16 activations, both K-major SWIZZLE_128B; warp 0 (one lane)
+//               TMA-loads B from a tensor map (zero fill past B and K), warps
+//               8-15 (one 16-row tile each) slice + decode the raw block
+//               bitsliced as K3 does, scale (bf16x2) and stmatrix A
+//   MMA         warp 1 (one lane): 4 x tcgen05.mma.kind::f16 (M=128, N=BN,
+//               K=16) per stage into a double-buffered fp32 TMEM accumulator;
+//               tcgen05.commit frees the operand stage / publishes the tile
+//   epilogue    warps 4-7: tcgen05.ld 32 lanes x 32 columns -> Y (S = 1), or
+//               fp32 partials + an acq_rel ticket; the last split of a tile sums
+//               the partials in split order (deterministic) and writes Y.
+// The dequantised weight is rounded to bf16 once (scale * (s - z)); products
+// and the K reduction run in fp32 on the tensor core.
 #pragma once
 #include <cuda.h>
 
@@ -32,197 +35,280 @@ namespace mq {
 struct GemmParams {
     const uint32_t* blob;
     long long step_words;  // words per (row tile, step) block
-    int sb_words;          // scale-block words at the head of a block (32 for G = 128)
+    int skip_words;        // scale words before the step's two G=128 groups (0)
     void* Y;
     int ldy;
     int B, N, K, nsteps, n_rt;
     int n_bt, n_tiles;  // token tiles, output tiles
+    int S, cs;          // K splits, steps per split
+    float* ws;          // fp32 partials [n_tiles * S][BN][128] when S > 1
+    int* tickets;       // [n_tiles], zero, self-resetting
     float out_scale;
     int y_f32;
 };
 
 constexpr int kGemmThreads = 512;
 constexpr int kGemmBM = 128;
-constexpr int kGemmBK = 128;
-constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 32 KB
-constexpr int kDecWarp0 = 8, kNumDecWarps = 8, kEpiWarp0 = 4;
+constexpr int kGemmBK = 64;  // K columns per operand stage (one swizzle atom)
+constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KB
+constexpr int kDecWarp0 = 8, kNumDecWarps = 8, kEpiWarp0 = 4, kWarpX = 0, kWarpMma = 1, kWarpW = 2;
+constexpr uint32_t kSmemBudget = 227 * 1024;
 
-template <int BN>
+__host__ __device__ constexpr uint32_t gemm_raw_block_bytes(int npl) { return 128u + 512u * (uint32_t)npl; }
+
+template <int BN, int NPL>
 struct GemmSmem {
-    static constexpr int NS = BN <= 64 ? 4 : 3;
     static constexpr uint32_t kBBytes = (uint32_t)BN * kGemmBK * 2;
-    static constexpr uint32_t kBarOff = NS * (kGemmABytes + kBBytes);
-    static constexpr uint32_t kBytes = kBarOff + 256 + 1024;  // + barriers, + alignment slack
+    static constexpr uint32_t kOpBytes = kGemmABytes + kBBytes;
+    static constexpr uint32_t kRawBytes = kNumDecWarps * gemm_raw_block_bytes(NPL);
+    static constexpr uint32_t kFixed = 1024 + 512;  // alignment slack + barriers
+    static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget) ? 3 : 2;
+    static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 4 : 3;
+    static constexpr uint32_t kRawOff = NS * kOpBytes;
+    static constexpr uint32_t kBarOff = kRawOff + RS * kRawBytes;
+    static constexpr uint32_t kBytes = kBarOff + kFixed;
+    static_assert(kBytes <= kSmemBudget, "K4 shared memory budget");
 };
 
 template <int R, bool CHILD, int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm(const __grid_constant__ CUtensorMap tmx, const GemmParams p) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
-    using SM = GemmSmem<BN>;
-    constexpr int NS = SM::NS;
-    constexpr uint32_t kTmemCols = 2 * BN;
+    using SM = GemmSmem<BN, NPL>;
+    constexpr int NS = SM::NS, RS = SM::RS;
+    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    constexpr uint32_t kBlk = gemm_raw_block_bytes(NPL);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
-    auto a_st = [&](int s) { return base + (uint32_t)s * kGemmABytes; };
-    auto b_st = [&](int s) { return base + NS * kGemmABytes + (uint32_t)s * SM::kBBytes; };
+    auto a_st = [&](int s) { return base + (uint32_t)s * SM::kOpBytes; };
+    auto b_st = [&](int s) { return base + (uint32_t)s * SM::kOpBytes + kGemmABytes; };
+    auto raw_st = [&](int s) { return base + SM::kRawOff + (uint32_t)s * SM::kRawBytes; };
     const uint32_t bar0 = base + SM::kBarOff;
-    auto full_bar = [&](int s) { return bar0 + 8u * s; };
-    auto empty_bar = [&](int s) { return bar0 + 8u * (NS + s); };
-    auto tfull_bar = [&](int b) { return bar0 + 8u * (2 * NS + b); };
-    auto tempty_bar = [&](int b) { return bar0 + 8u * (2 * NS + 2 + b); };
-    const uint32_t tmem_slot = bar0 + 8u * (2 * NS + 4);
-    uint32_t* tmem_slot_ptr =
-        reinterpret_cast<uint32_t*>(smem_raw + (tmem_slot - smem_addr(smem_raw)));
+    auto op_full = [&](int s) { return bar0 + 8u * s; };
+    auto op_empty = [&](int s) { return bar0 + 8u * (NS + s); };
+    auto raw_full = [&](int s) { return bar0 + 8u * (2 * NS + s); };
+    auto raw_empty = [&](int s) { return bar0 + 8u * (2 * NS + RS + s); };
+    auto tfull = [&](int b) { return bar0 + 8u * (2 * NS + 2 * RS + b); };
+    auto tempty = [&](int b) { return bar0 + 8u * (2 * NS + 2 * RS + 2 + b); };
+    const uint32_t tmem_slot = bar0 + 8u * (2 * NS + 2 * RS + 4);
+    const uint32_t flag_slot = tmem_slot + 4;
+    uint8_t* const gen_base = smem_raw + (base - smem_addr(smem_raw));
+    volatile uint32_t* tmem_slot_ptr = reinterpret_cast<volatile uint32_t*>(gen_base + (tmem_slot - base));
+    volatile int* flag_ptr = reinterpret_cast<volatile int*>(gen_base + (flag_slot - base));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(full_bar(s), 1 + kNumDecWarps);
-            mbar_init(empty_bar(s), 1);
+            mbar_init(op_full(s), 1 + kNumDecWarps);
+            mbar_init(op_empty(s), 1);
+        }
+        for (int s = 0; s < RS; ++s) {
+            mbar_init(raw_full(s), 1);
+            mbar_init(raw_empty(s), kNumDecWarps);
         }
         for (int b = 0; b < 2; ++b) {
-            mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), 4);
+            mbar_init(tfull(b), 1);
+            mbar_init(tempty(b), 4);
         }
         fence_mbar_init();
         tma_prefetch_desc(&tmx);
     }
-    if (warp == 1) tmem_alloc<kTmemCols>(tmem_slot);
+    if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
     pdl_launch_dependents();
 
-    const int nst = p.nsteps;
-    const int my_tiles = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int n_units = p.n_tiles * p.S;
+    const int my_units = (int)blockIdx.x < n_units ? (n_units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // unit -> (tile, split, step range); consecutive units are splits of one tile
+    auto unit_of = [&](int ui, int& tile, int& split, int& st0, int& nst) {
+        const int u = (int)blockIdx.x + ui * (int)gridDim.x;
+        tile = u / p.S;
+        split = u - tile * p.S;
+        st0 = split * p.cs;
+        nst = max(0, min(p.nsteps, st0 + p.cs) - st0);
+    };
 
-    if (warp == 0) {
+    if (warp == kWarpX) {
         // ---------------- TMA producer: activations -------------------------
         if (lane == 0) {
             pdl_wait();  // X is written by the previous kernel
             int ks = 0;
-            for (int ti = 0; ti < my_tiles; ++ti) {
-                const int tile = blockIdx.x + ti * gridDim.x;
+            for (int ui = 0; ui < my_units; ++ui) {
+                int tile, split, st0, nst;
+                unit_of(ui, tile, split, st0, nst);
                 const int bt = tile % p.n_bt;
-                for (int kk = 0; kk < 2 * nst; ++kk, ++ks) {
+                for (int kk = 0; kk < 4 * nst; ++kk, ++ks) {
                     const int s = ks % NS;
-                    mbar_wait(empty_bar(s), ((ks / NS) & 1) ^ 1);
-                    mbar_expect_tx(full_bar(s), SM::kBBytes);
-                    const int k0 = kk * kGemmBK;
-                    tma_load_2d(b_st(s), &tmx, k0, bt * BN, full_bar(s));
-                    tma_load_2d(b_st(s) + BN * 128, &tmx, k0 + 64, bt * BN, full_bar(s));
+                    mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                    mbar_expect_tx(op_full(s), SM::kBBytes);
+                    tma_load_2d(b_st(s), &tmx, st0 * 256 + kk * kGemmBK, bt * BN, op_full(s));
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kWarpW) {
+        // ---------------- TMA producer: raw weight blocks ---------------------
+        if (lane == 0) {
+            int rs_i = 0;
+            for (int ui = 0; ui < my_units; ++ui) {
+                int tile, split, st0, nst;
+                unit_of(ui, tile, split, st0, nst);
+                const int rt0 = (tile / p.n_bt) * (kGemmBM / 16);
+                const int nvalid = min(kNumDecWarps, p.n_rt - rt0);
+                for (int st = st0; st < st0 + nst; ++st, ++rs_i) {
+                    const int s = rs_i % RS;
+                    mbar_wait(raw_empty(s), ((rs_i / RS) & 1) ^ 1);
+                    mbar_expect_tx(raw_full(s), (uint32_t)nvalid * kBlk);
+                    for (int d = 0; d < nvalid; ++d)
+                        bulk_g2s_nohint(raw_st(s) + (uint32_t)d * kBlk,
+                                        p.blob + ((long long)(rt0 + d) * p.nsteps + st) * p.step_words + p.skip_words,
+                                        kBlk, raw_full(s));
+                }
+            }
+        }
+    } else if (warp == kWarpMma) {
         // ---------------- MMA issuer ----------------------------------------
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc_bf16(kGemmBM, BN);
             int ks = 0;
-            for (int ti = 0; ti < my_tiles; ++ti) {
-                const int buf = ti & 1;
-                mbar_wait(tempty_bar(buf), ((ti >> 1) & 1) ^ 1);
+            for (int ui = 0; ui < my_units; ++ui) {
+                int tile, split, st0, nst;
+                unit_of(ui, tile, split, st0, nst);
+                const int buf = ui & 1;
+                mbar_wait(tempty(buf), ((ui >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(buf * BN);
-                for (int kk = 0; kk < 2 * nst; ++kk, ++ks) {
+                for (int kk = 0; kk < 4 * nst; ++kk, ++ks) {
                     const int s = ks % NS;
-                    mbar_wait(full_bar(s), (ks / NS) & 1);
+                    mbar_wait(op_full(s), (ks / NS) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int k16 = 0; k16 < kGemmBK / 16; ++k16) {
-                        const uint32_t atom = (uint32_t)(k16 >> 2), off = (uint32_t)(k16 & 3) * 32u;
-                        const uint64_t ad = umma_desc_k_sw128(a_st(s) + atom * 16384u + off);
-                        const uint64_t bd = umma_desc_k_sw128(b_st(s) + atom * (BN * 128u) + off);
+                        const uint64_t ad = umma_desc_k_sw128(a_st(s) + (uint32_t)k16 * 32u);
+                        const uint64_t bd = umma_desc_k_sw128(b_st(s) + (uint32_t)k16 * 32u);
                         umma_bf16(d, ad, bd, idesc, (kk | k16) != 0);
                     }
-                    umma_commit(empty_bar(s));
+                    umma_commit(op_empty(s));
                 }
-                umma_commit(tfull_bar(buf));
+                umma_commit(tfull(buf));
             }
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        // ---------------- epilogue: TMEM -> Y ----------------------------------
+        // ---------------- epilogue: TMEM -> Y / split-K partials ---------------
         const int q = warp & 3;
-        for (int ti = 0; ti < my_tiles; ++ti) {
-            const int tile = blockIdx.x + ti * gridDim.x;
+        const int et = threadIdx.x - 32 * kEpiWarp0;  // 0..127 = TMEM lane = tile row
+        for (int ui = 0; ui < my_units; ++ui) {
+            int tile, split, st0, nst;
+            unit_of(ui, tile, split, st0, nst);
             const int mt = tile / p.n_bt, bt = tile % p.n_bt;
-            const int buf = ti & 1;
-            mbar_wait(tfull_bar(buf), (ti >> 1) & 1);
+            const int buf = ui & 1;
+            mbar_wait(tfull(buf), (ui >> 1) & 1);
             tc_fence_after();
-            const int row = mt * kGemmBM + 32 * q + lane;
+            const int row = mt * kGemmBM + et;
+            const int b_lim = min(BN, p.B - bt * BN);
+            auto store_y = [&](int j, float v) {
+                const long long o = (long long)(bt * BN + j) * p.ldy + row;
+                if (p.y_f32) reinterpret_cast<float*>(p.Y)[o] = v;
+                else reinterpret_cast<uint16_t*>(p.Y)[o] = f32_to_bf16_rn(v);
+            };
+            float* part = p.ws + ((long long)tile * p.S + split) * (BN * kGemmBM);
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN + 32 * c), v);
                 tmem_ld_wait();
-                if (row < p.N) {
-                    const int b0 = bt * BN + 32 * c;
-                    if (p.y_f32) {
-                        float* Y = reinterpret_cast<float*>(p.Y);
+                if (p.S == 1) {
+                    if (row < p.N) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
-                            if (b0 + j < p.B) Y[(long long)(b0 + j) * p.ldy + row] = __uint_as_float(v[j]);
-                    } else {
-                        uint16_t* Y = reinterpret_cast<uint16_t*>(p.Y);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (b0 + j < p.B)
-                                Y[(long long)(b0 + j) * p.ldy + row] = f32_to_bf16_rn(__uint_as_float(v[j]));
+                            if (32 * c + j < b_lim) store_y(32 * c + j, __uint_as_float(v[j]));
                     }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) part[(32 * c + j) * kGemmBM + et] = __uint_as_float(v[j]);
                 }
             }
+            // TMEM buffer can be refilled as soon as it is read
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(buf));
+            if (lane == 0) mbar_arrive(tempty(buf));
+            if (p.S > 1) {
+                // publish partials; the last split of the tile reduces in split order
+                __threadfence();
+                named_bar_sync(1, 128);
+                if (et == 0) *flag_ptr = (atom_add_acq_rel(p.tickets + tile, 1) == p.S - 1);
+                named_bar_sync(1, 128);
+                const int last = *flag_ptr;
+                if (last) {
+                    __threadfence();
+                    const float* t0 = p.ws + (long long)tile * p.S * (BN * kGemmBM);
+                    if (row < p.N) {
+#pragma unroll 1
+                        for (int j0 = 0; j0 < b_lim; j0 += 8) {
+                            float acc[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
+                            for (int sp = 0; sp < p.S; ++sp) {  // split order: deterministic
+                                const float* src = t0 + (long long)sp * (BN * kGemmBM) + j0 * kGemmBM + et;
+                                float v[8];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) v[u] = j0 + u < BN ? __ldcg(src + u * kGemmBM) : 0.0f;
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) acc[u] += v[u];
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u)
+                                if (j0 + u < b_lim) store_y(j0 + u, acc[u]);
+                        }
+                    }
+                    if (et == 0) p.tickets[tile] = 0;
+                }
+                named_bar_sync(1, 128);  // flag slot reuse
+            }
         }
     } else if (warp >= kDecWarp0) {
-        // ---------------- decode producers: P8 blob -> bf16 A operand -----------
+        // ---------------- decode producers: raw blocks -> bf16 A operand --------
         const int dw = warp - kDecWarp0;
         const int g = lane >> 2;
-        const int total = my_tiles * nst;
         // stmatrix row address: matrix j = lane >> 3 holds rows +8 (j & 1), columns +8 (j >> 1)
-        const int j = lane >> 3;
-        const uint32_t row_off = (uint32_t)(16 * dw + (lane & 7) + 8 * (j & 1)) * 128u;
+        const int jm = lane >> 3;
+        const uint32_t row_off = (uint32_t)(16 * dw + (lane & 7) + 8 * (jm & 1)) * 128u;
         const uint32_t swz = (uint32_t)(lane & 7);
-        auto block_of = [&](int f) -> const uint32_t* {
-            const int tile = blockIdx.x + (f / nst) * gridDim.x;
-            const int st = f - (f / nst) * nst;
-            const int rt = (tile / p.n_bt) * (kGemmBM / 16) + dw;
-            return rt < p.n_rt ? p.blob + ((long long)rt * nst + st) * p.step_words : nullptr;
-        };
-        uint4 raw[NPL], nxt[NPL];
-        float sc[4], nsc[4];
-        auto load = [&](const uint32_t* b, uint4 (&rw)[NPL], float (&s4)[4]) {
-            if (b == nullptr) return;
-            s4[0] = ldg_f32(reinterpret_cast<const float*>(b) + g);
-            s4[1] = ldg_f32(reinterpret_cast<const float*>(b) + g + 8);
-            s4[2] = ldg_f32(reinterpret_cast<const float*>(b) + 16 + g);
-            s4[3] = ldg_f32(reinterpret_cast<const float*>(b) + 24 + g);
-#pragma unroll
-            for (int jj = 0; jj < NPL; ++jj)
-                rw[jj] = ldg_stream(reinterpret_cast<const uint4*>(b + p.sb_words + jj * 128) + lane);
-        };
-        const uint32_t* cur = total > 0 ? block_of(0) : nullptr;
-        load(cur, raw, sc);
+        int ks = 0, rs_i = 0;
+        for (int ui = 0; ui < my_units; ++ui) {
+            int tile, split, st0, nst;
+            unit_of(ui, tile, split, st0, nst);
+            const bool valid = (tile / p.n_bt) * (kGemmBM / 16) + dw < p.n_rt;
 #pragma unroll 1
-        for (int f = 0; f < total; ++f) {
-            const uint32_t* nb = f + 1 < total ? block_of(f + 1) : nullptr;
-            load(nb, nxt, nsc);
+            for (int f = 0; f < nst; ++f, ++rs_i) {
+                const int rsl = rs_i % RS;
+                mbar_wait(raw_full(rsl), (rs_i / RS) & 1);
+                uint4 raw[NPL];
+                float sc[4];
+                const uint32_t blk = raw_st(rsl) + (uint32_t)dw * kBlk;
+                if (valid) {
+                    sc[0] = lds32f(blk + 4u * g);
+                    sc[1] = lds32f(blk + 4u * (g + 8));
+                    sc[2] = lds32f(blk + 4u * (16 + g));
+                    sc[3] = lds32f(blk + 4u * (24 + g));
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int ks = 2 * f + h;
-                const int s = ks % NS;
-                mbar_wait(empty_bar(s), ((ks / NS) & 1) ^ 1);
-                if (cur != nullptr) {
-                    const uint32_t s_lo = bf16x2_splat(sc[2 * h] * p.out_scale);
-                    const uint32_t s_hi = bf16x2_splat(sc[2 * h + 1] * p.out_scale);
-                    const uint32_t abase = a_st(s) + row_off;
+                    for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds128(blk + 128u + 512u * jj + 16u * lane);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(raw_empty(rsl));
+                // one operand stage per word: a proxy fence per stage keeps the
+                // decoders one stage behind the MMA at most (batching two words
+                // per fence measured slower: it needs two free stages at once)
 #pragma unroll
-                    for (int wi = 0; wi < 2; ++wi) {
-                        const int w = 2 * h + wi;
+                for (int w = 0; w < 4; ++w, ++ks) {
+                    const int s = ks % NS;
+                    mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                    if (valid) {
+                        const uint32_t s_lo = bf16x2_splat(sc[(w >> 1) * 2] * p.out_scale);
+                        const uint32_t s_hi = bf16x2_splat(sc[(w >> 1) * 2 + 1] * p.out_scale);
                         uint32_t T[NPL];
 #pragma unroll
                         for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(raw[jj], w);
@@ -232,29 +318,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         decode_word<R, false>(Sl, A);
 #pragma unroll
                         for (int qq = 0; qq < 16; ++qq) A[qq] = hmul2_bf16(A[qq], (qq & 1) ? s_hi : s_lo);
+                        const uint32_t abase = a_st(s) + row_off;
 #pragma unroll
                         for (int k16 = 0; k16 < 4; ++k16) {
-                            const uint32_t chunk = (uint32_t)(2 * k16 + (j >> 1));
-                            stmatrix_x4(abase + (uint32_t)wi * 16384u + ((chunk ^ swz) << 4), A[4 * k16],
-                                        A[4 * k16 + 1], A[4 * k16 + 2], A[4 * k16 + 3]);
+                            const uint32_t chunk = (uint32_t)(2 * k16 + (jm >> 1));
+                            stmatrix_x4(abase + ((chunk ^ swz) << 4), A[4 * k16], A[4 * k16 + 1],
+                                        A[4 * k16 + 2], A[4 * k16 + 3]);
                         }
+                        fence_proxy_async_smem();
                     }
-                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(op_full(s));
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(full_bar(s));
             }
-            cur = nb;
-#pragma unroll
-            for (int jj = 0; jj < NPL; ++jj) raw[jj] = nxt[jj];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) sc[i] = nsc[i];
         }
     }
 
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kWarpMma) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
     }

@@ -33,8 +33,16 @@ cudaError_t launch_unpack_ref_layout(const unsigned long long* base, const uint3
                                      const uint32_t* b3, int N, int K, uint8_t* codes,
                                      cudaStream_t s);
 
+struct GemmConfig {
+    int bn, n_tiles, S, cs, grid;
+};
+// Split-K tickets at the head of the K4 workspace (same convention as K3's).
+constexpr size_t kGemmTicketBytes = 64 * 1024;
+GemmConfig choose_gemm_config(int N, int K, int B, int sms);
+size_t gemm_ws_bytes(const GemmConfig& c);
 cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
-                        int ldy, int B, int r, bool child, float out_scale, bool y_f32, int sms,
-                        cudaStream_t stream, bool pdl, const char** why);
+                        int ldy, int B, int r, bool child, float out_scale, bool y_f32,
+                        const GemmConfig& c, void* ws, cudaStream_t stream, bool pdl,
+                        const char** why);
 
 }  // namespace mq

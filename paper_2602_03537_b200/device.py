@@ -82,6 +82,18 @@ def gemv_workspace_bytes(N: int, K: int, B: int, flags: int) -> int:
     return v
 
 
+_GEMM_WS: dict[tuple[int, int, int], int] = {}
+
+
+def gemm_workspace_bytes(N: int, K: int, B: int) -> int:
+    """Cached mq_gemm_workspace_bytes (split-K partials for small tile counts)."""
+    key = (N, K, B)
+    v = _GEMM_WS.get(key)
+    if v is None:
+        v = _GEMM_WS[key] = _lib.lib().mq_gemm_workspace_bytes(N, K, B, 0)
+    return v
+
+
 def reserve_workspace(nbytes: int, stream=None) -> None:
     WORKSPACES.get(int(nbytes), _lib.stream_ptr(stream))
 
@@ -272,9 +284,12 @@ class PlaneTensor:
             raise ValueError("bad output tensor")
         if pdl:
             flags |= _lib.MQ_PDL
+        sp = _lib.stream_ptr(stream)
+        need = gemm_workspace_bytes(self.N, self.K, B)
+        ws = WORKSPACES.get(need, sp)
         _lib.call("mq_gemm", _lib.ptr(self.blob), _lib.ptr(X), X.stride(0), _lib.ptr(out),
                   out.stride(0), B, self.N, self.K, self.G, self.nplanes, r, scale, flags,
-                  _lib.stream_ptr(stream))
+                  _lib.ptr(ws), 0 if ws is None else ws.numel(), sp)
         return out
 
     def linear(self, X: torch.Tensor, r: int, out: torch.Tensor | None = None,
