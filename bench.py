@@ -102,6 +102,17 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
+def workload_config(model: str, n_blocks: int, bits: int, batch: int, world: int) -> dict:
+    """The config both arms report (same workload, same keys)."""
+    from paper_2602_03537_b200.model import KINDS, SHAPES, tp_layer_dims
+
+    dims = ", ".join("%s %dx%d" % ((k,) + tp_layer_dims(SHAPES[model], k, 1)) for k in KINDS)
+    return {"workload": "%s linear stack decode: %d blocks x {%s}, int8 parent sliced to r bits "
+                        "(rounding MSB slice), G=128" % (model, n_blocks, dims),
+            "model": model, "bits": bits, "batch": batch, "group_size": 128,
+            "parallelism": "tp%d" % world}
+
+
 # ------------------------------------------------------------ CPU baseline --
 class CpuReference:
     """One Llama-3.1-8B block (qkv, o, gate_up, down) on the host cores.
@@ -115,18 +126,19 @@ class CpuReference:
     Preparation (slice + pack) is untimed, as in the reference bench.
     """
 
-    def __init__(self, r: int, batch: int, threads: int):
+    def __init__(self, r: int, batch: int, threads: int, model: str = "Llama-3.1-8B"):
         import numpy as np
         from concurrent.futures import ThreadPoolExecutor
 
         from oracle import oracle as O
-        from paper_2602_03537_b200.model import KINDS, LLAMA31_8B, tp_layer_dims
+        from paper_2602_03537_b200.model import KINDS, SHAPES, tp_layer_dims
 
         self.r, self.threads, self.O = r, threads, O
+        self.n_blocks = SHAPES[model].n_layers
         rng = np.random.default_rng(0)
         self.layers = []
         for kind in KINDS:
-            N, K = tp_layer_dims(LLAMA31_8B, kind, 1)
+            N, K = tp_layer_dims(SHAPES[model], kind, 1)
             parent = rng.integers(0, 256, size=(N, K), dtype=np.uint8)
             scales = rng.uniform(0.005, 0.02, size=(N, K // 128)).astype(np.float32)
             child = O.slice_codes(parent, 8, r)
@@ -175,7 +187,7 @@ def run_reference(args):
         return 0
     threads = os.cpu_count() or 1
     r = args.bits
-    ref = CpuReference(r, args.batch, threads)
+    ref = CpuReference(r, args.batch, threads, args.model)
     samples = []
     for i in range(args.warmup + args.steps):
         t = ref.block_seconds()
@@ -184,15 +196,13 @@ def run_reference(args):
     ref.close()
     kind, backend = ref.kind, ref.backend
     per_block = statistics.median(samples)
-    tok_s = args.batch / (32 * per_block)
+    tok_s = args.batch / (ref.n_blocks * per_block)
     line = {
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 32 * per_block * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref.n_blocks * per_block * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic",
-        "config": {"workload": "Llama-3.1-8B linear stack decode (32 blocks x qkv/o/gate_up/down), "
-                               "int8 parent sliced to r=%d, G=128" % r,
-                   "model": "Llama-3.1-8B", "bits": r, "batch": args.batch, "group_size": 128},
+        "config": workload_config(args.model, ref.n_blocks, r, args.batch, args.gpus),
         "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": "one full transformer block (4 linears, all rows) per step, "
                                    "x32 blocks; backend %s" % backend},
@@ -200,6 +210,66 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def prefill_leg(torch, mq, clocks, batches=(64, 256, 1024), bits=(4, 8), reps=10):
+    """Qwen3-14B linears through K4 (tcgen05) at prefill batches: TFLOP/s per
+    layer and for the 4-layer block, vs the measured bf16 peak and a dense
+    bf16 cuBLAS GEMM of the same shape (3 weight copies rotated: L2-cold)."""
+    from paper_2602_03537_b200.model import QWEN3_14B, KINDS, full_layer_dims
+
+    with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+        pk = json.load(f)
+    tf_peak = float(pk.get("bf16_tflops", 1631.2))
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks.active(True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        e1.synchronize()
+        clocks.active(False)
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    res = {}
+    for kind in KINDS:
+        N, K = full_layer_dims(QWEN3_14B, kind)
+        pts = [mq.PlaneTensor.random_parent(N, K, seed=i) for i in range(3)]
+        Wd = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        for B in batches:
+            X = torch.randn(B, K, device="cuda").to(torch.bfloat16)
+            Y = torch.empty(B, N, device="cuda", dtype=torch.bfloat16)
+            dense = timed(lambda: torch.matmul(X, Wd.t(), out=Y))
+            for r in bits:
+                it = [0]
+
+                def run():
+                    pts[it[0] % 3].gemm(X, r, out=Y)
+                    it[0] += 1
+                t = timed(run)
+                res[(kind, B, r)] = (t, dense, 2.0 * B * N * K)
+        del pts, Wd
+        torch.cuda.empty_cache()
+    out = {"model": "Qwen3-14B", "peak_tflops": tf_peak, "peak_kind": "measured bf16 (burst)",
+           "per_layer": {}, "block": {}}
+    for (kind, B, r), (t, dense, fl) in res.items():
+        out["per_layer"]["%s_B%d_r%d" % (kind, B, r)] = {
+            "us": t * 1e6, "tflops": fl / t / 1e12, "frac": fl / t / 1e12 / tf_peak,
+            "dense_bf16_us": dense * 1e6, "vs_dense": dense / t}
+    for B in batches:
+        for r in bits:
+            t = sum(res[(k, B, r)][0] for k in KINDS)
+            d = sum(res[(k, B, r)][1] for k in KINDS)
+            fl = sum(res[(k, B, r)][2] for k in KINDS)
+            out["block"]["B%d_r%d" % (B, r)] = {
+                "us": t * 1e6, "tflops": fl / t / 1e12, "frac": fl / t / 1e12 / tf_peak,
+                "tok_s_40_blocks": B / (40 * t), "vs_dense": d / t}
+    return out
 
 
 # ------------------------------------------------------------------ GPU arm --
@@ -212,8 +282,11 @@ def main():
     ap.add_argument("--bits", type=int, default=4, choices=LADDER)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=None, help="debug: fewer blocks")
-    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="headline r only (no per-bits, mode C)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-hetero", action="store_true", help="skip the C3 heterogeneous-config leg")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the C4 tcgen05 prefill leg")
+    ap.add_argument("--model", default="Llama-3.1-8B", help="Llama-3.1-8B | Qwen3-14B | Phi-3-Medium")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -233,10 +306,11 @@ def main():
 
     import paper_2602_03537_b200 as mq
     from paper_2602_03537_b200.device import algorithmic_bytes
-    from paper_2602_03537_b200.model import LLAMA31_8B, LinearStack
+    from paper_2602_03537_b200.model import SHAPES, LinearStack
 
     peak, peak_kind = _peaks()
-    stack = LinearStack(LLAMA31_8B, batch=args.batch, tp=world, rank=rank, process_group=pg,
+    shape = SHAPES[args.model]
+    stack = LinearStack(shape, batch=args.batch, tp=world, rank=rank, process_group=pg,
                         n_layers=args.layers)
     n_blocks = stack.n_layers
     clocks = ClockSampler(local)
@@ -362,15 +436,54 @@ def main():
                 stack.layers[i] = (n, kind, pt)
             torch.cuda.empty_cache()
 
+    # C3: heterogeneous per-layer bit-widths (EvoPress-style budget-exact 3.5-bit
+    # config over the unfused linears, the reference's own moves), CUDA graph of
+    # the unfused stack: one launch per linear, each at its own r
+    hetero = None
+    if not args.no_hetero and args.model == "Llama-3.1-8B":
+        from paper_2602_03537_b200.config import budget_config, level_histogram
+
+        del stack.graph
+        cfg = budget_config(3.5, shape=shape, seed=0, mutations=200, n_layers=args.layers)
+        hs = LinearStack(shape, batch=args.batch, tp=world, rank=rank, process_group=pg,
+                         n_layers=args.layers, fused=False)
+        hs.capture(cfg.assignment)
+        for _ in range(args.warmup):
+            hs.step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks.active(True)
+        e0.record(hs.stream)
+        for _ in range(args.steps):
+            hs.step()
+        e1.record(hs.stream)
+        barrier()
+        clocks.active(False)
+        hsec = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+        hb = hs.step_bytes(hs.config)
+        hetero = {"tok_s": args.batch * args.steps / hsec, "ms_per_step": hsec / args.steps * 1e3,
+                  "avg_bits": 3.5, "histogram": {str(k): v for k, v in level_histogram(cfg).items()},
+                  "launches_per_step": hs.launches_per_step(), "GB_per_step": hb / 1e9,
+                  "stack_GBps": hb / (hsec / args.steps) / 1e9,
+                  "stack_frac": hb / (hsec / args.steps) / 1e9 / peak,
+                  "config": "budget_config(3.5, seed=0, mutations=200) over 224 unfused linears"}
+        del hs
+        torch.cuda.empty_cache()
+
+    # C4: prefill on the tcgen05 path (K4), Qwen3-14B linear shapes, per layer
+    prefill = None
+    if not args.no_prefill and world == 1:
+        prefill = prefill_leg(torch, mq, clocks)
+
     clk = clocks.summary()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        ref = CpuReference(r, args.batch, threads)
+        ref = CpuReference(r, args.batch, threads, args.model)
         ref.block_seconds()  # warm-up
         per_block = statistics.median(ref.block_seconds() for _ in range(3))
         ref.close()
-        cpu = {"value": args.batch / (32 * per_block), "unit": UNIT, "cores": threads,
+        cpu = {"value": args.batch / (ref.n_blocks * per_block), "unit": UNIT, "cores": threads,
                "kind": ref.kind,
                "sample": "one full Llama-3.1-8B block (4 linears, all rows) at r=%d, median of 3, "
                          "x32 blocks; %s" % (r, ref.backend)}
@@ -382,14 +495,11 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init int8 parents, N(0,1) bf16 activations)",
-        "config": {"workload": "Llama-3.1-8B linear stack decode: %d blocks x {qkv 6144x4096, "
-                               "o 4096x4096, gate_up 28672x4096, down 4096x14336}, int8 parent "
-                               "sliced on the fly (mode P), G=128" % n_blocks,
-                   "model": "Llama-3.1-8B", "bits": args.bits, "batch": args.batch,
-                   "group_size": 128, "parallelism": "tp%d" % world,
+        "config": dict(workload_config(args.model, n_blocks, args.bits, args.batch, world), **{
+                   "mode": "P (parent resident, sliced on the fly)",
                    "l2": "inputs > L2 (%.1f GB of planes read per step vs 126 MB L2)" % (
                        head["bytes_per_step"] / 1e9),
-                   "graph": "CUDA graph, %d K3 launches/step, PDL" % stack.launches_per_step()},
+                   "graph": "CUDA graph, %d K3 launches/step, PDL" % stack.launches_per_step()}),
         "per_bits": {str(b): {"tok_s": v["tok_s"], "ms_per_step": v["ms_per_step"],
                               "GB_per_step": v["bytes_per_step"] / 1e9,
                               "stack_GBps": v["bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9,
@@ -405,6 +515,8 @@ def main():
                      "kernel": "k_gemv gate_up %dx%d r=%d B=%d" % (pt0.N, pt0.K, r, args.batch),
                      "bytes_per_launch": kbytes, "us_per_launch": k_sec * 1e6,
                      "peak_kind": peak_kind},
+        "hetero_c3": hetero,
+        "prefill_c4": prefill,
         "cpu_baseline": cpu,
         "clocks": clk,
         # K3 launches inside the headline timed region (K captured steps)

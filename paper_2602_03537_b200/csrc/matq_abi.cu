@@ -83,10 +83,14 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     const double fixup = 2.0;  // measured: a split-K tile costs ~2 steps (partials, ticket, reduction)
     const int sms = sm_count();
     double best = 1e30;
-    for (int S = 1; S <= std::min(nsteps, 64); ++S) {
-        if (force_s && S != std::min(force_s, nsteps)) continue;
-        const int cs = mq::cdiv(nsteps, S);
-        if (mq::cdiv(nsteps, cs) != S && !force_s) continue;  // would leave an empty chunk
+    for (int S_try = 1; S_try <= std::min(nsteps, 64); ++S_try) {
+        if (force_s && S_try != std::min(force_s, nsteps)) continue;
+        const int cs = mq::cdiv(nsteps, S_try);
+        // a chunk count that would leave an empty chunk is never used: its
+        // CTAs would not take a ticket and the tile's fixup would never run
+        // (a forced MQ_GEMV_SPLIT is rounded to the effective chunk count)
+        const int S = mq::cdiv(nsteps, cs);
+        if (S != S_try && !force_s) continue;
         const size_t xs = (size_t)ncopy * Bx * (cs * 256 + 8) * 2;
         if (xs > kXsMax && cs > 1) continue;
         int cpc = sms / S;

@@ -52,24 +52,33 @@ PHI3_MEDIUM = DecoderShape("Phi-3-Medium", 5120, 17920, 40, 10, 128, 40)
 SHAPES = {s.name: s for s in (LLAMA31_8B, QWEN3_14B, PHI3_MEDIUM)}
 
 KINDS = ("qkv", "o", "gate_up", "down")
+# unfused linears (heterogeneous configs assign r per q / k / v / gate / up, BASELINE C3)
+KINDS_UNFUSED = ("q", "k", "v", "o", "gate", "up", "down")
 
 
-def layer_names(shape: DecoderShape) -> list[str]:
-    return ["layers.%d.%s" % (i, k) for i in range(shape.n_layers) for k in KINDS]
+def layer_names(shape: DecoderShape, fused: bool = True) -> list[str]:
+    kinds = KINDS if fused else KINDS_UNFUSED
+    return ["layers.%d.%s" % (i, k) for i in range(shape.n_layers) for k in kinds]
 
 
-def tp_layer_dims(shape: DecoderShape, kind: str, tp: int) -> tuple[int, int]:
-    """(N, K) of one rank's shard of a fused linear."""
-    h, inter = shape.hidden, shape.intermediate
-    if kind == "qkv":
-        return shape.qkv_out // tp, h
-    if kind == "o":
-        return h, shape.q_out // tp
-    if kind == "gate_up":
-        return 2 * inter // tp, h
-    if kind == "down":
-        return h, inter // tp
-    raise KeyError(kind)
+def full_layer_dims(shape: DecoderShape, kind: str) -> tuple[int, int]:
+    """(N, K) of an unsharded linear (fused qkv / gate_up, or unfused)."""
+    h, inter, hd = shape.hidden, shape.intermediate, shape.head_dim
+    dims = {"qkv": (shape.qkv_out, h), "o": (h, shape.q_out), "gate_up": (2 * inter, h),
+            "down": (h, inter), "q": (shape.q_out, h), "k": (shape.n_kv_heads * hd, h),
+            "v": (shape.n_kv_heads * hd, h), "gate": (inter, h), "up": (inter, h)}
+    return dims[kind]
+
+
+def tp_layer_dims(shape: DecoderShape, kind: str, tp: int, rank: int = 0) -> tuple[int, int]:
+    """(N, K) of rank ``rank``'s shard (tp.shard_plan: rows for column-parallel,
+    whole scale groups of K for row-parallel)."""
+    N, K = full_layer_dims(shape, kind)
+    if tp == 1:
+        return N, K
+    from .tp import shard_plan
+
+    return shard_plan(kind, N, K, tp, rank).shape
 
 
 def _gain_matched_scales(K: int):
@@ -87,7 +96,7 @@ def _gain_matched_scales(K: int):
 class LinearStack:
     def __init__(self, shape: DecoderShape = LLAMA31_8B, batch: int = 1, group_size: int = 128,
                  tp: int = 1, rank: int = 0, process_group=None, seed: int = 0,
-                 n_layers: int | None = None):
+                 n_layers: int | None = None, fused: bool = True):
         _lib.require_cuda()
         if batch < 1 or batch > 32:
             raise ValueError("decode batch must lie in [1, 32]")
@@ -96,19 +105,21 @@ class LinearStack:
         self.G = group_size
         self.tp, self.rank, self.pg = tp, rank, process_group
         self.n_layers = n_layers or shape.n_layers
+        self.fused = fused
+        kinds = KINDS if fused else KINDS_UNFUSED
         self.layers: list[tuple[str, str, PlaneTensor]] = []
         for i in range(self.n_layers):
-            for kind in KINDS:
-                N, K = tp_layer_dims(shape, kind, tp)
+            for kind in kinds:
+                N, K = tp_layer_dims(shape, kind, tp, rank)
                 pt = PlaneTensor.random_parent(N, K, group_size,
-                                               seed=seed * 1000003 + (i * 4 + KINDS.index(kind)) * 8 + rank,
+                                               seed=seed * 1000003 + (i * 8 + kinds.index(kind)) * 8 + rank,
                                                scale_range=_gain_matched_scales(K * tp if kind in ("o", "down") else K))
                 self.layers.append(("layers.%d.%s" % (i, kind), kind, pt))
         h = shape.hidden
         dev = torch.device("cuda", torch.cuda.current_device())
         self.x = torch.zeros((batch, h), dtype=torch.bfloat16, device=dev)
         self.bufs = {}
-        for name, kind, pt in self.layers[:4]:
+        for name, kind, pt in self.layers[:len(kinds)]:
             self.bufs[kind] = torch.zeros((batch, pt.N), dtype=torch.bfloat16, device=dev)
         self.x_host = torch.zeros((batch, h), dtype=torch.bfloat16, pin_memory=True)
         self.y_host = torch.zeros((batch, h), dtype=torch.bfloat16, pin_memory=True)
@@ -146,18 +157,18 @@ class LinearStack:
         s = self.stream
         x = self.x
         b = self.bufs
+        # fused: x -> qkv -> (q part) -> o -> gate_up -> (gate part) -> down -> x
+        # unfused: x -> q, k, v; q -> o; o -> gate, up; gate -> down -> x
+        src = {"qkv": lambda pt: x, "q": lambda pt: x, "k": lambda pt: x, "v": lambda pt: x,
+               "o": lambda pt: (b["qkv"][:, :pt.K] if self.fused else b["q"]),
+               "gate_up": lambda pt: b["o"], "gate": lambda pt: b["o"], "up": lambda pt: b["o"],
+               "down": lambda pt: (b["gate_up"][:, :pt.K] if self.fused else b["gate"])}
         for name, kind, pt in self.layers:
             r = config[name]
-            if kind == "qkv":
-                pt.gemv(x, r, out=b["qkv"], pdl=pdl, stream=s)
-            elif kind == "o":
-                pt.gemv(b["qkv"][:, :pt.K], r, out=b["o"], pdl=pdl, stream=s)
-                self._all_reduce(b["o"])
-            elif kind == "gate_up":
-                pt.gemv(b["o"], r, out=b["gate_up"], pdl=pdl, stream=s)
-            else:
-                pt.gemv(b["gate_up"][:, :pt.K], r, out=x, pdl=pdl, stream=s)
-                self._all_reduce(x)
+            out = x if kind == "down" else b[kind]
+            pt.linear(src[kind](pt), r, out=out, pdl=pdl, stream=s)
+            if kind in ("o", "down"):
+                self._all_reduce(out)
 
     def capture(self, config, pdl: bool = True) -> None:
         """(Re)capture the decode step for a per-layer bit-width config."""

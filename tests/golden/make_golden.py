@@ -116,6 +116,51 @@ def main() -> None:
                 par["Y_%d_r%d" % (i, r)] = matmul_ref(MatmulTask(X=X, layer=pl))
     par["n_cases"] = np.int64(3)
     np.savez_compressed(os.path.join(HERE, "parent_cases.npz"), **par)
+
+    # 5. EvoPress-style heterogeneous config over the 224 unfused Llama-3.1-8B
+    #    linears: the reference's own budget-exact completion + 200 level
+    #    switches (evo.py:147-172, :53-96), seed 0, budget 3.5 bits (evo.py:186).
+    import json
+
+    from nestquant.evo import _uniform_completed, mutate_level_switch
+
+    dims = {"q": (4096, 4096), "k": (1024, 4096), "v": (1024, 4096), "o": (4096, 4096),
+            "gate": (14336, 4096), "up": (14336, 4096), "down": (4096, 14336)}
+    sizes = {"layers.%d.%s" % (i, k): dims[k][0] * dims[k][1]
+             for i in range(32) for k in ("q", "k", "v", "o", "gate", "up", "down")}
+    budget = int(round(3.5 * sum(sizes.values())))
+    rng = np.random.default_rng(0)
+    cfg = _uniform_completed(budget, sizes, (2, 3, 4, 6, 8), rng)
+    for _ in range(200):
+        cfg, _ = mutate_level_switch(cfg, sizes, rng)
+    with open(os.path.join(HERE, "llama31_8b_3p5bit_seed0.json"), "w") as fh:
+        json.dump({"budget_bits": budget, "assignment": cfg.assignment}, fh, indent=0, sort_keys=True)
+
+    # 6. MQPT containers written by the reference (checkpoint.py:78-107): an
+    #    int8 parent (raw-byte code sections) and a sliced model with per-layer
+    #    bit-widths (bit-plane packed sections for r <= 4).
+    from nestquant.checkpoint import Checkpoint, SlicedModel, write_checkpoint
+
+    rng = np.random.default_rng(99)
+    bws = BitWidthSet((2, 3, 4, 6, 8), (1.0, 0.5, 0.25, 0.125, 0.0625))
+    layers, ck = [], {}
+    for i, (n, k, G) in enumerate([(24, 256, 128), (17, 200, 128), (8, 1000, 128)]):
+        G = 128
+        codes = rng.integers(0, 256, size=(n, k)).astype(np.uint8)
+        scales = rng.uniform(0.005, 0.02, size=(n, -(-k // G))).astype(np.float32)
+        layers.append(NestedLayer(name="blk.%d" % i, codes=codes, grid=QuantGrid(8, G, scales), bits=bws))
+        ck["codes_%d" % i] = codes
+        ck["scales_%d" % i] = scales
+    parent = Checkpoint(bits=bws, group_size=128, damp_rel=0.01, layers=layers)
+    write_checkpoint(parent, os.path.join(HERE, "parent.mqpt"))
+    sl = [slice_layer(ly, r) for ly, r in zip(layers, (2, 6, 4))]
+    for i, s_ in enumerate(sl):
+        ck["child_codes_%d" % i] = s_.codes
+        ck["child_scales_%d" % i] = s_.scales
+        ck["child_bits_%d" % i] = np.int64(s_.bits)
+    child = SlicedModel(master_bits=8, bits=bws, group_size=128, damp_rel=0.01, layers=sl)
+    write_checkpoint(child, os.path.join(HERE, "sliced.mqpt"))
+    np.savez_compressed(os.path.join(HERE, "mqpt_cases.npz"), **ck)
     print("golden fixtures written to", HERE)
 
 

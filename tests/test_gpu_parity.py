@@ -174,7 +174,7 @@ def test_gemv_forced_decompositions(mq, split, monkeypatch):
             want = O.parent_matmul_ref(codes, scales, 128, r, X)
             for _ in range(2):
                 got = pt.gemv(Xd, r, out_dtype=torch.float32).cpu().numpy()
-                assert rel_err(got, want) <= 1e-4, (mode, n, k, B, r)
+                assert rel_err(got, want) <= 1e-4, (split, n, k, B, r)
 
 
 def test_gemv_mode_c_matches_mode_p(mq):
