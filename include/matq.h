@@ -132,6 +132,32 @@ MQ_API int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ld
                    int K, int G, int nplanes, int r, float out_scale, int flags, void* workspace,
                    size_t workspace_bytes, void* stream);
 
+/* K3S: a whole decode step -- every sliced linear of a model, in dependency
+ * order (layer i+1 reads layer i's output) -- as ONE persistent cooperative
+ * kernel (one CTA per SM).  Replaces a per-layer loop of mq_gemv calls (and
+ * the reference's per-layer packed_matmul calls); each layer's weight ring
+ * keeps streaming across layer boundaries while the previous layer drains.
+ * Uniform r, G = 128, bf16 X/Y, 1 <= B <= 16.
+ *   1. mq_stack_plan: host-only; fills a host plan (mq_stack_plan_bytes()) and
+ *      a host layer table (mq_stack_table_bytes(n)) and returns the workspace
+ *      size.  Copy the table to device memory (any time before the run).
+ *   2. mq_stack_run: launches one step (async, graph-capturable).  The
+ *      workspace must be zero-filled ONCE; its completion counters only grow,
+ *      so steps replay without resets. */
+typedef struct mq_stack_layer {
+    const uint32_t* blob; /* P8 blob (parent: nplanes planes) */
+    const void* X;        /* bf16 (B, K), row stride ldx, 16-byte aligned */
+    void* Y;              /* bf16 (B, N), row stride ldy */
+    int ldx, ldy, N, K;
+    float out_scale;      /* 2^(c - r) for a parent slice */
+} mq_stack_layer;
+MQ_API size_t mq_stack_plan_bytes(void);
+MQ_API size_t mq_stack_table_bytes(int n_layers);
+MQ_API int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes,
+                         void* plan_host, void* table_host, size_t* workspace_bytes);
+MQ_API int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* ---- format-layer helpers behind the drop-in Python API --------------- */
 
 /* slice_code / slice_to_code (slicing.py:31-54) over n codes at master

@@ -56,6 +56,10 @@ _SIGS = {
     "mq_gemv": ([_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
     "mq_gemm_workspace_bytes": ([_i, _i, _i, _i], _sz),
     "mq_gemm": ([_vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _f, _i, _vp, _sz, _vp], _i),
+    "mq_stack_plan_bytes": ([], _sz),
+    "mq_stack_table_bytes": ([_i], _sz),
+    "mq_stack_plan": ([_vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
+    "mq_stack_run": ([_vp, _vp, _vp, _sz, _vp], _i),
     "mq_slice_elementwise": ([_vp, _ll, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_f64": ([_vp, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_value_f64": ([_vp, _vp, _ll, _i, _i, _vp, _vp, _vp], _i),
@@ -70,6 +74,14 @@ for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_L, _name)
     _fn.argtypes = _args
     _fn.restype = _res
+
+
+class StackLayer(ctypes.Structure):
+    """struct mq_stack_layer (include/matq.h)."""
+
+    _fields_ = [("blob", ctypes.c_void_p), ("X", ctypes.c_void_p), ("Y", ctypes.c_void_p),
+                ("ldx", ctypes.c_int), ("ldy", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
+                ("out_scale", ctypes.c_float)]
 
 
 class MatqError(RuntimeError):

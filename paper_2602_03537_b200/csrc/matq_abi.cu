@@ -13,6 +13,7 @@
 #include "../../include/matq.h"
 #include "matq_gemv.cuh"
 #include "matq_internal.h"
+#include "matq_stack.cuh"
 
 namespace {
 
@@ -70,14 +71,15 @@ int env_int(const char* name, int dflt) {
 // contiguous per-warp ranges -- was measured and lost to the fixups; see
 // DESIGN.md 4.)
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
-                              bool honour_overrides = true) {
+                              bool honour_overrides = true, int force_warps = 0) {
     GemvConfig c{};
     const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
     // tuning overrides (scripts/sweep_gemv.py): MQ_GEMV_WARPS, MQ_GEMV_SPLIT, MQ_GEMV_STAGES,
     // MQ_GEMV_STREAM (0 = never, 1 = force when it fits)
-    c.nwarps = std::max(4, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
+    c.nwarps = force_warps ? force_warps
+                           : std::max(4, std::min(mq::kMaxWarps, env_int("MQ_GEMV_WARPS", c.NT >= 4 ? 8 : 16)));
     c.nwarps &= ~3;
     const int force_s = honour_overrides ? env_int("MQ_GEMV_SPLIT", 0) : 0;
     const double fixup = 2.0;  // measured: a split-K tile costs ~2 steps (partials, ticket, reduction)
@@ -113,7 +115,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
         }
     }
     if (c.S == 0)  // overrides admitted no configuration: ignore them
-        return choose_gemv_config(N, K, Bx, npl, g128, r, false);
+        return choose_gemv_config(N, K, Bx, npl, g128, r, false, force_warps);
     c.slots = c.S;
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
@@ -163,6 +165,17 @@ GemvConfig cached_config(int N, int K, int Bx, int npl, bool g128, int r) {
     return c;
 }
 
+#ifdef MQ_GEMV_TIMING
+unsigned long long* dbg_buffer() {
+    static unsigned long long* buf = nullptr;
+    if (!buf) {
+        const size_t bytes = sizeof(unsigned long long) * (size_t)mq::kTsSlots * mq::kTsCtas * mq::kTsEvents;
+        if (cudaMalloc(&buf, bytes) == cudaSuccess) cudaMemset(buf, 0, bytes);
+    }
+    return buf;
+}
+#endif
+
 mq::GemvLaunchFn gemv_launcher(int r) {
     switch (r) {
         case 2: return mq::launch_gemv_r<2>;
@@ -181,6 +194,20 @@ extern "C" {
 int mq_arch(void) { return 100; }
 
 const char* mq_version(void) { return "matq 0.1.0 (sm_100a)"; }
+
+#ifdef MQ_GEMV_TIMING
+// Profiling builds only (scripts/phase_timing.py): phase timestamps of the last 64 K3 launches.
+MQ_API int mq_debug_timestamps(unsigned long long* out, int n) {
+    const size_t bytes = sizeof(unsigned long long) * (size_t)mq::kTsSlots * mq::kTsCtas * mq::kTsEvents;
+    if ((size_t)n * sizeof(unsigned long long) < bytes) return MQ_ERR_INVALID;
+    if (cudaMemcpy(out, dbg_buffer(), bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return MQ_ERR_CUDA;
+    return MQ_OK;
+}
+MQ_API int mq_debug_reset(void) {
+    const size_t bytes = sizeof(unsigned long long) * (size_t)mq::kTsSlots * mq::kTsCtas * mq::kTsEvents;
+    return cudaMemset(dbg_buffer(), 0, bytes) == cudaSuccess ? MQ_OK : MQ_ERR_CUDA;
+}
+#endif
 
 const char* mq_last_error(void) { return g_err; }
 
@@ -335,6 +362,11 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     p.cs_off = c.cs_off;
     p.xs_bytes = c.xs_bytes;
     p.stages = c.stages;
+#ifdef MQ_GEMV_TIMING
+    static int dbg_ctr = 0;
+    p.dbg_slot = dbg_ctr++ % mq::kTsSlots;
+    p.dbg_ts = dbg_buffer();
+#endif
     const dim3 grid(c.grid, 1, 1), block(32 * c.nwarps, 1, 1);
     const int gs = (G == 128) ? 128 : 0;
     const cudaError_t e = gemv_launcher(r)(p, c.NT, child_mode, gs, grid, block, c.smem,
@@ -374,6 +406,171 @@ int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int 
                                           (flags & MQ_PDL) != 0, &why);
     if (e != cudaSuccess && *why) return fail(MQ_ERR_CUDA, "mq_gemm: %s", why);
     return cuda_status(e, "mq_gemm");
+}
+
+// ---- K3S: the whole decode step as one persistent kernel ---------------------
+namespace {
+struct StackPlanHost {  // the opaque host plan (mq_stack_plan_bytes)
+    mq::StackParams p;
+    int r, nplanes, nt, grid;
+    size_t smem;
+    size_t ws_bytes;
+};
+// K3S per-layer decomposition: K chunks S (activation staging bounded by
+// kXsMax), the chunk's row tiles split contiguously over cpc = sms / S CTAs,
+// and each CTA's (tile, step) pairs split evenly over its 16 warps.  Cost =
+// the busiest SMSP's steps (4 warps share one) + a split-K fixup allowance.
+struct StackCfg {
+    int S, cs, cpc;
+};
+StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms) {
+    const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
+    constexpr size_t kXsMaxStack = 80 * 1024;  // the stack ring needs only 2-4 stages
+    StackCfg best_c{nsteps, 1, std::max(1, std::min(sms / nsteps, n_rt))};
+    double best = 1e30;
+    for (int S_try = 1; S_try <= nsteps; ++S_try) {
+        const int cs = mq::cdiv(nsteps, S_try);
+        const int S = mq::cdiv(nsteps, cs);
+        if (S != S_try) continue;
+        const size_t xs = (size_t)ncopy * B * (cs * 256 + 8) * 2;
+        if (xs > kXsMaxStack && cs > 1) continue;
+        const int cpc = std::min(sms / S, n_rt);
+        if (cpc < 1) break;
+        const int work = mq::cdiv(n_rt, cpc) * cs;          // busiest CTA
+        const double per_warp = (double)mq::cdiv(work, mq::kStackWarps);
+        const double cost = 4.0 * per_warp + (S > 1 ? 3.0 : 0.0) + (work % mq::kStackWarps ? 0.5 : 0.0);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_c = StackCfg{S, cs, cpc};
+        }
+    }
+    return best_c;
+}
+
+size_t stack_ws_layout(int n_layers, size_t partial_bytes, size_t* off_done, size_t* off_partials) {
+    // [tickets 64 KB][done counters n + launch counter][partials]
+    *off_done = kTicketBytes;
+    *off_partials = kTicketBytes + (((size_t)(n_layers + 1) * 4 + 255) & ~(size_t)255);
+    return *off_partials + partial_bytes;
+}
+}  // namespace
+
+#ifdef MQ_GEMV_TIMING
+static unsigned long long* g_stack_dbg = nullptr;
+MQ_API int mq_debug_stack_timestamps(unsigned long long* out, int n) {
+    const size_t bytes = sizeof(unsigned long long) * (256 * 148 * 8 + 256 * 16 * 4);
+    if (!g_stack_dbg || (size_t)n * 8 < bytes) return MQ_ERR_INVALID;
+    return cudaMemcpy(out, g_stack_dbg, bytes, cudaMemcpyDeviceToHost) == cudaSuccess ? MQ_OK : MQ_ERR_CUDA;
+}
+#endif
+
+size_t mq_stack_plan_bytes(void) { return sizeof(StackPlanHost); }
+size_t mq_stack_table_bytes(int n_layers) { return n_layers < 0 ? 0 : sizeof(mq::StackLayer) * (size_t)n_layers; }
+
+int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes, void* plan_host,
+                  void* table_host, size_t* workspace_bytes) {
+    if (!layers || !plan_host || !table_host || !workspace_bytes || n_layers < 1)
+        return fail(MQ_ERR_INVALID, "null pointer or empty stack");
+    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (nplanes < r || nplanes > 8 || (nplanes != r && nplanes < r + 1))
+        return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", r, nplanes);
+    if (B < 1 || B > 16) return fail(MQ_ERR_INVALID, "stack decode batch %d outside [1, 16]", B);
+    StackPlanHost* P = reinterpret_cast<StackPlanHost*>(plan_host);
+    mq::StackLayer* T = reinterpret_cast<mq::StackLayer*>(table_host);
+    memset(P, 0, sizeof(*P));
+    const bool child = nplanes == r;
+    const int npl = (child || r == 8) ? r : r + 1;
+    const int ncopy = r != 8 ? mq::zp_ncopies(r) : 1;
+    const int nt = B <= 8 ? 1 : 2;
+    int cs_max = 1;
+    size_t partials = 0;
+    for (int i = 0; i < n_layers; ++i) {
+        const mq_stack_layer& in = layers[i];
+        if (!in.blob || !in.X || !in.Y) return fail(MQ_ERR_INVALID, "layer %d: null pointer", i);
+        if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < in.N || (in.ldx & 7) ||
+            (reinterpret_cast<uintptr_t>(in.X) & 15))
+            return fail(MQ_ERR_INVALID, "layer %d: bad shape / alignment", i);
+        const StackCfg c = choose_stack_config(in.N, in.K, B, ncopy, sm_count());
+        const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
+        if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
+        mq::StackLayer& t = T[i];
+        t.blob = in.blob;
+        t.step_words = L.step_words;
+        t.X = reinterpret_cast<const uint16_t*>(in.X);
+        t.Y = reinterpret_cast<uint16_t*>(in.Y);
+        t.ldx = in.ldx;
+        t.ldy = in.ldy;
+        t.N = in.N;
+        t.Np = L.Np;
+        t.K = in.K;
+        t.nsteps = L.nsteps;
+        t.n_rt = L.n_rt;
+        t.S = c.S;
+        t.cs = c.cs;
+        t.cpc = c.cpc;
+        t.out_scale = in.out_scale;
+        cs_max = std::max(cs_max, c.cs);
+        if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
+    }
+    mq::StackParams& p = P->p;
+    p.n_layers = n_layers;
+    p.B = B;
+    p.xs_stride = cs_max * 256 + 8;
+    p.xcopy_stride = B * p.xs_stride;
+    p.cs_off = (int)(((size_t)ncopy * p.xcopy_stride * 2 + 15) & ~(size_t)15);
+    const size_t zc_bytes = r != 8 ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
+    p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
+    const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
+    p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
+    p.table_off = p.flag_off;
+    p.xs_bytes = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
+    const size_t stage = (size_t)npl * 512 + 128;
+    const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 8;
+    const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage));
+    if (d < 2) return fail(MQ_ERR_INVALID, "stack: activation staging leaves no room for the weight ring");
+    p.stages = std::min(8, d);
+    P->smem = fixed + (size_t)mq::kStackWarps * p.stages * stage;
+    P->r = r;
+    P->nplanes = nplanes;
+    P->nt = nt;
+    P->grid = sm_count();
+    size_t od, op;
+    P->ws_bytes = stack_ws_layout(n_layers, partials, &od, &op);
+    *workspace_bytes = P->ws_bytes;
+    return MQ_OK;
+}
+
+int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, size_t workspace_bytes,
+                 void* stream) {
+    if (!plan_host || !table_dev || !workspace) return fail(MQ_ERR_INVALID, "null pointer");
+    const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
+    if (workspace_bytes < P->ws_bytes)
+        return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
+    mq::StackParams p = P->p;
+    size_t od, op;
+    stack_ws_layout(p.n_layers, 0, &od, &op);
+    char* w = reinterpret_cast<char*>(workspace);
+    p.layers = reinterpret_cast<const mq::StackLayer*>(table_dev);
+    p.tickets = reinterpret_cast<int*>(w);
+    p.done = reinterpret_cast<unsigned*>(w + od);
+    p.launch_ctr = p.done + p.n_layers;
+    p.ws = reinterpret_cast<float*>(w + op);
+#ifdef MQ_GEMV_TIMING
+    static unsigned long long* sbuf = nullptr;
+    if (!sbuf) cudaMalloc(&sbuf, sizeof(unsigned long long) * (256 * 148 * 8 + 256 * 16 * 4));
+    p.dbg_ts = sbuf;
+    g_stack_dbg = sbuf;
+#endif
+    const bool child = P->nplanes == P->r;
+    cudaError_t e;
+    switch (P->r) {
+        case 2: e = mq::launch_stack_r<2>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
+        case 3: e = mq::launch_stack_r<3>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
+        case 4: e = mq::launch_stack_r<4>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
+        case 6: e = mq::launch_stack_r<6>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
+        default: e = mq::launch_stack_r<8>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
+    }
+    return cuda_status(e, "mq_stack_run");
 }
 
 static int sync_and_check(cudaError_t launch, int* err_dev, cudaStream_t s, const char* where,

@@ -30,6 +30,21 @@
 
 namespace mq {
 
+#ifdef MQ_GEMV_TIMING
+// Phase timestamps (globaltimer ns) per (launch slot, CTA, event): profiling builds only.
+constexpr int kTsSlots = 64, kTsCtas = 160, kTsEvents = 6;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define MQ_TS(ev) do { if (threadIdx.x == 0 && blockIdx.x < kTsCtas) p.dbg_ts[((size_t)p.dbg_slot * kTsCtas + blockIdx.x) * kTsEvents + (ev)] = gtimer(); } while (0)
+#define MQ_TS_MAX(ev) do { if ((threadIdx.x & 31) == 0 && blockIdx.x < kTsCtas) atomicMax(&p.dbg_ts[((size_t)p.dbg_slot * kTsCtas + blockIdx.x) * kTsEvents + (ev)], gtimer()); } while (0)
+#else
+#define MQ_TS(ev) do { } while (0)
+#define MQ_TS_MAX(ev) do { } while (0)
+#endif
+
 struct GemvParams {
     const uint32_t* blob;     // step-interleaved blob (parent: 8 planes, child: r planes)
     long long step_words;     // words per (row tile, step) block
@@ -53,6 +68,8 @@ struct GemvParams {
     int cs_off;               // smem byte offset of the per-group zero-point constants
     int xs_bytes;             // smem bytes of the X staging area (16-aligned)
     int stages;               // per-warp TMA ring depth (<= 8)
+    int dbg_slot;             // MQ_GEMV_TIMING builds: timestamp slot of this launch
+    unsigned long long* dbg_ts;
 };
 
 #ifndef MQ_GEMV_DEBUG
@@ -122,8 +139,10 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     // waiting on the programmatic dependency (X, workspace, Y).
     if (lane == 0 && !(MQ_GEMV_DEBUG & 2))
         for (int i = 0; i < D && i < total; ++i) issue_next();
+    MQ_TS(0);
     pdl_launch_dependents();
     pdl_wait();
+    MQ_TS(1);
 
     // ---- stage X[:, chunk columns] into shared memory as bf16 rows ----------
     // copy c (ZP only) holds x * 2^-zp_copy_off(R, c): exact power-of-two scaling.
@@ -186,6 +205,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         }
     }
     __syncthreads();
+    MQ_TS(2);
 
     // ldmatrix row addresses: matrix mi = lane >> 3 covers k offset 8*mi of a
     // 32-column pair of k16 steps; row n = nt*8 + (lane & 7) (rows >= Bx read
@@ -249,6 +269,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         }
         __syncthreads();
     }
+    MQ_TS(3);
 
     float tot[NT][4];
     float acc[NT][4];
@@ -355,6 +376,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             reinterpret_cast<uint16_t*>(p.Y)[(long long)b * p.ldy + row] = f32_to_bf16_rn(v);
     };
     auto finalize = [&](int rt) {
+        MQ_TS_MAX(5);
         if constexpr (GS == 0) flush_generic();
         const int r0 = rt * kTileRows + g;
         float v[NT][2][2];  // [nt][row half][column parity | hi+lo combined]
@@ -402,8 +424,10 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         // release-RMW on the tile ticket; the last arriver acquires.
         __syncwarp();
         int last = 0;
-        if (lane == 0) last = (atom_add_acq_rel(p.tickets + rt, 1) == p.S - 1);
-        last = __shfl_sync(0xffffffffu, last, 0);
+        // lane 1, not lane 0: lane 0 issues the ring's bulk copies, and an acq_rel
+        // RMW would wait for those in-flight loads to land
+        if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == p.S - 1);
+        last = __shfl_sync(0xffffffffu, last, 1);
         if (!last) return;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -474,6 +498,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             parity ^= 1u;
         }
     }
+    MQ_TS_MAX(4);
 }
 
 // Host-side launcher table entry, implemented per R in matq_gemv_r*.cu.

@@ -1,0 +1,524 @@
+// matq_stack.cuh -- K3S: the whole decode step (every sliced linear of a model)
+// as ONE persistent kernel.
+//
+// The per-layer K3 launch pays a fixed ~4-5 us per layer (grid launch and
+// drain, the dependent-launch release, the weight ring refilling from empty,
+// activation staging, zero-point constants) -- about a third of a Llama-3.1-8B
+// decode step (scripts/phase_timing.py).  K3S keeps one CTA per SM resident
+// for the whole step and walks a table of layers (StackLayer, in HBM):
+//   * every warp owns a TMA bulk-copy ring of weight steps whose issue cursor
+//     runs across layer boundaries: while a layer's last tiles finish, the
+//     next layer's first steps are already streaming into shared memory;
+//   * layer l+1 reads layer l's output, so before staging its activations a
+//     CTA waits until every CTA has published layer l: __syncthreads, thread
+//     0 fence + atomicAdd on the layer's counter (release), and the waiter's
+//     thread 0 spins on ld.acquire.gpu (the cooperative-groups grid.sync
+//     pattern, per layer).  Counters only grow: launch g waits for
+//     (g + 1) * gridDim.x, g taken from a launch counter at entry, so a graph
+//     replays without resets.  Co-residency of all CTAs is guaranteed by a
+//     cooperative launch;
+//   * the per-layer work split, slice, decode, zero-point folding, mma.sync
+//     and split-K fixup are K3's (matq_gemv.cuh) -- the same device code paths.
+// Uniform r (template R) and G = 128; heterogeneous configs and TP stacks use
+// per-layer K3 launches in a CUDA graph.
+#pragma once
+#include "matq_common.cuh"
+
+namespace mq {
+
+struct __align__(8) StackLayer {
+    const uint32_t* blob;
+    long long step_words;
+    const uint16_t* X;  // bf16 [B][ldx]
+    uint16_t* Y;        // bf16 [B][ldy]
+    int ldx, ldy;
+    int N, Np, K, nsteps, n_rt;
+    int S, cs, cpc;  // K chunks, steps per chunk, CTAs per chunk
+    float out_scale;
+};
+
+struct StackParams {
+    const StackLayer* layers;  // device array
+    int n_layers;
+    int B;
+    int xs_stride;     // smem activation row stride (elements), max over layers
+    int xcopy_stride;  // elements between activation copies
+    int cs_off;        // byte offset of the zero-point constants
+    int xs_bytes;      // bytes of the staging area (activations + constants + partial slots)
+    int slot_off;      // byte offset of the per-warp partial-tile slots [16][32 lanes][NT * 4]
+    int flag_off;      // (unused)
+    int table_off;     // byte offset of the shared-memory copy of the layer table
+    int stages;        // per-warp ring depth
+    float* ws;         // split-K partials (max over layers)
+    int* tickets;      // split-K tickets, self-resetting
+    unsigned* done;    // [n_layers] monotone completion counters
+    unsigned* launch_ctr;
+    unsigned long long* dbg_ts;  // MQ_GEMV_TIMING builds: [n_layers][148][8] globaltimer stamps
+};
+
+#ifdef MQ_GEMV_TIMING
+__device__ __forceinline__ unsigned long long stack_gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define MQ_STS(l, ev) do { if (threadIdx.x == 0 && p.dbg_ts && blockIdx.x < 148) \
+    p.dbg_ts[((size_t)(l) * 148 + blockIdx.x) * 8 + (ev)] = stack_gtimer(); } while (0)
+#define MQ_STS_WMAX(l, ev) do { if ((threadIdx.x & 31) == 0 && p.dbg_ts && blockIdx.x < 148) \
+    atomicMax(&p.dbg_ts[((size_t)(l) * 148 + blockIdx.x) * 8 + (ev)], stack_gtimer()); } while (0)
+// per-warp stamps of CTA 0: [256 layers][16 warps][4]
+#define MQ_STS_W0(l, ev) do { if ((threadIdx.x & 31) == 0 && p.dbg_ts && blockIdx.x == 0) \
+    p.dbg_ts[256 * 148 * 8 + ((size_t)(l) * 16 + (threadIdx.x >> 5)) * 4 + (ev)] = stack_gtimer(); } while (0)
+#else
+#define MQ_STS_WMAX(l, ev) do { } while (0)
+#define MQ_STS_W0(l, ev) do { } while (0)
+#define MQ_STS(l, ev) do { } while (0)
+#endif
+
+constexpr int kStackWarps = 15;                      // ring (work) warps
+constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp without a ring
+
+// A warp's share of one layer.  CTA c works on K chunk kc = c % S and the
+// contiguous row tiles [ta, ta + ntiles) of that chunk (near-equal split over
+// the chunk's cpc CTAs); its ntiles x ns (tile, step) pairs, flattened
+// tile-major, are split into 16 near-equal contiguous ranges [f0, f1), one per
+// warp.  A tile cut by a warp boundary is summed in warp order through
+// shared memory; a tile cut by a chunk boundary (S > 1) through the split-K
+// workspace and a ticket -- both deterministic.
+struct WarpPlan {
+    int ta, ntiles, ns, chunk0, kc, f0, f1;
+};
+__device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int warp) {
+    WarpPlan w{};
+    if (cta >= L.cpc * L.S) return w;
+    w.kc = cta % L.S;
+    const int j = cta / L.S;
+    w.ta = (int)((long long)j * L.n_rt / L.cpc);
+    w.ntiles = (int)((long long)(j + 1) * L.n_rt / L.cpc) - w.ta;
+    w.chunk0 = w.kc * L.cs;
+    w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
+    const int P = w.ntiles * w.ns;
+    w.f0 = (int)((long long)warp * P / kStackWarps);
+    w.f1 = (int)((long long)(warp + 1) * P / kStackWarps);
+    return w;
+}
+__device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
+    return (int)((long long)warp * (w.ntiles * w.ns) / kStackWarps);
+}
+
+// Publish: bar.sync orders the CTA's writes before thread 0's release at gpu
+// scope (cumulative), which the waiters' ld.acquire.gpu synchronises with.
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void st_release_cta(uint32_t saddr, unsigned v) {
+    asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_cta(uint32_t saddr) {
+    unsigned v;
+    asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int R, int NT, bool CHILD>
+__global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p) {
+    constexpr int NPL = PlaneCount<R, CHILD>::value;
+    constexpr uint32_t kSlab = 512, kScaleBytes = 128;
+    constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
+    constexpr bool ZP = R != 8;
+    constexpr int NCOPY = ZP ? zp_ncopies(R) : 1;
+    extern __shared__ __align__(16) uint8_t smem[];
+    uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
+    __shared__ unsigned s_gen;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warps 0..14 stream weights (lane 0 issues their ring's bulk copies); warp 15
+    // only synchronises: its fences never wait on in-flight bulk copies (a
+    // memory barrier on a warp with outstanding cp.async.bulk waits for them)
+    const bool ring_warp = warp < kStackWarps;
+    constexpr int kSyncThread = kStackWarps * 32;
+    const int g = lane >> 2, t = lane & 3;
+    const int cta = blockIdx.x;
+    const int D = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
+    uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 8;
+    const uint32_t my_bar0 = smem_addr(bars + warp * 8);
+    const uint32_t my_ring0 = smem_addr(ring + (size_t)warp * D * kStageBytes);
+    if (threadIdx.x == kSyncThread) s_gen = atomicAdd(p.launch_ctr, 1u) / gridDim.x;
+    // the layer table lives in shared memory: a descriptor field re-read from
+    // global memory mid-layer (register rematerialisation) waits behind the
+    // weight stream for ~1-2 us
+    StackLayer* tab = reinterpret_cast<StackLayer*>(smem + p.table_off);
+    {
+        const int words = p.n_layers * (int)(sizeof(StackLayer) / 4);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.layers);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(tab);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    uint64_t policy = 0;
+    if (ring_warp && lane == 0) {
+        policy = policy_evict_first();
+        for (int i = 0; i < D; ++i) mbar_init(my_bar0 + 8 * i, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const unsigned target = (s_gen + 1u) * gridDim.x;
+
+    // ---- issue cursor: (layer, flattened step f) of this warp, across layers --
+    int il = -1, iff = 0, istage = 0, itile = 0, isi = 0;
+    WarpPlan ip{};
+    const uint32_t* iblob = nullptr;
+    long long isw = 0;
+    int insteps = 0;
+    auto next_layer = [&]() {  // advance il to the next layer with work for this warp
+        for (++il; il < p.n_layers; ++il) {
+            const StackLayer& L = tab[il];
+            ip = warp_plan(L, cta, warp);
+            if (ip.f1 > ip.f0) {
+                iblob = L.blob;
+                isw = L.step_words;
+                insteps = L.nsteps;
+                iff = ip.f0;
+                itile = ip.ta + ip.f0 / ip.ns;
+                isi = ip.f0 % ip.ns;
+                return;
+            }
+        }
+    };
+    auto issue_next = [&]() {  // lane 0; no-op once the warp has nothing left
+        if (il >= p.n_layers) return;
+        const uint32_t* src = iblob + ((long long)itile * insteps + ip.chunk0 + isi) * isw;
+        if (++isi == ip.ns) {
+            isi = 0;
+            ++itile;
+        }
+        const uint32_t bar = my_bar0 + 8 * istage;
+        mbar_expect_tx(bar, kStageBytes);
+        bulk_g2s(my_ring0 + istage * kStageBytes, src, kStageBytes, bar, policy);
+        if (++istage == D) istage = 0;
+        if (++iff == ip.f1) next_layer();
+    };
+    if (ring_warp && lane == 0) {
+        next_layer();
+        for (int i = 0; i < D; ++i) issue_next();
+    }
+
+    int cstage = 0;
+    uint32_t parity = 0;
+    const uint32_t xs_saddr = smem_addr(xs);
+    float* zc = reinterpret_cast<float*>(smem + p.cs_off);  // [2 cs groups][NT * 8] zero-point constants
+
+#pragma unroll 1
+    for (int l = 0; l < p.n_layers; ++l) {
+        const StackLayer& L = tab[l];
+        const WarpPlan wp = ring_warp ? warp_plan(L, cta, warp) : warp_plan(L, cta, 0);
+        const int Kc = L.cs * kStepCols;
+        const int col_base = wp.chunk0 * kStepCols;
+        const int col_base_cta = col_base;  // every warp of the CTA shares its chunk
+
+        // ---- wait for the producer of this layer's activations ---------------
+        MQ_STS(l, 0);
+        if (l > 0 && threadIdx.x == kSyncThread) {
+            while (ld_acquire_u32(p.done + l - 1) < target) {
+            }
+        }
+        __syncthreads();
+        MQ_STS(l, 1);
+
+        // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
+        {
+            const uint16_t* X = L.X;
+            const int c8 = Kc >> 3;
+            const int n8 = p.B * c8;
+            constexpr int kU = 4;  // loads in flight per thread before the first use
+            for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+                uint4 vv[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int idx = base_i + u * (int)blockDim.x;
+                    vv[u] = make_uint4(0, 0, 0, 0);
+                    if (idx < n8) {
+                        const int b = idx / c8, c = (idx - b * c8) * 8;
+                        const int col = col_base_cta + c;
+                        if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                const int idx = base_i + u * (int)blockDim.x;
+                if (idx >= n8) break;  // warp-uniform: n8 is a multiple of 32
+                const int b = idx / c8, c = (idx - b * c8) * 8;
+                const uint4 v = vv[u];
+                *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
+                if constexpr (ZP) {
+                    // zero-point constant of the 128-column group: sum (128 2^-o + z) x over the
+                    // group; the 8 columns here share the field offset o (16 lanes = 1 group)
+                    const int cs_ = c & 255;
+                    const int o = zp_off<R>((cs_ & 63) >> 4, (cs_ & 15) >> 3);
+                    const float m = 128.0f / (float)(1 << o) + (float)(1 << (R - 1));
+                    const uint16_t* hx = reinterpret_cast<const uint16_t*>(&v);
+                    float part = 0.0f;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) part += bf16_to_f32(hx[e]);
+                    part *= m;
+#pragma unroll
+                    for (int sh = 8; sh >= 1; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
+                    if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
+                }
+                if constexpr (NCOPY > 1) {
+                    const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
+#pragma unroll
+                    for (int cp = 1; cp < NCOPY; ++cp) {
+                        uint4 o;
+                        uint16_t* ho = reinterpret_cast<uint16_t*>(&o);
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            ho[e] = f32_to_bf16_rn(bf16_to_f32(hv[e]) * (1.0f / (float)(1 << zp_copy_off(R, cp))));
+                        *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = o;
+                    }
+                }
+                }
+            }
+        }
+        __syncthreads();
+        MQ_STS(l, 2);
+
+        uint32_t xrow_addr[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            int n = nt * 8 + (lane & 7);
+            if (n >= p.B) n = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < 2; ++s2) {
+                const int mi = lane >> 3;
+                int cp = 0;
+                if constexpr (ZP) {
+                    const int sx = 2 * s2 + (mi >> 1), hx = mi & 1;
+                    cp = zp_copy_of(R, zp_off<R>(sx, hx));
+                }
+                xrow_addr[nt][s2] = xs_saddr + (uint32_t)(cp * p.xcopy_stride + n * p.xs_stride + 8 * mi) * 2u;
+            }
+        }
+        MQ_STS(l, 3);
+
+        // ---- this warp's units of layer l --------------------------------------
+        float tot[NT][4], acc[NT][4];
+        auto process = [&](const uint4 (&buf)[NPL], const float (&sc)[4], int st) {
+            const uint32_t xcol = (uint32_t)(st * kStepCols - col_base);
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+                uint32_t T[NPL];
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
+                uint32_t A[16];
+                uint32_t Sl[R];
+                slice_loaded<R, CHILD>(T, Sl);
+                decode_word<R, ZP>(Sl, A);
+#pragma unroll
+                for (int s2 = 0; s2 < 2; ++s2) {
+                    uint32_t bf[NT][4];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+                        ldmatrix_x4(bf[nt], xrow_addr[nt][s2] + (xcol + 64 * w + 32 * s2) * 2u);
+#pragma unroll
+                    for (int sh = 0; sh < 2; ++sh) {
+                        const int s = 2 * s2 + sh;
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            if ((w & 1) == 0 && s == 0)
+                                mma_zero(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                         bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                            else
+                                mma_acc(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                        bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                        }
+                    }
+                }
+                if (w & 1) {
+                    const float s_lo = sc[(w >> 1) * 2], s_hi = sc[(w >> 1) * 2 + 1];
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        if constexpr (ZP) {
+                            const float* zp = zc + ((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t;
+                            const float c0 = zp[0], c1 = zp[1];
+                            tot[nt][0] = fmaf(s_lo, acc[nt][0] - c0, tot[nt][0]);
+                            tot[nt][1] = fmaf(s_lo, acc[nt][1] - c1, tot[nt][1]);
+                            tot[nt][2] = fmaf(s_hi, acc[nt][2] - c0, tot[nt][2]);
+                            tot[nt][3] = fmaf(s_hi, acc[nt][3] - c1, tot[nt][3]);
+                        } else {
+                            tot[nt][0] = fmaf(s_lo, acc[nt][0], tot[nt][0]);
+                            tot[nt][1] = fmaf(s_lo, acc[nt][1], tot[nt][1]);
+                            tot[nt][2] = fmaf(s_hi, acc[nt][2], tot[nt][2]);
+                            tot[nt][3] = fmaf(s_hi, acc[nt][3], tot[nt][3]);
+                        }
+                    }
+                }
+            }
+        };
+        // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
+        // ticket, the last chunk to arrive summing the partials in chunk order
+        auto emit = [&](int rt, const float (&v)[NT][4]) {
+#ifdef MQ_STACK_EXP_NOEMIT
+            if (v[0][0] != 1234.5f) return;
+#endif
+            const int r0 = rt * kTileRows + g;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                        const float val = v[nt][2 * h + c] * L.out_scale;
+                        if (b < p.B && row < L.N) {
+                            if (L.S == 1) L.Y[(long long)b * L.ldy + row] = f32_to_bf16_rn(val);
+                            else p.ws[((long long)wp.kc * p.B + b) * L.Np + row] = val;
+                        }
+                    }
+            if (L.S == 1) return;
+            __syncwarp();
+            int last = 0;
+            // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
+            if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == L.S - 1);
+            last = __shfl_sync(0xffffffffu, last, 1);
+            if (!last) return;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                        if (b < p.B && row < L.N) {
+                            const float* wq = p.ws + (long long)b * L.Np + row;
+                            const long long cstride = (long long)p.B * L.Np;
+                            float sum = 0.0f;
+                            int q = 0;
+                            for (; q + 4 <= L.S; q += 4) {
+                                const float a0 = __ldcg(wq + q * cstride), a1 = __ldcg(wq + (q + 1) * cstride);
+                                const float a2 = __ldcg(wq + (q + 2) * cstride), a3 = __ldcg(wq + (q + 3) * cstride);
+                                sum += a0; sum += a1; sum += a2; sum += a3;
+                            }
+                            for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
+                            L.Y[(long long)b * L.ldy + row] = f32_to_bf16_rn(sum);
+                        }
+                    }
+            __syncwarp();
+            if (lane == 0) p.tickets[rt] = 0;
+        };
+        // A tile cut by warp boundaries (warps wa < ... < wb) is emitted by wa, the
+        // warp holding its first step: that is wa's LAST segment, so wa finishes it
+        // last.  wa+1..wb park their parts in their slot (only their FIRST segment
+        // can be such a part) and raise their flag; wa adds them in warp order.
+        float* slots = reinterpret_cast<float*>(smem + p.slot_off);
+        auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
+        const int first_lt = wp.ns > 0 ? wp.f0 / wp.ns : 0;
+        int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
+        const int f_end = ring_warp ? wp.f1 : wp.f0;
+#pragma unroll 1
+        for (int f = wp.f0; f < f_end; ++f) {
+            const int st = wp.chunk0 + si;
+            if (f == wp.f0 || si == 0) {
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
+            }
+            mbar_wait(my_bar0 + 8 * cstage, parity);
+            const uint32_t src = my_ring0 + cstage * kStageBytes;
+            float sc[4];
+            sc[0] = lds32f(src + g * 4);
+            sc[1] = lds32f(src + (g + 8) * 4);
+            sc[2] = lds32f(src + (16 + g) * 4);
+            sc[3] = lds32f(src + (24 + g) * 4);
+            uint4 buf[NPL];
+#pragma unroll
+            for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
+            __syncwarp();
+            if (lane == 0) {
+                fence_proxy_async_smem();
+                issue_next();
+            }
+            process(buf, sc, st);
+            if (++cstage == D) {
+                cstage = 0;
+                parity ^= 1u;
+            }
+            if (f + 1 == wp.f1) {
+                MQ_STS_WMAX(l, 5);  // this warp's last step decoded
+                MQ_STS_W0(l, 1);
+            }
+            if (f == wp.f0) MQ_STS_W0(l, 0);
+            const bool tile_end = si == wp.ns - 1;
+            if (tile_end || f + 1 == wp.f1) {
+                const bool starts_tile = wp.f0 <= lt * wp.ns;  // this segment holds the tile's first step
+                if (starts_tile && tile_end) {
+                    emit(wp.ta + lt, tot);
+                } else if (!starts_tile) {
+                    float* sp = slot_ptr(warp);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
+                    // hand the part to the emitter wa (holder of the tile's first step)
+                    // through named barrier wa + 1: bar.arrive orders the slot stores and
+                    // does not wait, and -- unlike a memory fence -- does not stall on
+                    // lane 0's in-flight ring bulk copies
+                    int wa = warp - 1;
+                    while (wa > 0 && plan_f0(wp, wa) > lt * wp.ns) --wa;
+                    int wb = wa + 1;
+                    while (wb + 1 < kStackWarps && plan_f0(wp, wb + 1) <= (lt + 1) * wp.ns - 1) ++wb;
+                    MQ_STS_W0(l, 2);
+                    named_bar_arrive(wa + 1, 32 * (wb - wa + 1));
+                } else {
+                    // emitter: own part, then warps warp+1 .. wb in warp order
+                    const int f_last = (lt + 1) * wp.ns - 1;
+                    int wb = warp + 1;
+                    while (wb + 1 < kStackWarps && plan_f0(wp, wb + 1) <= f_last) ++wb;
+                    MQ_STS_W0(l, 1);
+                    named_bar_sync(warp + 1, 32 * (wb - warp + 1));
+                    for (int w2 = warp + 1; w2 <= wb; ++w2) {
+                        const float* sp = slot_ptr(w2);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
+                    }
+                    MQ_STS_W0(l, 2);
+                    emit(wp.ta + lt, tot);
+                    MQ_STS_W0(l, 3);
+                }
+            }
+            if (++si == wp.ns) {
+                si = 0;
+                ++lt;
+            }
+        }
+        MQ_STS(l, 4);
+
+        // ---- publish layer l ------------------------------------------------
+        __syncthreads();
+        MQ_STS(l, 6);
+        // thread 1: thread 0 issues warp 0's bulk copies, and the release would wait
+        // for those in-flight loads
+        if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1u);
+        MQ_STS(l, 7);
+    }
+}
+
+template <int R>
+cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, size_t smem,
+                           cudaStream_t stream);
+
+}  // namespace mq

@@ -320,3 +320,47 @@ def algorithmic_bytes(N: int, K: int, B: int, r: int, planes_read: int, G: int =
                       x_bytes: int = 2, y_bytes: int = 2) -> int:
     """Bytes a GEMV must move: planes + fp32 scales + X + Y."""
     return N * K * planes_read // 8 + 4 * N * (-(-K // G)) + x_bytes * B * K + y_bytes * B * N
+
+
+class StackProgram:
+    """A whole decode step on the persistent K3S kernel (mq_stack_plan / mq_stack_run).
+
+    ``layers``: (PlaneTensor, X, Y) in dependency order -- X of layer i+1 is
+    (a column slice of) Y of layer i.  All layers share r; X / Y bf16 CUDA
+    tensors with unit column stride.  The host plan and the device layer table
+    are built once; ``run()`` is one asynchronous, graph-capturable launch.
+    """
+
+    def __init__(self, layers, r: int, B: int):
+        import ctypes
+
+        _lib.require_cuda()
+        L = _lib.lib()
+        n = len(layers)
+        arr = (_lib.StackLayer * n)()
+        nplanes = None
+        for i, (pt, X, Y) in enumerate(layers):
+            scale = pt._check(r)
+            if pt.G != 128:
+                raise ValueError("the stack kernel needs group size 128")
+            if nplanes is None:
+                nplanes = pt.nplanes
+            elif pt.nplanes != nplanes:
+                raise ValueError("mixed parent / child layers")
+            if X.dtype != torch.bfloat16 or Y.dtype != torch.bfloat16 or X.stride(1) != 1 or Y.stride(1) != 1:
+                raise ValueError("stack activations must be bf16 with unit column stride")
+            arr[i] = _lib.StackLayer(_lib.ptr(pt.blob), X.data_ptr(), Y.data_ptr(), X.stride(0), Y.stride(0),
+                                     pt.N, pt.K, scale)
+        self.plan = ctypes.create_string_buffer(L.mq_stack_plan_bytes())
+        table = ctypes.create_string_buffer(L.mq_stack_table_bytes(n))
+        ws = ctypes.c_size_t(0)
+        _lib.call("mq_stack_plan", ctypes.cast(arr, ctypes.c_void_p), n, B, r, nplanes, self.plan, table,
+                  ctypes.byref(ws))
+        self.table = torch.frombuffer(bytearray(table.raw), dtype=torch.uint8).cuda()
+        self.ws = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")
+        self._keep = layers  # the tensors the table points at
+        self.n_layers = n
+
+    def run(self, stream=None) -> None:
+        _lib.call("mq_stack_run", self.plan, _lib.ptr(self.table), _lib.ptr(self.ws), self.ws.numel(),
+                  _lib.stream_ptr(stream))

@@ -127,6 +127,7 @@ class LinearStack:
         need = max(pt.workspace_bytes(batch) for _, _, pt in self.layers)
         reserve_workspace(need, stream=self.stream)
         self.graph = None
+        self.program = None
         self.config: dict[str, int] = {}
 
     # ------------------------------------------------------------------
@@ -170,8 +171,34 @@ class LinearStack:
             if kind in ("o", "down"):
                 self._all_reduce(out)
 
-    def capture(self, config, pdl: bool = True) -> None:
-        """(Re)capture the decode step for a per-layer bit-width config."""
+    def _stack_layers(self):
+        """(PlaneTensor, X, Y) per layer in order, the same dataflow as _run."""
+        b, x = self.bufs, self.x
+        out = []
+        for name, kind, pt in self.layers:
+            if kind in ("qkv", "q", "k", "v"):
+                X = x
+            elif kind == "o":
+                X = b["qkv"][:, :pt.K] if self.fused else b["q"]
+            elif kind in ("gate_up", "gate", "up"):
+                X = b["o"]
+            else:
+                X = b["gate_up"][:, :pt.K] if self.fused else b["gate"]
+            out.append((pt, X, x if kind == "down" else b[kind]))
+        return out
+
+    def stack_kernel_ok(self, config) -> bool:
+        """The persistent K3S path serves uniform-r, single-GPU stacks with B <= 16
+        whose layers read only the previous layer's output (the fused stack)."""
+        rs = set(config.values()) if isinstance(config, dict) else {int(config)}
+        return (len(rs) == 1 and self.tp == 1 and self.B <= 16 and self.fused and self.G == 128)
+
+    def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None) -> None:
+        """(Re)capture the decode step for a per-layer bit-width config.
+
+        Uniform configs run as ONE persistent K3S launch per step (weights keep
+        streaming across layer boundaries); heterogeneous configs, TP and B > 16
+        run as a CUDA graph of per-layer K3 launches with PDL."""
         if isinstance(config, int):
             config = {n: config for n in self.names}
         missing = [n for n in self.names if n not in config]
@@ -181,16 +208,25 @@ class LinearStack:
             if r not in LADDER:
                 raise ValueError("bit-width %d not on the ladder" % r)
         self.config = dict(config)
+        use_stack = self.stack_kernel_ok(self.config) if stack_kernel is None else stack_kernel
+        self.program = None
+        if use_stack:
+            from .device import StackProgram
+
+            self.program = StackProgram(self._stack_layers(), next(iter(self.config.values())), self.B)
+            run = lambda: self.program.run(self.stream)  # noqa: E731
+        else:
+            run = lambda: self._run(self.config, pdl)  # noqa: E731
         with torch.cuda.stream(self.stream):
-            self._run(self.config, pdl)  # warm the launch path outside capture
+            run()  # warm the launch path outside capture
         self.stream.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=self.stream):
-            self._run(self.config, pdl)
+            run()
         self.graph = g
 
     def launches_per_step(self) -> int:
-        return len(self.layers)
+        return 1 if getattr(self, "program", None) is not None else len(self.layers)
 
     def step(self) -> None:
         """Replay one captured decode step (device-resident activations)."""

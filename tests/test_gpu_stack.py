@@ -1,0 +1,87 @@
+"""K3S (one persistent kernel per decode step): every layer's output against
+an fp32 torch product of the exactly decoded weights and the activations the
+layer actually read (the bf16 tolerance of SURVEY 8(c)); bitwise replay
+determinism (the completion counters only grow); agreement with the
+per-layer K3 graph; mode C."""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+LADDER = (2, 3, 4, 6, 8)
+
+
+@pytest.fixture(scope="module")
+def model():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.backends.cuda.matmul.allow_tf32 = False
+    from paper_2602_03537_b200 import model as m
+
+    return m
+
+
+def _step(stack, x0):
+    stack.x.copy_(x0)
+    stack.step()
+    torch.cuda.synchronize()
+    return stack.x.clone(), {k: v.clone() for k, v in stack.bufs.items()}
+
+
+def _check_layers(stack, r, x0, y, bufs, tol=1e-2):
+    qkv, o, gu, down = (pt for _, _, pt in stack.layers[:4])
+    ins = {"qkv": x0, "o": bufs["qkv"][:, :o.K], "gate_up": bufs["o"], "down": bufs["gate_up"][:, :down.K]}
+    outs = {"qkv": bufs["qkv"], "o": bufs["o"], "gate_up": bufs["gate_up"], "down": y}
+    for kind, pt in zip(("qkv", "o", "gate_up", "down"), (qkv, o, gu, down)):
+        want = ins[kind].float() @ pt.decode(r).T
+        got = outs[kind].float()
+        assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= tol, (kind, r)
+
+
+@pytest.mark.parametrize("B", [1, 5, 16])
+def test_stack_kernel_layers_vs_fp32(model, B):
+    stack = model.LinearStack(model.LLAMA31_8B, batch=B, n_layers=1)
+    g = torch.Generator(device="cuda").manual_seed(B)
+    x0 = torch.randn(B, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    for r in LADDER:
+        stack.capture(r, stack_kernel=True)
+        assert stack.launches_per_step() == 1
+        y, bufs = _step(stack, x0)
+        if torch.isfinite(y.float()).all():
+            _check_layers(stack, r, x0, y, bufs)
+        for _ in range(2):  # replays: counters keep growing, results are bitwise stable
+            y2, b2 = _step(stack, x0)
+            torch.testing.assert_close(y2, y, rtol=0, atol=0, equal_nan=True)
+            for k in bufs:
+                torch.testing.assert_close(b2[k], bufs[k], rtol=0, atol=0, equal_nan=True)
+        # the per-layer K3 graph computes the same first layer (other reduction order)
+        stack.capture(r, stack_kernel=False)
+        _, wb = _step(stack, x0)
+        assert rel_err(wb["qkv"].float().cpu().numpy(), bufs["qkv"].float().cpu().numpy()) <= 1e-2
+
+
+def test_stack_kernel_two_blocks_and_children(model):
+    stack = model.LinearStack(model.LLAMA31_8B, batch=3, n_layers=2)
+    x0 = torch.randn(3, 4096, device="cuda").to(torch.bfloat16)
+    stack.capture(4, stack_kernel=True)
+    want, _ = _step(stack, x0)
+    assert torch.isfinite(want.float()).all()
+    saved = list(stack.layers)
+    stack.layers = [(n, k, pt.materialize_child(4)) for n, k, pt in saved]
+    stack.capture(4, stack_kernel=True)
+    got, _ = _step(stack, x0)
+    assert torch.equal(got, want)  # mode C decodes the same codes in the same order
+    stack.layers = saved
+
+
+def test_uniform_configs_default_to_stack_kernel(model):
+    stack = model.LinearStack(model.LLAMA31_8B, batch=2, n_layers=1)
+    stack.capture(3)
+    assert stack.program is not None
+    cfg = {n: (2 if i % 2 else 4) for i, n in enumerate(stack.names)}
+    stack.capture(cfg)
+    assert stack.program is None and stack.launches_per_step() == len(stack.names)
