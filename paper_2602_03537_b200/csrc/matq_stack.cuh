@@ -196,8 +196,13 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
             }
         }
     };
+    int cur_layer = 0;  // consumer's layer (experiments: cap the cross-layer prefetch)
+    int pending = 0;    // issues skipped while capped
     auto issue_next = [&]() {  // lane 0; no-op once the warp has nothing left
         if (il >= p.n_layers) return;
+#ifdef MQ_STACK_EXP_NOXLAYER
+        if (il > cur_layer) { ++pending; return; }
+#endif
         const uint32_t* src = iblob + ((long long)itile * insteps + ip.chunk0 + isi) * isw;
         if (++isi == ip.ns) {
             isi = 0;
@@ -311,6 +316,15 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
             }
         }
         MQ_STS(l, 3);
+#ifdef MQ_STACK_EXP_NOXLAYER
+        cur_layer = l;
+        if (ring_warp && lane == 0) {
+            const int n = pending;
+            pending = 0;
+            for (int i = 0; i < n; ++i) issue_next();
+        }
+        __syncwarp();
+#endif
 
         // ---- this warp's units of layer l --------------------------------------
         float tot[NT][4], acc[NT][4];
