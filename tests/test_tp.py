@@ -105,3 +105,57 @@ def test_even_split_edges():
     assert _even_split(5, 8, 7) == (5, 5)  # more ranks than units: empty shard
     with pytest.raises(ValueError):
         shard_plan("o", 16, 256, 2, 2)
+
+
+def _gpu_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)  # one GPU: both ranks share it; gloo carries the collective
+        from paper_2602_03537_b200.device import PlaneTensor
+        from paper_2602_03537_b200.tp import TPLinear
+
+        for i, (kind, N, K, G, B) in enumerate(CASES[:4]):
+            if G != 128:
+                continue
+            codes, scales, X = _case(N, K, G, B, seed=10 + i)
+            lin = TPLinear(codes, scales, kind, world, rank, G)
+            Xd = torch.from_numpy(X).cuda().to(torch.bfloat16)
+            for r in (2, 4, 8):
+                y = lin(Xd, r, out=torch.empty((B, lin.planes.N), device="cuda", dtype=torch.float32))
+                y = y.cpu()
+                if lin.plan.parallel == "column":
+                    outs = [None] * world
+                    dist.all_gather_object(outs, y.numpy())
+                    y = np.concatenate(outs, axis=1)
+                else:
+                    y = y.numpy()
+                full = PlaneTensor.from_codes(codes, 8, scales, G).gemv(Xd, r, out_dtype=torch.float32)
+                if rank == 0:
+                    q.put((kind, r, rel_err(y, full.cpu().numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_tplinear_two_ranks_on_device():
+    """TPLinear end to end on the device: two ranks (sharing cuda:0), real K3
+    shards, the row-parallel all-reduce through the collective; equals the
+    unsharded GEMV up to fp32 summation order."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    n = 0
+    while not q.empty():
+        kind, r, err = q.get()
+        assert err <= 1e-5, (kind, r, err)
+        n += 1
+    assert n >= 6
