@@ -73,9 +73,11 @@ int env_int(const char* name, int dflt) {
 GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
                               bool honour_overrides = true, int force_warps = 0) {
     GemvConfig c{};
-    const int ncopy = (g128 && r != 8) ? mq::zp_ncopies(r) : 1;
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     c.NT = Bx <= 8 ? 1 : (Bx <= 16 ? 2 : 4);
+    const int ncopy = (g128 && r != 8 && c.NT == 1) ? mq::zp_ncopies(r) : 1;  // k_gemv's ZP rule
+    // staging budget: fewer warps' rings at NT = 4 leave room for longer K chunks
+    const size_t xs_max = c.NT >= 4 ? 96 * 1024 : (c.NT == 2 ? 64 * 1024 : kXsMax);
     // tuning overrides (scripts/sweep_gemv.py): MQ_GEMV_WARPS, MQ_GEMV_SPLIT, MQ_GEMV_STAGES,
     // MQ_GEMV_STREAM (0 = never, 1 = force when it fits)
     c.nwarps = force_warps ? force_warps
@@ -94,7 +96,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
         const int S = mq::cdiv(nsteps, cs);
         if (S != S_try && !force_s) continue;
         const size_t xs = (size_t)ncopy * Bx * (cs * 256 + 8) * 2;
-        if (xs > kXsMax && cs > 1) continue;
+        if (xs > xs_max && cs > 1) continue;
         int cpc = sms / S;
         if (cpc < 1) break;
         cpc = std::min(cpc, n_rt);  // at least one row tile per CTA
@@ -120,7 +122,7 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
     c.cs_off = (int)(((size_t)ncopy * c.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const size_t zc_bytes = (g128 && r != 8) ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
+    const size_t zc_bytes = ncopy > 1 ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
     c.xs_bytes = (int)((c.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
     const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
@@ -480,8 +482,8 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     memset(P, 0, sizeof(*P));
     const bool child = nplanes == r;
     const int npl = (child || r == 8) ? r : r + 1;
-    const int ncopy = r != 8 ? mq::zp_ncopies(r) : 1;
     const int nt = B <= 8 ? 1 : 2;
+    const int ncopy = (r != 8 && nt == 1) ? mq::zp_ncopies(r) : 1;  // k_stack's ZP rule
     int cs_max = 1;
     size_t partials = 0;
     for (int i = 0; i < n_layers; ++i) {
@@ -518,7 +520,7 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     p.xs_stride = cs_max * 256 + 8;
     p.xcopy_stride = B * p.xs_stride;
     p.cs_off = (int)(((size_t)ncopy * p.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const size_t zc_bytes = r != 8 ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
+    const size_t zc_bytes = ncopy > 1 ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
     p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
@@ -557,7 +559,7 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
     p.ws = reinterpret_cast<float*>(w + op);
 #ifdef MQ_GEMV_TIMING
     static unsigned long long* sbuf = nullptr;
-    if (!sbuf) cudaMalloc(&sbuf, sizeof(unsigned long long) * (256 * 148 * 8 + 256 * 16 * 4));
+    if (!sbuf) cudaMalloc(&sbuf, sizeof(unsigned long long) * (256 * 148 * 8 + 256 * 16 * 4) + 65536);
     p.dbg_ts = sbuf;
     g_stack_dbg = sbuf;
 #endif

@@ -88,7 +88,10 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
     constexpr uint32_t kScaleBytes = GS == 128 ? 128 : 0;   // 2 groups x 16 rows, head of block
     constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
     // zero-point folding (zp_off<R>, matq_common.cuh): raw magic-encoded A + scaled activation copies
-    constexpr bool ZP = (GS == 128) && (R != 8) && !(MQ_GEMV_DEBUG & 1);
+    // zero-point folding only for NT == 1 (B <= 8): its scaled activation copies
+    // multiply the staging by 2-3x, which at larger B forces tiny K chunks and
+    // heavy split-K; there the exact HFMA2 decode (idle FMA pipe) is cheaper
+    constexpr bool ZP = (GS == 128) && (R != 8) && (NT == 1) && !(MQ_GEMV_DEBUG & 1);
     constexpr int NCOPY = ZP ? zp_ncopies(R) : 1;
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);

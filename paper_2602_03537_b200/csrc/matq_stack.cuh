@@ -111,6 +111,15 @@ __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
 __device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Explicit global stores: Y's pointer comes from the shared-memory layer table,
+// so a plain store would be GENERIC -- and a generic store is ordered behind the
+// warp's in-flight bulk copies into shared memory (~HBM latency).
+__device__ __forceinline__ void st_global_u16(uint16_t* p, uint16_t v) {
+    asm volatile("st.global.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+__device__ __forceinline__ void st_global_f32(float* p, float v) {
+    asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
 __device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
     asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -136,7 +145,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512, kScaleBytes = 128;
     constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
-    constexpr bool ZP = R != 8;
+    constexpr bool ZP = (R != 8) && (NT == 1);  // see k_gemv
     constexpr int NCOPY = ZP ? zp_ncopies(R) : 1;
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
@@ -396,8 +405,12 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                         const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
                         const float val = v[nt][2 * h + c] * L.out_scale;
                         if (b < p.B && row < L.N) {
-                            if (L.S == 1) L.Y[(long long)b * L.ldy + row] = f32_to_bf16_rn(val);
-                            else p.ws[((long long)wp.kc * p.B + b) * L.Np + row] = val;
+#ifdef MQ_STACK_EXP_DUMMYY
+                            if (L.S == 1) st_global_u16(reinterpret_cast<uint16_t*>(p.dbg_ts + 256 * 148 * 8 + 256 * 16 * 4) + ((blockIdx.x * 32 + lane) & 4095), f32_to_bf16_rn(val));
+#else
+                            if (L.S == 1) st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(val));
+#endif
+                            else st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
                         }
                     }
             if (L.S == 1) return;
@@ -425,7 +438,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                                 sum += a0; sum += a1; sum += a2; sum += a3;
                             }
                             for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
-                            L.Y[(long long)b * L.ldy + row] = f32_to_bf16_rn(sum);
+                            st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(sum));
                         }
                     }
             __syncwarp();
@@ -509,6 +522,13 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
 #pragma unroll
                             for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
                     }
+#ifdef MQ_GEMV_TIMING
+                    {   // stamp when the accumulators are actually available
+                        float dep = tot[0][0] + tot[0][3];
+                        asm volatile("mov.b32 %0, %0;" : "+f"(dep));
+                        if (dep == 1.2345e30f) tot[0][1] = dep;
+                    }
+#endif
                     MQ_STS_W0(l, 2);
                     emit(wp.ta + lt, tot);
                     MQ_STS_W0(l, 3);

@@ -22,8 +22,10 @@ from . import _lib
 
 LADDER = (2, 3, 4, 6, 8)
 MAX_GEMV_ROWS = 32
-# K3 serves B <= GEMV_MAX_ROWS; K4 (tcgen05) serves larger bf16 batches.
-GEMV_MAX_ROWS = 32
+# linear(): K3 serves bf16 batches up to GEMV_DISPATCH_ROWS (measured crossover,
+# profiles/r1_bench_batches.txt: at B = 32 K4 beats K3's NT = 4 tile), K4 (tcgen05)
+# serves larger bf16 batches; gemv() itself accepts up to MAX_GEMV_ROWS.
+GEMV_DISPATCH_ROWS = 16
 
 
 def _as_device_u8(codes) -> torch.Tensor:
@@ -294,13 +296,13 @@ class PlaneTensor:
 
     def linear(self, X: torch.Tensor, r: int, out: torch.Tensor | None = None,
                out_dtype: torch.dtype | None = None, pdl: bool = False, stream=None) -> torch.Tensor:
-        """Dispatch by batch: K3 (GEMV) up to GEMV_MAX_ROWS rows, K4 (tcgen05 GEMM) above.
+        """Dispatch by batch: K3 (GEMV) up to GEMV_DISPATCH_ROWS rows, K4 (tcgen05 GEMM) above.
 
         fp32 activations or G != 128 stay on K3 (in 32/16-row chunks), which keeps
         the reference API's 1e-4 agreement (hi + lo bf16 split of fp32 X).
         """
         B = X.shape[0]
-        if B <= GEMV_MAX_ROWS and not (X.dtype == torch.float32 and B > 16):
+        if B <= GEMV_DISPATCH_ROWS or (X.dtype == torch.float32 and B <= 16):
             return self.gemv(X, r, out=out, out_dtype=out_dtype, pdl=pdl, stream=stream)
         if X.dtype == torch.bfloat16 and self.G == 128:
             return self.gemm(X, r, out=out, out_dtype=out_dtype, pdl=pdl, stream=stream)
