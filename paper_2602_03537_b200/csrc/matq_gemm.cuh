@@ -6,20 +6,22 @@
 // (packed_kernels.c:177-210, driven in chunks of 16 rows by
 // kernels/_core.pyx:53-63).
 //
-// Persistent CTAs (one per SM, 16 warps).  Work unit = (output tile of 128
+// Persistent CTAs (one per SM, 23 warps).  Work unit = (output tile of 128
 // weight rows x BN tokens, K split).  Pipelines:
 //   raw ring    warp 2 (one lane) bulk-copies, per 256-column step, the eight
 //               16-row P8 blocks of the tile ([group scales][r+1 plane slabs],
-//               each contiguous) into shared memory (TMA, mbarrier complete_tx)
+//               each contiguous) into shared memory (TMA, mbarrier complete_tx);
+//               it does not wait on the previous kernel (weights are static)
 //   operand     per 64-column stage: A = 128 x 64 bf16 weights, B = BN x 64
 //   stages      bf16 activations, both K-major SWIZZLE_128B; warp 0 (one lane)
-//               TMA-loads B from a tensor map (zero fill past B and K), warps
-//               8-15 (one 16-row tile each) slice + decode the raw block
-//               bitsliced as K3 does, scale (bf16x2) and stmatrix A
+//               TMA-loads B from a tensor map (zero fill past B and K) after the
+//               programmatic-dependency wait; warps 7-22 decode (one 16-row
+//               block x one word pair each): slice + decode bitsliced as K3 does,
+//               scale (bf16x2) and stmatrix A
 //   MMA         warp 1 (one lane): 4 x tcgen05.mma.kind::f16 (M=128, N=BN,
 //               K=16) per stage into a double-buffered fp32 TMEM accumulator;
 //               tcgen05.commit frees the operand stage / publishes the tile
-//   epilogue    warps 4-7: tcgen05.ld 32 lanes x 32 columns -> Y (S = 1), or
+//   epilogue    warps 3-6: tcgen05.ld 32 lanes x 32 columns -> Y (S = 1), or
 //               fp32 partials + an acq_rel ticket; the last split of a tile sums
 //               the partials in split order (deterministic) and writes Y.
 // The dequantised weight is rounded to bf16 once (scale * (s - z)); products
@@ -47,11 +49,15 @@ struct GemmParams {
     int y_f32;
 };
 
-constexpr int kGemmThreads = 512;
+constexpr int kGemmThreads = 23 * 32;
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;  // K columns per operand stage (one swizzle atom)
 constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KB
-constexpr int kDecWarp0 = 8, kNumDecWarps = 8, kEpiWarp0 = 4, kWarpX = 0, kWarpMma = 1, kWarpW = 2;
+// warp 0: activation-tile producer, warp 1: TMEM + MMA, warp 2: raw-weight producer,
+// warps 3..6: epilogue (any 4 consecutive warps cover the 4 TMEM lane quadrants),
+// warps 7..22: decoders (row tile dw & 7, word pair dw >> 3)
+constexpr int kEpiWarp0 = 3, kDecWarp0 = 7, kNumDecWarps = 16, kWarpProd = 0, kWarpMma = 1, kWarpW = 2;
+constexpr int kRowTiles = kGemmBM / 16;  // raw blocks per step (8)
 constexpr uint32_t kSmemBudget = 227 * 1024;
 
 __host__ __device__ constexpr uint32_t gemm_raw_block_bytes(int npl) { return 128u + 512u * (uint32_t)npl; }
@@ -60,7 +66,7 @@ template <int BN, int NPL>
 struct GemmSmem {
     static constexpr uint32_t kBBytes = (uint32_t)BN * kGemmBK * 2;
     static constexpr uint32_t kOpBytes = kGemmABytes + kBBytes;
-    static constexpr uint32_t kRawBytes = kNumDecWarps * gemm_raw_block_bytes(NPL);
+    static constexpr uint32_t kRawBytes = kRowTiles * gemm_raw_block_bytes(NPL);
     static constexpr uint32_t kFixed = 1024 + 512;  // alignment slack + barriers
     static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget) ? 3 : 2;
     static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 4 : 3;
@@ -100,7 +106,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < NS; ++s) {
-            mbar_init(op_full(s), 1 + kNumDecWarps);
+            mbar_init(op_full(s), 1 + kRowTiles);  // the X tile + one decoder per row tile
             mbar_init(op_empty(s), 1);
         }
         for (int s = 0; s < RS; ++s) {
@@ -132,8 +138,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         nst = max(0, min(p.nsteps, st0 + p.cs) - st0);
     };
 
-    if (warp == kWarpX) {
-        // ---------------- TMA producer: activations -------------------------
+    // flattened (unit, step) sequence of this CTA
+    int total_steps = 0;
+    for (int ui = 0; ui < my_units; ++ui) {
+        int tile, split, st0, nst;
+        unit_of(ui, tile, split, st0, nst);
+        total_steps += nst;
+    }
+
+    if (warp == kWarpProd) {
+        // ---------------- producer: activation tiles ----------------------------
         if (lane == 0) {
             pdl_wait();  // X is written by the previous kernel
             int ks = 0;
@@ -141,31 +155,36 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 int tile, split, st0, nst;
                 unit_of(ui, tile, split, st0, nst);
                 const int bt = tile % p.n_bt;
-                for (int kk = 0; kk < 4 * nst; ++kk, ++ks) {
-                    const int s = ks % NS;
-                    mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
-                    mbar_expect_tx(op_full(s), SM::kBBytes);
-                    tma_load_2d(b_st(s), &tmx, st0 * 256 + kk * kGemmBK, bt * BN, op_full(s));
+                for (int si = 0; si < nst; ++si) {
+                    for (int kk = 0; kk < 4; ++kk, ++ks) {
+                        const int s = ks % NS;
+                        mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                        mbar_expect_tx(op_full(s), SM::kBBytes);
+                        tma_load_2d(b_st(s), &tmx, (st0 + si) * 256 + kk * kGemmBK, bt * BN, op_full(s));
+                    }
                 }
             }
         }
     } else if (warp == kWarpW) {
-        // ---------------- TMA producer: raw weight blocks ---------------------
+        // ---------------- producer: raw weight blocks (independent of X: no PDL wait) --
         if (lane == 0) {
-            int rs_i = 0;
-            for (int ui = 0; ui < my_units; ++ui) {
+            int r_ui = 0, r_si = 0;
+            for (int r_f = 0; r_f < total_steps; ++r_f) {
                 int tile, split, st0, nst;
-                unit_of(ui, tile, split, st0, nst);
-                const int rt0 = (tile / p.n_bt) * (kGemmBM / 16);
-                const int nvalid = min(kNumDecWarps, p.n_rt - rt0);
-                for (int st = st0; st < st0 + nst; ++st, ++rs_i) {
-                    const int s = rs_i % RS;
-                    mbar_wait(raw_empty(s), ((rs_i / RS) & 1) ^ 1);
-                    mbar_expect_tx(raw_full(s), (uint32_t)nvalid * kBlk);
-                    for (int d = 0; d < nvalid; ++d)
-                        bulk_g2s_nohint(raw_st(s) + (uint32_t)d * kBlk,
-                                        p.blob + ((long long)(rt0 + d) * p.nsteps + st) * p.step_words + p.skip_words,
-                                        kBlk, raw_full(s));
+                unit_of(r_ui, tile, split, st0, nst);
+                const int rt0 = (tile / p.n_bt) * kRowTiles;
+                const int nvalid = min(kRowTiles, p.n_rt - rt0);
+                const int s = r_f % RS;
+                mbar_wait(raw_empty(s), ((r_f / RS) & 1) ^ 1);
+                mbar_expect_tx(raw_full(s), (uint32_t)nvalid * kBlk);
+                const int st = st0 + r_si;
+                for (int d = 0; d < nvalid; ++d)
+                    bulk_g2s_nohint(raw_st(s) + (uint32_t)d * kBlk,
+                                    p.blob + ((long long)(rt0 + d) * p.nsteps + st) * p.step_words + p.skip_words,
+                                    kBlk, raw_full(s));
+                if (++r_si == nst) {
+                    r_si = 0;
+                    ++r_ui;
                 }
             }
         }
@@ -196,11 +215,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 umma_commit(tfull(buf));
             }
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        // ---------------- epilogue: TMEM -> Y / split-K partials ---------------
-        const int q = warp & 3;
-        const int et = threadIdx.x - 32 * kEpiWarp0;  // 0..127 = TMEM lane = tile row
-        for (int ui = 0; ui < my_units; ++ui) {
+    } else if (warp >= kEpiWarp0) {
+        // ---------------- epilogue: TMEM -> Y / split-K partials ---------------------
+        auto epilogue = [&](int ui) {
+            const int q = warp & 3;                  // TMEM lane quadrant of this warp
+            const int et = 32 * q + lane;            // 0..127 = TMEM lane = tile row
             int tile, split, st0, nst;
             unit_of(ui, tile, split, st0, nst);
             const int mt = tile / p.n_bt, bt = tile % p.n_bt;
@@ -268,50 +287,50 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 named_bar_sync(1, 128);  // flag slot reuse
             }
-        }
-    } else if (warp >= kDecWarp0) {
-        // ---------------- decode producers: raw blocks -> bf16 A operand --------
+        };
+        if (warp < kDecWarp0) {
+            for (int ui = 0; ui < my_units; ++ui) epilogue(ui);
+        } else {
+        // ---------------- decoders: raw blocks -> bf16 A operand -----------------
         const int dw = warp - kDecWarp0;
+        const int rtl = dw & (kRowTiles - 1), half = dw >> 3;  // row tile, word pair
         const int g = lane >> 2;
         // stmatrix row address: matrix j = lane >> 3 holds rows +8 (j & 1), columns +8 (j >> 1)
         const int jm = lane >> 3;
-        const uint32_t row_off = (uint32_t)(16 * dw + (lane & 7) + 8 * (jm & 1)) * 128u;
+        const uint32_t row_off = (uint32_t)(16 * rtl + (lane & 7) + 8 * (jm & 1)) * 128u;
         const uint32_t swz = (uint32_t)(lane & 7);
-        int ks = 0, rs_i = 0;
+        int fglob = 0;
         for (int ui = 0; ui < my_units; ++ui) {
             int tile, split, st0, nst;
             unit_of(ui, tile, split, st0, nst);
-            const bool valid = (tile / p.n_bt) * (kGemmBM / 16) + dw < p.n_rt;
+            const bool valid = (tile / p.n_bt) * kRowTiles + rtl < p.n_rt;
 #pragma unroll 1
-            for (int f = 0; f < nst; ++f, ++rs_i) {
-                const int rsl = rs_i % RS;
-                mbar_wait(raw_full(rsl), (rs_i / RS) & 1);
-                uint4 raw[NPL];
-                float sc[4];
-                const uint32_t blk = raw_st(rsl) + (uint32_t)dw * kBlk;
+            for (int f = 0; f < nst; ++f, ++fglob) {
+                const int rsl = fglob % RS;
+                mbar_wait(raw_full(rsl), (fglob / RS) & 1);
+                uint2 raw[NPL];  // the two words (of four) of this decoder's word pair
+                float sc[2];
+                const uint32_t blk = raw_st(rsl) + (uint32_t)rtl * kBlk;
                 if (valid) {
-                    sc[0] = lds32f(blk + 4u * g);
-                    sc[1] = lds32f(blk + 4u * (g + 8));
-                    sc[2] = lds32f(blk + 4u * (16 + g));
-                    sc[3] = lds32f(blk + 4u * (24 + g));
+                    sc[0] = lds32f(blk + 4u * (16 * half + g));
+                    sc[1] = lds32f(blk + 4u * (16 * half + g + 8));
 #pragma unroll
-                    for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds128(blk + 128u + 512u * jj + 16u * lane);
+                    for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds64(blk + 128u + 512u * jj + 16u * lane + 8u * half);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(raw_empty(rsl));
-                // one operand stage per word: a proxy fence per stage keeps the
-                // decoders one stage behind the MMA at most (batching two words
-                // per fence measured slower: it needs two free stages at once)
+                const uint32_t s_lo = valid ? bf16x2_splat(sc[0] * p.out_scale) : 0u;
+                const uint32_t s_hi = valid ? bf16x2_splat(sc[1] * p.out_scale) : 0u;
 #pragma unroll
-                for (int w = 0; w < 4; ++w, ++ks) {
+                for (int wi = 0; wi < 2; ++wi) {
+                    const int w = 2 * half + wi;
+                    const int ks = 4 * fglob + w;
                     const int s = ks % NS;
                     mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
                     if (valid) {
-                        const uint32_t s_lo = bf16x2_splat(sc[(w >> 1) * 2] * p.out_scale);
-                        const uint32_t s_hi = bf16x2_splat(sc[(w >> 1) * 2 + 1] * p.out_scale);
                         uint32_t T[NPL];
 #pragma unroll
-                        for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(raw[jj], w);
+                        for (int jj = 0; jj < NPL; ++jj) T[jj] = wi ? raw[jj].y : raw[jj].x;
                         uint32_t Sl[R];
                         slice_loaded<R, CHILD>(T, Sl);
                         uint32_t A[16];
@@ -331,6 +350,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     if (lane == 0) mbar_arrive(op_full(s));
                 }
             }
+        }
         }
     }
 

@@ -131,6 +131,11 @@ __device__ __forceinline__ void stmatrix_x4(uint32_t saddr, uint32_t r0, uint32_
                  "r"(r1), "r"(r2), "r"(r3)
                  : "memory");
 }
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ uint32_t hmul2_bf16(uint32_t a, uint32_t b) {
     uint32_t d;
     asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
