@@ -291,66 +291,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (warp < kDecWarp0) {
             for (int ui = 0; ui < my_units; ++ui) epilogue(ui);
         } else {
-        // ---------------- decoders: raw blocks -> bf16 A operand -----------------
-        const int dw = warp - kDecWarp0;
-        const int rtl = dw & (kRowTiles - 1), half = dw >> 3;  // row tile, word pair
-        const int g = lane >> 2;
-        // stmatrix row address: matrix j = lane >> 3 holds rows +8 (j & 1), columns +8 (j >> 1)
-        const int jm = lane >> 3;
-        const uint32_t row_off = (uint32_t)(16 * rtl + (lane & 7) + 8 * (jm & 1)) * 128u;
-        const uint32_t swz = (uint32_t)(lane & 7);
-        int fglob = 0;
-        for (int ui = 0; ui < my_units; ++ui) {
-            int tile, split, st0, nst;
-            unit_of(ui, tile, split, st0, nst);
-            const bool valid = (tile / p.n_bt) * kRowTiles + rtl < p.n_rt;
+            // ---------------- decoders: raw blocks -> bf16 A operand -----------------
+            const int dw = warp - kDecWarp0;
+            const int rtl = dw & (kRowTiles - 1), half = dw >> 3;  // row tile, word pair
+            const int g = lane >> 2;
+            // stmatrix row address: matrix j = lane >> 3 holds rows +8 (j & 1), columns +8 (j >> 1)
+            const int jm = lane >> 3;
+            const uint32_t row_off = (uint32_t)(16 * rtl + (lane & 7) + 8 * (jm & 1)) * 128u;
+            const uint32_t swz = (uint32_t)(lane & 7);
+            int fglob = 0;
+            for (int ui = 0; ui < my_units; ++ui) {
+                int tile, split, st0, nst;
+                unit_of(ui, tile, split, st0, nst);
+                const bool valid = (tile / p.n_bt) * kRowTiles + rtl < p.n_rt;
 #pragma unroll 1
-            for (int f = 0; f < nst; ++f, ++fglob) {
-                const int rsl = fglob % RS;
-                mbar_wait(raw_full(rsl), (fglob / RS) & 1);
-                uint2 raw[NPL];  // the two words (of four) of this decoder's word pair
-                float sc[2];
-                const uint32_t blk = raw_st(rsl) + (uint32_t)rtl * kBlk;
-                if (valid) {
-                    sc[0] = lds32f(blk + 4u * (16 * half + g));
-                    sc[1] = lds32f(blk + 4u * (16 * half + g + 8));
-#pragma unroll
-                    for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds64(blk + 128u + 512u * jj + 16u * lane + 8u * half);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(raw_empty(rsl));
-                const uint32_t s_lo = valid ? bf16x2_splat(sc[0] * p.out_scale) : 0u;
-                const uint32_t s_hi = valid ? bf16x2_splat(sc[1] * p.out_scale) : 0u;
-#pragma unroll
-                for (int wi = 0; wi < 2; ++wi) {
-                    const int w = 2 * half + wi;
-                    const int ks = 4 * fglob + w;
-                    const int s = ks % NS;
-                    mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                for (int f = 0; f < nst; ++f, ++fglob) {
+                    const int rsl = fglob % RS;
+                    mbar_wait(raw_full(rsl), (fglob / RS) & 1);
+                    uint2 raw[NPL];  // the two words (of four) of this decoder's word pair
+                    float sc[2];
+                    const uint32_t blk = raw_st(rsl) + (uint32_t)rtl * kBlk;
                     if (valid) {
-                        uint32_t T[NPL];
+                        sc[0] = lds32f(blk + 4u * (16 * half + g));
+                        sc[1] = lds32f(blk + 4u * (16 * half + g + 8));
 #pragma unroll
-                        for (int jj = 0; jj < NPL; ++jj) T[jj] = wi ? raw[jj].y : raw[jj].x;
-                        uint32_t Sl[R];
-                        slice_loaded<R, CHILD>(T, Sl);
-                        uint32_t A[16];
-                        decode_word<R, false>(Sl, A);
-#pragma unroll
-                        for (int qq = 0; qq < 16; ++qq) A[qq] = hmul2_bf16(A[qq], (qq & 1) ? s_hi : s_lo);
-                        const uint32_t abase = a_st(s) + row_off;
-#pragma unroll
-                        for (int k16 = 0; k16 < 4; ++k16) {
-                            const uint32_t chunk = (uint32_t)(2 * k16 + (jm >> 1));
-                            stmatrix_x4(abase + ((chunk ^ swz) << 4), A[4 * k16], A[4 * k16 + 1],
-                                        A[4 * k16 + 2], A[4 * k16 + 3]);
-                        }
-                        fence_proxy_async_smem();
+                        for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds64(blk + 128u + 512u * jj + 16u * lane + 8u * half);
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(op_full(s));
+                    if (lane == 0) mbar_arrive(raw_empty(rsl));
+                    const uint32_t s_lo = valid ? bf16x2_splat(sc[0] * p.out_scale) : 0u;
+                    const uint32_t s_hi = valid ? bf16x2_splat(sc[1] * p.out_scale) : 0u;
+#pragma unroll
+                    for (int wi = 0; wi < 2; ++wi) {
+                        const int w = 2 * half + wi;
+                        const int ks = 4 * fglob + w;
+                        const int s = ks % NS;
+                        mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                        if (valid) {
+                            uint32_t T[NPL];
+#pragma unroll
+                            for (int jj = 0; jj < NPL; ++jj) T[jj] = wi ? raw[jj].y : raw[jj].x;
+                            uint32_t Sl[R];
+                            slice_loaded<R, CHILD>(T, Sl);
+                            uint32_t A[16];
+                            decode_word<R, false>(Sl, A);
+#pragma unroll
+                            for (int qq = 0; qq < 16; ++qq) A[qq] = hmul2_bf16(A[qq], (qq & 1) ? s_hi : s_lo);
+                            const uint32_t abase = a_st(s) + row_off;
+#pragma unroll
+                            for (int k16 = 0; k16 < 4; ++k16) {
+                                const uint32_t chunk = (uint32_t)(2 * k16 + (jm >> 1));
+                                stmatrix_x4(abase + ((chunk ^ swz) << 4), A[4 * k16], A[4 * k16 + 1],
+                                            A[4 * k16 + 2], A[4 * k16 + 3]);
+                            }
+                            fence_proxy_async_smem();
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(op_full(s));
+                    }
                 }
             }
-        }
         }
     }
 
