@@ -122,7 +122,10 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     c.xs_stride = c.cs * 256 + 8;
     c.xcopy_stride = Bx * c.xs_stride;
     c.cs_off = (int)(((size_t)ncopy * c.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const size_t zc_bytes = ncopy > 1 ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
+    // zero-point constants whenever k_gemv folds the zero point (its ZP rule; r = 6
+    // folds with a single activation copy, so this is not ncopy > 1)
+    const bool zp = g128 && r != 8 && c.NT == 1;
+    const size_t zc_bytes = zp ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
     c.xs_bytes = (int)((c.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
     const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
@@ -520,7 +523,8 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     p.xs_stride = cs_max * 256 + 8;
     p.xcopy_stride = B * p.xs_stride;
     p.cs_off = (int)(((size_t)ncopy * p.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const size_t zc_bytes = ncopy > 1 ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
+    const bool zp = r != 8 && nt == 1;  // k_stack's ZP rule (r = 6: one copy, constants still needed)
+    const size_t zc_bytes = zp ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
     p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
