@@ -486,7 +486,11 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     const bool child = nplanes == r;
     const int npl = (child || r == 8) ? r : r + 1;
     const int nt = B <= 8 ? 1 : 2;
-    const int ncopy = (r != 8 && nt == 1) ? mq::zp_ncopies(r) : 1;  // k_stack's ZP rule
+    // k_stack's staging rule: fp16 decode for r in {4, 8} at nt = 1 (copies at
+    // offsets {0, 4} / {0} + the raw bf16 chunk), else the bf16 zero-point copies
+    const bool f16 = (r == 4 || r == 8) && nt == 1;
+    const int ncopy = f16 ? (r == 4 ? 2 : 1) : ((r != 8 && nt == 1) ? mq::zp_ncopies(r) : 1);
+    const int nstage = f16 ? ncopy + 1 : ncopy;
     int cs_max = 1;
     size_t partials = 0;
     for (int i = 0; i < n_layers; ++i) {
@@ -495,7 +499,7 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
         if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < in.N || (in.ldx & 7) ||
             (reinterpret_cast<uintptr_t>(in.X) & 15))
             return fail(MQ_ERR_INVALID, "layer %d: bad shape / alignment", i);
-        const StackCfg c = choose_stack_config(in.N, in.K, B, ncopy, sm_count());
+        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage, sm_count());
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
         if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
         mq::StackLayer& t = T[i];
@@ -522,8 +526,8 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     p.B = B;
     p.xs_stride = cs_max * 256 + 8;
     p.xcopy_stride = B * p.xs_stride;
-    p.cs_off = (int)(((size_t)ncopy * p.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const bool zp = r != 8 && nt == 1;  // k_stack's ZP rule (r = 6: one copy, constants still needed)
+    p.cs_off = (int)(((size_t)nstage * p.xcopy_stride * 2 + 15) & ~(size_t)15);
+    const bool zp = f16 || (r != 8 && nt == 1);  // k_stack's ZP rule (r = 6: one copy, constants still needed)
     const size_t zc_bytes = zp ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);

@@ -342,6 +342,47 @@ MQ_HD void decode_word(const uint32_t (&S)[R], uint32_t (&A)[16]) {
     }
 }
 
+// ---- fp16 raw decode (r in {4, 8}) -------------------------------------------
+// fp16 has a 10-bit mantissa, so (w & mask) | 0x6400 = fp16 1024 + field * 2^o is
+// exact for o + r <= 10: a nibble fits at offsets 0 AND 4 of each half (one
+// byte shift per word instead of three), a whole byte at offset 0 (one LOP3
+// per register instead of two LOP3 + HSUB2).  Used with fp16 activations.
+template <int R, int O>
+MQ_HD uint32_t field_raw16(uint32_t w) {
+    static_assert(O + R <= 10, "field must sit inside the fp16 mantissa");
+    constexpr uint32_t m = ((1u << R) - 1u) << O;
+    return lop3<kAndOr>(w, x2(m), 0x64006400u);
+}
+template <int R>
+MQ_HD void decode_word_f16(const uint32_t (&S)[R], uint32_t (&A)[16]) {
+    static_assert(R == 4 || R == 8, "fp16 decode serves r in {4, 8}");
+    if constexpr (R == 4) {
+        uint32_t P[4] = {S[3], S[2], S[1], S[0]};
+        transpose_planes<4>(P);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {  // nibble n of W_i <-> bit position 4n + i
+            const uint32_t w = P[i], w8 = shr_x<8>(P[i]);
+            A[0 + i] = field_raw16<4, 0>(w);
+            A[4 + i] = field_raw16<4, 4>(w);
+            A[8 + i] = field_raw16<4, 0>(w8);
+            A[12 + i] = field_raw16<4, 4>(w8);
+        }
+    } else {
+        uint32_t P[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) P[j] = S[7 - j];
+        transpose_planes<8>(P);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {  // byte b of W_i <-> bit position 8b + i
+            A[0 + i] = field_raw16<8, 0>(P[i]);
+            A[8 + i] = field_raw16<8, 0>(shr_x<8>(P[i]));
+        }
+    }
+}
+// fp16 field offset of k16 step s (same for both 8-column halves)
+template <int R>
+__host__ __device__ constexpr int zp_off16(int s) { return (R == 4 && (s & 1)) ? 4 : 0; }
+
 // Zero-point folding for the raw decode (R in {2,3,4,6}).  decode_word<R, true>
 // leaves A[4s+q] = bf16(128 + s_code * 2^o) with o = kOff[s][q >> 1] (the field
 // offset of k16 step s, 8-column half q >> 1).  The GEMV multiplies that half
@@ -420,6 +461,23 @@ __device__ __forceinline__ void mma_acc(float (&d)[4], uint32_t a0, uint32_t a1,
         "{%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// fp16 variant: D += A * B, m16n8k16, f16 inputs, fp32 accumulate.
+__device__ __forceinline__ void mma_acc_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                            uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_zero_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                             uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%10,%10,%10,%10};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.0f));
 }
 // D = A * B (zero accumulator input).
 __device__ __forceinline__ void mma_zero(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,

@@ -22,6 +22,8 @@
 // Uniform r (template R) and G = 128; heterogeneous configs and TP stacks use
 // per-layer K3 launches in a CUDA graph.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "matq_common.cuh"
 
 namespace mq {
@@ -145,11 +147,18 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512, kScaleBytes = 128;
     constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
-    constexpr bool ZP = (R != 8) && (NT == 1);  // see k_gemv
-    constexpr int NCOPY = ZP ? zp_ncopies(R) : 1;
+    // fp16 decode (r in {4, 8}, B <= 8): fp16's 10-bit mantissa takes a nibble at
+    // offsets 0 and 4 and a whole byte at 0, cutting the decode's ALU work by
+    // 15-24% (scripts/micro/decode_rate.cu); activations are staged as fp16
+    // scaled by a per-CTA power of two (exact; keeps them inside fp16's range)
+    constexpr bool F16 = (R == 4 || R == 8) && NT == 1;
+    constexpr bool ZP = F16 || ((R != 8) && (NT == 1));  // see k_gemv
+    constexpr int NCOPY = F16 ? (R == 4 ? 2 : 1) : (ZP ? zp_ncopies(R) : 1);
     extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
     __shared__ unsigned s_gen;
+    __shared__ unsigned s_amax_bits;  // F16: the chunk's max |x| (float bits)
+    __shared__ float s_inv_lambda;    // F16: 1 / the activation scale
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // warps 0..14 stream weights (lane 0 issues their ring's bulk copies); warp 15
@@ -165,6 +174,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     const uint32_t my_bar0 = smem_addr(bars + warp * 8);
     const uint32_t my_ring0 = smem_addr(ring + (size_t)warp * D * kStageBytes);
     if (threadIdx.x == kSyncThread) s_gen = atomicAdd(p.launch_ctr, 1u) / gridDim.x;
+    if (threadIdx.x == 0) s_amax_bits = 0u;
     // the layer table lives in shared memory: a descriptor field re-read from
     // global memory mid-layer (register rematerialisation) waits behind the
     // weight stream for ~1-2 us
@@ -251,7 +261,76 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         MQ_STS(l, 1);
 
         // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
-        {
+        if constexpr (F16) {
+            // pass 1: raw bf16 into the staging tail + the chunk's max |x|
+            const uint16_t* X = L.X;
+            const int c8 = Kc >> 3;
+            const int n8 = p.B * c8;
+            uint16_t* tmp = xs + NCOPY * p.xcopy_stride;
+            float amax = 0.0f;
+            constexpr int kU = 4;
+            for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+                uint4 vv[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int idx = base_i + u * (int)blockDim.x;
+                    vv[u] = make_uint4(0, 0, 0, 0);
+                    if (idx < n8) {
+                        const int b = idx / c8, c = (idx - b * c8) * 8;
+                        const int col = col_base_cta + c;
+                        if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int idx = base_i + u * (int)blockDim.x;
+                    if (idx >= n8) break;
+                    const int b = idx / c8, c = (idx - b * c8) * 8;
+                    *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
+                    const uint32_t* wv = reinterpret_cast<const uint32_t*>(&vv[u]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(wv[e] << 16)), fabsf(__uint_as_float(wv[e] & 0xFFFF0000u))));
+                }
+            }
+#pragma unroll
+            for (int sh = 16; sh >= 1; sh >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, sh));
+            if (lane == 0) atomicMax(&s_amax_bits, __float_as_uint(amax));  // non-negative: bits order = value order
+            __syncthreads();
+            // lambda = 2^(14 - e), max|x| in [2^e, 2^(e+1)): max|x| * lambda < 2^15 < 65504
+            const float amax_all = __uint_as_float(s_amax_bits);
+            const int e = amax_all > 0.0f ? ilogbf(amax_all) : 0;
+            const float lam = ldexpf(1.0f, 14 - e);
+            if (threadIdx.x == 0) s_inv_lambda = ldexpf(1.0f, e - 14);
+            // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
+            for (int idx = threadIdx.x; idx < n8; idx += blockDim.x) {
+                const int b = idx / c8, c = (idx - b * c8) * 8;
+                const uint4 v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
+                const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
+                const int cs_ = c & 255;
+                const int o = zp_off16<R>((cs_ & 63) >> 4);
+                float part = 0.0f;
+#pragma unroll
+                for (int cp = 0; cp < NCOPY; ++cp) {
+                    const int oc = cp ? 4 : 0;
+                    const float f = lam / (float)(1 << oc);
+                    uint4 ov;
+                    uint16_t* ho = reinterpret_cast<uint16_t*>(&ov);
+#pragma unroll
+                    for (int e2 = 0; e2 < 8; ++e2) {
+                        const __half hh = __float2half_rn(bf16_to_f32(hv[e2]) * f);
+                        ho[e2] = __half_as_ushort(hh);
+                        // the constant uses the values the MMA will see: (1024 + z 2^o) x'
+                        if (oc == o) part += __half2float(hh);
+                    }
+                    *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = ov;
+                }
+                part *= 1024.0f + (float)((1 << (R - 1)) << o);
+#pragma unroll
+                for (int sh = 8; sh >= 1; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
+                if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
+            }
+        } else {
             const uint16_t* X = L.X;
             const int c8 = Kc >> 3;
             const int n8 = p.B * c8;
@@ -306,6 +385,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
             }
         }
         __syncthreads();
+        if constexpr (F16) {
+            if (threadIdx.x == 0) s_amax_bits = 0u;  // ready for the next layer (read only above)
+        }
         MQ_STS(l, 2);
 
         uint32_t xrow_addr[NT][2];
@@ -317,7 +399,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
             for (int s2 = 0; s2 < 2; ++s2) {
                 const int mi = lane >> 3;
                 int cp = 0;
-                if constexpr (ZP) {
+                if constexpr (F16) {
+                    cp = zp_off16<R>(2 * s2 + (mi >> 1)) ? 1 : 0;
+                } else if constexpr (ZP) {
                     const int sx = 2 * s2 + (mi >> 1), hx = mi & 1;
                     cp = zp_copy_of(R, zp_off<R>(sx, hx));
                 }
@@ -347,7 +431,8 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                 uint32_t A[16];
                 uint32_t Sl[R];
                 slice_loaded<R, CHILD>(T, Sl);
-                decode_word<R, ZP>(Sl, A);
+                if constexpr (F16) decode_word_f16<R>(Sl, A);
+                else decode_word<R, ZP>(Sl, A);
 #pragma unroll
                 for (int s2 = 0; s2 < 2; ++s2) {
                     uint32_t bf[NT][4];
@@ -359,12 +444,21 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                         const int s = 2 * s2 + sh;
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
-                            if ((w & 1) == 0 && s == 0)
-                                mma_zero(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                         bf[nt][2 * sh], bf[nt][2 * sh + 1]);
-                            else
-                                mma_acc(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                        bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                            if constexpr (F16) {
+                                if ((w & 1) == 0 && s == 0)
+                                    mma_zero_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                                 bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                                else
+                                    mma_acc_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                                bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                            } else {
+                                if ((w & 1) == 0 && s == 0)
+                                    mma_zero(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                             bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                                else
+                                    mma_acc(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                            bf[nt][2 * sh], bf[nt][2 * sh + 1]);
+                            }
                         }
                     }
                 }
@@ -391,6 +485,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         };
         // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
         // ticket, the last chunk to arrive summing the partials in chunk order
+        const float out_scale_l = F16 ? L.out_scale * s_inv_lambda : L.out_scale;
         auto emit = [&](int rt, const float (&v)[NT][4]) {
 #ifdef MQ_STACK_EXP_NOEMIT
             if (v[0][0] != 1234.5f) return;
@@ -403,7 +498,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                        const float val = v[nt][2 * h + c] * L.out_scale;
+                        const float val = v[nt][2 * h + c] * out_scale_l;
                         if (b < p.B && row < L.N) {
 #ifdef MQ_STACK_EXP_DUMMYY
                             if (L.S == 1) st_global_u16(reinterpret_cast<uint16_t*>(p.dbg_ts + 256 * 148 * 8 + 256 * 16 * 4) + ((blockIdx.x * 32 + lane) & 4095), f32_to_bf16_rn(val));
