@@ -286,6 +286,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-hetero", action="store_true", help="skip the C3 heterogeneous-config leg")
     ap.add_argument("--no-prefill", action="store_true", help="skip the C4 tcgen05 prefill leg")
+    ap.add_argument("--no-full", action="store_true", help="skip the full-model decode leg")
     ap.add_argument("--model", default="Llama-3.1-8B", help="Llama-3.1-8B | Qwen3-14B | Phi-3-Medium")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -500,6 +501,45 @@ def main():
         del hs
         torch.cuda.empty_cache()
 
+    # Full-model decode: the same sliced linears inside a
+    # Llama-3.1-8B-shaped decoder (bf16 attention over a 256-token KV cache,
+    # RMSNorm, RoPE, SiLU, bf16 lm_head), one CUDA graph per token; set beside
+    # the paper's own full-model numbers (RTX A6000)
+    full = None
+    if not args.no_full and world == 1 and args.model == "Llama-3.1-8B":
+        from paper_2602_03537_b200.llama import LlamaDecoder
+
+        if stack.graph is not None:
+            del stack.graph
+            stack.graph = None
+        torch.cuda.empty_cache()
+        paper = {2: 138.0, 3: 124.4, 4: 109.3}
+        dec = LlamaDecoder(batch=args.batch, context=256, bits=args.bits, n_layers=args.layers)
+        full = {"context": 256, "lm_head": "bf16 128256x4096", "attention": "torch SDPA (GQA), bf16",
+                "per_bits": {}}
+        for rb in (2, 3, 4, 8):
+            dec.set_bits(rb)
+            dec.capture()
+            for _ in range(args.warmup):
+                dec.step()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            clocks.active(True)
+            e0.record(dec.stream)
+            for _ in range(args.steps):
+                dec.step()
+            e1.record(dec.stream)
+            barrier()
+            clocks.active(False)
+            fsec = e0.elapsed_time(e1) / 1e3 / args.steps
+            rec = {"tok_s": args.batch / fsec, "ms_per_step": fsec * 1e3}
+            if rb in paper and args.batch == 1:
+                rec["paper_a6000_tok_s"] = paper[rb]
+                rec["vs_paper"] = (args.batch / fsec) / paper[rb]
+            full["per_bits"][str(rb)] = rec
+        del dec
+        torch.cuda.empty_cache()
+
     # C4: prefill on the tcgen05 path (K4), Qwen3-14B linear shapes, per layer
     prefill = None
     if not args.no_prefill and world == 1:
@@ -544,6 +584,7 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "roofline": roof,
         "roofline_k3_gate_up": roof_k3,
+        "full_model_decode": full,
         "hetero_c3": hetero,
         "prefill_c4": prefill,
         "cpu_baseline": cpu,

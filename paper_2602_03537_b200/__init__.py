@@ -9,10 +9,11 @@ C ABI, include/matq.h); there is no CPU fallback.
 """
 
 from . import _lib  # noqa: F401  (fails loudly if libmatq.so is missing)
-from .device import PlaneTensor, algorithmic_bytes, reserve_workspace
+from .device import PlaneTensor, StackProgram, algorithmic_bytes, reserve_workspace
 from .grid import BitWidthSet, GridError, QuantGrid, base_scale, dequant, dequant_value
 from .matmul import (MatmulError, MatmulTask, PackedLayer, bench, matmul_packed,
                      matmul_packed_device, matmul_ref, random_task)
+from .module import MatLinear
 from .packing import PackedTensor, PackError, pack, pack_slice, to_canonical, to_interleaved, unpack
 from .slicing import (BitConfig, NestedLayer, SlicedLayer, SliceError, slice_code, slice_layer,
                       slice_model, slice_to_code)

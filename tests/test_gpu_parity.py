@@ -458,3 +458,30 @@ def test_gemm_split_k_deterministic_and_ticket_reset(mq):
     # the shared workspace serves a K3 split-K GEMV afterwards (tickets at zero)
     y = pt.gemv(Xd[:1], 4, out_dtype=torch.float32).cpu().numpy()
     assert rel_err(y, O.parent_matmul_ref(codes, scales, 128, 4, X[:1])) <= 1e-4
+
+
+def test_matlinear_module(mq):
+    """The torch module: decode and prefill batches, leading dims, bits switch
+    without touching the weights, bias, fp32 input through the reference-API path."""
+    codes, scales = _parent(320, 1024, seed=55)
+    lin = mq.MatLinear.from_codes(codes, scales, 128, bits=4)
+    x = torch.from_numpy(_x_bf16(2 * 3, 1024, seed=9)).cuda().to(torch.bfloat16).reshape(2, 3, 1024)
+    for r in LADDER:
+        lin.set_bits(r)
+        y = lin(x)
+        assert y.shape == (2, 3, 320) and y.dtype == torch.bfloat16
+        want = O.parent_matmul_ref(codes, scales, 128, r, x.reshape(6, 1024).float().cpu().numpy())
+        assert rel_err(y.reshape(6, 320).float().cpu().numpy(), want) <= 1e-2
+    xp = torch.from_numpy(_x_bf16(100, 1024, seed=10)).cuda().to(torch.bfloat16)  # prefill -> K4
+    lin.set_bits(8)
+    want = O.parent_matmul_ref(codes, scales, 128, 8, xp.float().cpu().numpy())
+    assert rel_err(lin(xp).float().cpu().numpy(), want) <= 1e-2
+    bias = torch.randn(320, device="cuda")
+    lb = mq.MatLinear(lin.planes, 8, bias=bias)
+    want_b = lin(xp[:4]).float() + bias
+    assert rel_err(lb(xp[:4]).float().cpu().numpy(), want_b.cpu().numpy()) <= 1e-2
+    x32 = torch.from_numpy(_x_bf16(4, 1024, seed=11)).cuda()
+    want = O.parent_matmul_ref(codes, scales, 128, 8, x32.cpu().numpy())
+    assert rel_err(lin(x32).cpu().numpy(), want) <= 1e-4
+    with pytest.raises(ValueError):
+        lin.set_bits(5)
