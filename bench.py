@@ -474,7 +474,7 @@ def main():
     if not args.no_hetero and args.model == "Llama-3.1-8B":
         from paper_2602_03537_b200.config import budget_config, level_histogram
 
-        del stack.graph
+        stack.graph = None
         cfg = budget_config(3.5, shape=shape, seed=0, mutations=200, n_layers=args.layers)
         hs = LinearStack(shape, batch=args.batch, tp=world, rank=rank, process_group=pg,
                          n_layers=args.layers, fused=False)
@@ -509,9 +509,7 @@ def main():
     if not args.no_full and world == 1 and args.model == "Llama-3.1-8B":
         from paper_2602_03537_b200.llama import LlamaDecoder
 
-        if stack.graph is not None:
-            del stack.graph
-            stack.graph = None
+        stack.graph = None
         torch.cuda.empty_cache()
         paper = {2: 138.0, 3: 124.4, 4: 109.3}
         dec = LlamaDecoder(batch=args.batch, context=256, bits=args.bits, n_layers=args.layers)
