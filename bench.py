@@ -469,7 +469,8 @@ def main():
 
     # C3: heterogeneous per-layer bit-widths (EvoPress-style budget-exact 3.5-bit
     # config over the unfused linears, the reference's own moves), CUDA graph of
-    # the unfused stack: one launch per linear, each at its own r
+    # the unfused stack: one launch per linear, each at its own r (faster here
+    # than the per-layer-dispatch K3S kernel, scripts/stack_matrix.py)
     hetero = None
     if not args.no_hetero and args.model == "Llama-3.1-8B":
         from paper_2602_03537_b200.config import budget_config, level_histogram

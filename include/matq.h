@@ -137,7 +137,9 @@ MQ_API int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ld
  * kernel (one CTA per SM).  Replaces a per-layer loop of mq_gemv calls (and
  * the reference's per-layer packed_matmul calls); each layer's weight ring
  * keeps streaming across layer boundaries while the previous layer drains.
- * Uniform r, G = 128, bf16 X/Y, 1 <= B <= 16.
+ * G = 128, bf16 X/Y, 1 <= B <= 16.  r > 0: every layer sliced to r.  r = 0:
+ * each layer's own r (mq_stack_layer.r; an EvoPress configuration), parents
+ * only (nplanes = 8) -- one kernel dispatching per layer on its width.
  *   1. mq_stack_plan: host-only; fills a host plan (mq_stack_plan_bytes()) and
  *      a host layer table (mq_stack_table_bytes(n)) and returns the workspace
  *      size.  Copy the table to device memory (any time before the run).
@@ -150,6 +152,7 @@ typedef struct mq_stack_layer {
     void* Y;              /* bf16 (B, N), row stride ldy */
     int ldx, ldy, N, K;
     float out_scale;      /* 2^(c - r) for a parent slice */
+    int r;                /* this layer's bits when mq_stack_plan's r = 0; else ignored */
 } mq_stack_layer;
 MQ_API size_t mq_stack_plan_bytes(void);
 MQ_API size_t mq_stack_table_bytes(int n_layers);

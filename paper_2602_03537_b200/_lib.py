@@ -81,7 +81,7 @@ class StackLayer(ctypes.Structure):
 
     _fields_ = [("blob", ctypes.c_void_p), ("X", ctypes.c_void_p), ("Y", ctypes.c_void_p),
                 ("ldx", ctypes.c_int), ("ldy", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
-                ("out_scale", ctypes.c_float)]
+                ("out_scale", ctypes.c_float), ("r", ctypes.c_int)]
 
 
 class MatqError(RuntimeError):

@@ -428,9 +428,8 @@ struct StackPlanHost {  // the opaque host plan (mq_stack_plan_bytes)
 struct StackCfg {
     int S, cs, cpc;
 };
-StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms) {
+StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXsMaxStack) {
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
-    constexpr size_t kXsMaxStack = 80 * 1024;  // the stack ring needs only 2-4 stages
     StackCfg best_c{nsteps, 1, std::max(1, std::min(sms / nsteps, n_rt))};
     double best = 1e30;
     for (int S_try = 1; S_try <= nsteps; ++S_try) {
@@ -476,33 +475,56 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
                   void* table_host, size_t* workspace_bytes) {
     if (!layers || !plan_host || !table_host || !workspace_bytes || n_layers < 1)
         return fail(MQ_ERR_INVALID, "null pointer or empty stack");
-    if (!valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
-    if (nplanes < r || nplanes > 8 || (nplanes != r && nplanes < r + 1))
-        return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", r, nplanes);
+    if (r != 0 && !valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
+    if (r == 0 && nplanes != 8) return fail(MQ_ERR_INVALID, "per-layer bits need parent (8-plane) blobs");
     if (B < 1 || B > 16) return fail(MQ_ERR_INVALID, "stack decode batch %d outside [1, 16]", B);
     StackPlanHost* P = reinterpret_cast<StackPlanHost*>(plan_host);
     mq::StackLayer* T = reinterpret_cast<mq::StackLayer*>(table_host);
     memset(P, 0, sizeof(*P));
-    const bool child = nplanes == r;
-    const int npl = (child || r == 8) ? r : r + 1;
     const int nt = B <= 8 ? 1 : 2;
-    // k_stack's staging rule: fp16 decode for r in {4, 8} at nt = 1 (copies at
-    // offsets {0, 4} / {0} + the raw bf16 chunk), else the bf16 zero-point copies
-    const bool f16 = (r == 4 || r == 8) && nt == 1;
-    const int ncopy = f16 ? (r == 4 ? 2 : 1) : ((r != 8 && nt == 1) ? mq::zp_ncopies(r) : 1);
-    const int nstage = f16 ? ncopy + 1 : ncopy;
-    int cs_max = 1;
-    size_t partials = 0;
+    int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1;
+    bool zp_any = false, uniform = true;
+    size_t partials = 0, stage_max = 0;
+    // staging holds the most copies any layer stages and the ring the largest
+    // stage: every layer's K chunk is sized for both, so any layer fits
+    for (int i = 0; i < n_layers; ++i) {
+        const int ri = r ? r : layers[i].r;
+        if (!valid_r(ri)) return fail(MQ_ERR_INVALID, "layer %d: unsupported bits %d", i, ri);
+        // k_stack's staging rule: fp16 decode for r in {4, 8} at nt = 1 (copies at
+        // offsets {0, 4} / {0} + the raw bf16 chunk), else the bf16 zero-point copies
+        const bool f16 = (ri == 4 || ri == 8) && nt == 1;
+        const int ncopy = f16 ? (ri == 4 ? 2 : 1) : ((ri != 8 && nt == 1) ? mq::zp_ncopies(ri) : 1);
+        nstage_max = std::max(nstage_max, f16 ? ncopy + 1 : ncopy);
+        // k_stack's ZP rule (r = 6: one copy, constants still needed)
+        zp_any = zp_any || f16 || (ri != 8 && nt == 1);
+        const int npl = (nplanes == ri || ri == 8) ? ri : ri + 1;
+        stage_max = std::max(stage_max, (size_t)npl * 512 + 128);
+        nsteps_max = std::max(nsteps_max, mq::pad256(std::max(layers[i].K, 1)) / 256);
+    }
+    // everything but the activation chunk: table, partial slots, zero-point
+    // constants, barriers, a 2-deep ring
+    const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
+                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + mq::kStackWarps * 64 + (size_t)2 * mq::kStackWarps * stage_max + 256;
+    const size_t xs_budget = std::min<size_t>(80 * 1024, kSmemFullSm - std::min(other, kSmemFullSm));
     for (int i = 0; i < n_layers; ++i) {
         const mq_stack_layer& in = layers[i];
+        const int ri = r ? r : in.r;
+        if (!valid_r(ri)) return fail(MQ_ERR_INVALID, "layer %d: unsupported bits %d", i, ri);
+        if (nplanes < ri || nplanes > 8 || (nplanes != ri && nplanes < ri + 1))
+            return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", ri, nplanes);
         if (!in.blob || !in.X || !in.Y) return fail(MQ_ERR_INVALID, "layer %d: null pointer", i);
         if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < in.N || (in.ldx & 7) ||
             (reinterpret_cast<uintptr_t>(in.X) & 15))
             return fail(MQ_ERR_INVALID, "layer %d: bad shape / alignment", i);
-        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage, sm_count());
+        if (i == 0) r_first = ri;
+        uniform = uniform && ri == r_first;
+        const bool child = nplanes == ri;
+        const int npl = (child || ri == 8) ? ri : ri + 1;
+        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget);
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
         if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
         mq::StackLayer& t = T[i];
+        memset(&t, 0, sizeof(t));
         t.blob = in.blob;
         t.step_words = L.step_words;
         t.X = reinterpret_cast<const uint16_t*>(in.X);
@@ -518,6 +540,8 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
         t.cs = c.cs;
         t.cpc = c.cpc;
         t.out_scale = in.out_scale;
+        t.r = ri;
+        t.stage_bytes = npl * 512 + 128;
         cs_max = std::max(cs_max, c.cs);
         if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
     }
@@ -526,21 +550,20 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     p.B = B;
     p.xs_stride = cs_max * 256 + 8;
     p.xcopy_stride = B * p.xs_stride;
-    p.cs_off = (int)(((size_t)nstage * p.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const bool zp = f16 || (r != 8 && nt == 1);  // k_stack's ZP rule (r = 6: one copy, constants still needed)
-    const size_t zc_bytes = zp ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
+    p.cs_off = (int)(((size_t)nstage_max * p.xcopy_stride * 2 + 15) & ~(size_t)15);
+    const size_t zc_bytes = zp_any ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
     p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
     p.table_off = p.flag_off;
     p.xs_bytes = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
-    const size_t stage = (size_t)npl * 512 + 128;
     const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 8;
-    const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage));
+    const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage_max));
     if (d < 2) return fail(MQ_ERR_INVALID, "stack: activation staging leaves no room for the weight ring");
     p.stages = std::min(8, d);
-    P->smem = fixed + (size_t)mq::kStackWarps * p.stages * stage;
-    P->r = r;
+    p.stage_stride = (int)stage_max;
+    P->smem = fixed + (size_t)mq::kStackWarps * p.stages * stage_max;
+    P->r = uniform ? r_first : 0;  // 0: the per-layer dispatch kernel
     P->nplanes = nplanes;
     P->nt = nt;
     P->grid = sm_count();
@@ -574,6 +597,7 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
     const bool child = P->nplanes == P->r;
     cudaError_t e;
     switch (P->r) {
+        case 0: e = mq::launch_stack_mixed(p, P->nt, P->grid, P->smem, (cudaStream_t)stream); break;
         case 2: e = mq::launch_stack_r<2>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
         case 3: e = mq::launch_stack_r<3>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
         case 4: e = mq::launch_stack_r<4>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;

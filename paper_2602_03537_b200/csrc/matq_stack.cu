@@ -4,9 +4,9 @@
 namespace mq {
 
 namespace {
-template <int R, int NT, bool CHILD>
+template <int NT, int R, bool CHILD>
 cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaStream_t stream) {
-    auto kern = k_stack<R, NT, CHILD>;
+    auto kern = k_stack<NT, R, CHILD>;
     static int smem_set = 0;
     if ((int)smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -32,11 +32,16 @@ cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, s
                            cudaStream_t stream) {
     constexpr bool kChildOk = R < 8;
     if (child && kChildOk) {
-        if (nt == 1) return launch_one_stack<R, 1, kChildOk>(p, grid, smem, stream);
-        return launch_one_stack<R, 2, kChildOk>(p, grid, smem, stream);
+        if (nt == 1) return launch_one_stack<1, R, kChildOk>(p, grid, smem, stream);
+        return launch_one_stack<2, R, kChildOk>(p, grid, smem, stream);
     }
-    if (nt == 1) return launch_one_stack<R, 1, false>(p, grid, smem, stream);
-    return launch_one_stack<R, 2, false>(p, grid, smem, stream);
+    if (nt == 1) return launch_one_stack<1, R, false>(p, grid, smem, stream);
+    return launch_one_stack<2, R, false>(p, grid, smem, stream);
+}
+
+cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream) {
+    if (nt == 1) return launch_one_stack<1, 0, false>(p, grid, smem, stream);
+    return launch_one_stack<2, 0, false>(p, grid, smem, stream);
 }
 
 template cudaError_t launch_stack_r<2>(const StackParams&, int, bool, int, size_t, cudaStream_t);

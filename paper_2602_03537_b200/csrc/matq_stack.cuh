@@ -19,8 +19,9 @@
 //     cooperative launch;
 //   * the per-layer work split, slice, decode, zero-point folding, mma.sync
 //     and split-K fixup are K3's (matq_gemv.cuh) -- the same device code paths.
-// Uniform r (template R) and G = 128; heterogeneous configs and TP stacks use
-// per-layer K3 launches in a CUDA graph.
+// G = 128.  Uniform stacks run k_stack<NT, R>; heterogeneous stacks (per-layer
+// r, parents) run k_stack<NT, 0>, which dispatches each layer on its r.  TP
+// stacks use per-layer K3 launches in a CUDA graph.
 #pragma once
 #include <cuda_fp16.h>
 
@@ -37,6 +38,8 @@ struct __align__(8) StackLayer {
     int N, Np, K, nsteps, n_rt;
     int S, cs, cpc;  // K chunks, steps per chunk, CTAs per chunk
     float out_scale;
+    int r;            // slice width (the mixed kernel dispatches on it)
+    int stage_bytes;  // one ring stage: 128 B of scales + the planes read at r
 };
 
 struct StackParams {
@@ -51,6 +54,7 @@ struct StackParams {
     int flag_off;      // (unused)
     int table_off;     // byte offset of the shared-memory copy of the layer table
     int stages;        // per-warp ring depth
+    int stage_stride;  // bytes per ring slot (the largest stage of the stack)
     float* ws;         // split-K partials (max over layers)
     int* tickets;      // split-K tickets, self-resetting
     unsigned* done;    // [n_layers] monotone completion counters
@@ -107,6 +111,14 @@ __device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int 
 __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
     return (int)((long long)warp * (w.ntiles * w.ns) / kStackWarps);
 }
+// Warps after wa holding a part of the tile ending at step f_last: those whose
+// range starts inside the tile and is not empty (a CTA with fewer (tile, step)
+// pairs than warps leaves some warps without work; they never arrive).
+__device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last) {
+    int n = 0;
+    for (int v = wa + 1; v < kStackWarps && plan_f0(w, v) <= f_last; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
+    return n;
+}
 
 // Publish: bar.sync orders the CTA's writes before thread 0's release at gpu
 // scope (cumulative), which the waiters' ld.acquire.gpu synchronises with.
@@ -142,11 +154,71 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     return v;
 }
 
+constexpr int kSyncThread = kStackWarps * 32;
+
+// Per-warp weight ring: the issue cursor (lane 0) walks (layer, flattened step)
+// of this warp across layer boundaries; each layer's stage is its own size
+// (scales + its plane count) in slots of the plan's largest stage.
+struct RingCtx {
+    uint32_t bar0, ring0, stride;
+    int D;
+    uint64_t policy;
+    int cta, warp, n_layers;
+    const StackLayer* tab;
+};
+struct StackCursor {
+    int il, iff, istage, itile, isi, insteps;
+    WarpPlan ip;
+    const uint32_t* iblob;
+    long long isw;
+    uint32_t ibytes;
+};
+__device__ __forceinline__ void cursor_next_layer(StackCursor& c, const RingCtx& rc) {
+    for (++c.il; c.il < rc.n_layers; ++c.il) {  // the next layer with work for this warp
+        const StackLayer& L = rc.tab[c.il];
+        c.ip = warp_plan(L, rc.cta, rc.warp);
+        if (c.ip.f1 > c.ip.f0) {
+            c.iblob = L.blob;
+            c.isw = L.step_words;
+            c.insteps = L.nsteps;
+            c.ibytes = (uint32_t)L.stage_bytes;
+            c.iff = c.ip.f0;
+            c.itile = c.ip.ta + c.ip.f0 / c.ip.ns;
+            c.isi = c.ip.f0 % c.ip.ns;
+            return;
+        }
+    }
+}
+__device__ __forceinline__ void cursor_issue(StackCursor& c, const RingCtx& rc) {  // no-op when done
+    if (c.il >= rc.n_layers) return;
+    const uint32_t* src = c.iblob + ((long long)c.itile * c.insteps + c.ip.chunk0 + c.isi) * c.isw;
+    if (++c.isi == c.ip.ns) {
+        c.isi = 0;
+        ++c.itile;
+    }
+    const uint32_t bar = rc.bar0 + 8 * c.istage;
+    mbar_expect_tx(bar, c.ibytes);
+    bulk_g2s(rc.ring0 + c.istage * rc.stride, src, c.ibytes, bar, rc.policy);
+    if (++c.istage == rc.D) c.istage = 0;
+    if (++c.iff == c.ip.f1) cursor_next_layer(c, rc);
+}
+
+struct StackShared {
+    unsigned gen;
+    unsigned amax_bits;  // F16: the chunk's max |x| (float bits)
+    float inv_lambda;    // F16: 1 / the activation scale
+};
+
+// One layer of the step, slice width R.  Uniform stacks instantiate k_stack
+// with R fixed; heterogeneous stacks (an EvoPress configuration: per-layer r)
+// dispatch here on the layer table's r -- the ring and cursor are shared.
 template <int R, int NT, bool CHILD>
-__global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p) {
+__device__ __forceinline__ void stack_layer(const StackParams& p, const StackLayer* tab, int l,
+                                            StackCursor& cur, const RingCtx& rc, int& cstage,
+                                            uint32_t& parity, StackShared& sh, uint8_t* smem,
+                                            unsigned target) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512, kScaleBytes = 128;
-    constexpr uint32_t kStageBytes = kScaleBytes + NPL * kSlab;
     // fp16 decode (r in {4, 8}, B <= 8): fp16's 10-bit mantissa takes a nibble at
     // offsets 0 and 4 and a whole byte at 0, cutting the decode's ALU work by
     // 15-24% (scripts/micro/decode_rate.cu); activations are staged as fp16
@@ -154,201 +226,117 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     constexpr bool F16 = (R == 4 || R == 8) && NT == 1;
     constexpr bool ZP = F16 || ((R != 8) && (NT == 1));  // see k_gemv
     constexpr int NCOPY = F16 ? (R == 4 ? 2 : 1) : (ZP ? zp_ncopies(R) : 1);
-    extern __shared__ __align__(16) uint8_t smem[];
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
-    __shared__ unsigned s_gen;
-    __shared__ unsigned s_amax_bits;  // F16: the chunk's max |x| (float bits)
-    __shared__ float s_inv_lambda;    // F16: 1 / the activation scale
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // warps 0..14 stream weights (lane 0 issues their ring's bulk copies); warp 15
-    // only synchronises: its fences never wait on in-flight bulk copies (a
-    // memory barrier on a warp with outstanding cp.async.bulk waits for them)
     const bool ring_warp = warp < kStackWarps;
-    constexpr int kSyncThread = kStackWarps * 32;
     const int g = lane >> 2, t = lane & 3;
-    const int cta = blockIdx.x;
-    const int D = p.stages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
-    uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 8;
-    const uint32_t my_bar0 = smem_addr(bars + warp * 8);
-    const uint32_t my_ring0 = smem_addr(ring + (size_t)warp * D * kStageBytes);
-    if (threadIdx.x == kSyncThread) s_gen = atomicAdd(p.launch_ctr, 1u) / gridDim.x;
-    if (threadIdx.x == 0) s_amax_bits = 0u;
-    // the layer table lives in shared memory: a descriptor field re-read from
-    // global memory mid-layer (register rematerialisation) waits behind the
-    // weight stream for ~1-2 us
-    StackLayer* tab = reinterpret_cast<StackLayer*>(smem + p.table_off);
-    {
-        const int words = p.n_layers * (int)(sizeof(StackLayer) / 4);
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.layers);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(tab);
-        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
-    }
-    uint64_t policy = 0;
-    if (ring_warp && lane == 0) {
-        policy = policy_evict_first();
-        for (int i = 0; i < D; ++i) mbar_init(my_bar0 + 8 * i, 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    const unsigned target = (s_gen + 1u) * gridDim.x;
-
-    // ---- issue cursor: (layer, flattened step f) of this warp, across layers --
-    int il = -1, iff = 0, istage = 0, itile = 0, isi = 0;
-    WarpPlan ip{};
-    const uint32_t* iblob = nullptr;
-    long long isw = 0;
-    int insteps = 0;
-    auto next_layer = [&]() {  // advance il to the next layer with work for this warp
-        for (++il; il < p.n_layers; ++il) {
-            const StackLayer& L = tab[il];
-            ip = warp_plan(L, cta, warp);
-            if (ip.f1 > ip.f0) {
-                iblob = L.blob;
-                isw = L.step_words;
-                insteps = L.nsteps;
-                iff = ip.f0;
-                itile = ip.ta + ip.f0 / ip.ns;
-                isi = ip.f0 % ip.ns;
-                return;
-            }
-        }
-    };
-    int cur_layer = 0;  // consumer's layer (experiments: cap the cross-layer prefetch)
-    int pending = 0;    // issues skipped while capped
-    auto issue_next = [&]() {  // lane 0; no-op once the warp has nothing left
-        if (il >= p.n_layers) return;
-#ifdef MQ_STACK_EXP_NOXLAYER
-        if (il > cur_layer) { ++pending; return; }
-#endif
-        const uint32_t* src = iblob + ((long long)itile * insteps + ip.chunk0 + isi) * isw;
-        if (++isi == ip.ns) {
-            isi = 0;
-            ++itile;
-        }
-        const uint32_t bar = my_bar0 + 8 * istage;
-        mbar_expect_tx(bar, kStageBytes);
-        bulk_g2s(my_ring0 + istage * kStageBytes, src, kStageBytes, bar, policy);
-        if (++istage == D) istage = 0;
-        if (++iff == ip.f1) next_layer();
-    };
-    if (ring_warp && lane == 0) {
-        next_layer();
-        for (int i = 0; i < D; ++i) issue_next();
-    }
-
-    int cstage = 0;
-    uint32_t parity = 0;
+    const int D = rc.D;
     const uint32_t xs_saddr = smem_addr(xs);
     float* zc = reinterpret_cast<float*>(smem + p.cs_off);  // [2 cs groups][NT * 8] zero-point constants
 
-#pragma unroll 1
-    for (int l = 0; l < p.n_layers; ++l) {
-        const StackLayer& L = tab[l];
-        const WarpPlan wp = ring_warp ? warp_plan(L, cta, warp) : warp_plan(L, cta, 0);
-        const int Kc = L.cs * kStepCols;
-        const int col_base = wp.chunk0 * kStepCols;
-        const int col_base_cta = col_base;  // every warp of the CTA shares its chunk
+    const StackLayer& L = tab[l];
+    const WarpPlan wp = ring_warp ? warp_plan(L, rc.cta, warp) : warp_plan(L, rc.cta, 0);
+    const int Kc = L.cs * kStepCols;
+    const int col_base = wp.chunk0 * kStepCols;  // every warp of the CTA shares its chunk
 
-        // ---- wait for the producer of this layer's activations ---------------
-        MQ_STS(l, 0);
-        if (l > 0 && threadIdx.x == kSyncThread) {
-            while (ld_acquire_u32(p.done + l - 1) < target) {
+    // ---- wait for the producer of this layer's activations ---------------
+    MQ_STS(l, 0);
+    if (l > 0 && threadIdx.x == kSyncThread) {
+        while (ld_acquire_u32(p.done + l - 1) < target) {
+        }
+    }
+    __syncthreads();
+    MQ_STS(l, 1);
+
+    // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
+    if constexpr (F16) {
+        // pass 1: raw bf16 into the staging tail + the chunk's max |x|
+        const uint16_t* X = L.X;
+        const int c8 = Kc >> 3;
+        const int n8 = p.B * c8;
+        uint16_t* tmp = xs + NCOPY * p.xcopy_stride;
+        float amax = 0.0f;
+        constexpr int kU = 4;
+        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+            uint4 vv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = base_i + u * (int)blockDim.x;
+                vv[u] = make_uint4(0, 0, 0, 0);
+                if (idx < n8) {
+                    const int b = idx / c8, c = (idx - b * c8) * 8;
+                    const int col = col_base + c;
+                    if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = base_i + u * (int)blockDim.x;
+                if (idx >= n8) break;
+                const int b = idx / c8, c = (idx - b * c8) * 8;
+                *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
+                const uint32_t* wv = reinterpret_cast<const uint32_t*>(&vv[u]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(wv[e] << 16)), fabsf(__uint_as_float(wv[e] & 0xFFFF0000u))));
             }
         }
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
+        if (lane == 0) atomicMax(&sh.amax_bits, __float_as_uint(amax));  // non-negative: bits order = value order
         __syncthreads();
-        MQ_STS(l, 1);
-
-        // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
-        if constexpr (F16) {
-            // pass 1: raw bf16 into the staging tail + the chunk's max |x|
-            const uint16_t* X = L.X;
-            const int c8 = Kc >> 3;
-            const int n8 = p.B * c8;
-            uint16_t* tmp = xs + NCOPY * p.xcopy_stride;
-            float amax = 0.0f;
-            constexpr int kU = 4;
-            for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
-                uint4 vv[kU];
+        // lambda = 2^(14 - e), max|x| in [2^e, 2^(e+1)): max|x| * lambda < 2^15 < 65504
+        const float amax_all = __uint_as_float(sh.amax_bits);
+        const int e = amax_all > 0.0f ? ilogbf(amax_all) : 0;
+        const float lam = ldexpf(1.0f, 14 - e);
+        if (threadIdx.x == 0) sh.inv_lambda = ldexpf(1.0f, e - 14);
+        // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
+        for (int idx = threadIdx.x; idx < n8; idx += blockDim.x) {
+            const int b = idx / c8, c = (idx - b * c8) * 8;
+            const uint4 v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
+            const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
+            const int cs_ = c & 255;
+            const int o = zp_off16<R>((cs_ & 63) >> 4);
+            float part = 0.0f;
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int idx = base_i + u * (int)blockDim.x;
-                    vv[u] = make_uint4(0, 0, 0, 0);
-                    if (idx < n8) {
-                        const int b = idx / c8, c = (idx - b * c8) * 8;
-                        const int col = col_base_cta + c;
-                        if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
-                    }
+            for (int cp = 0; cp < NCOPY; ++cp) {
+                const int oc = cp ? 4 : 0;
+                const float f = lam / (float)(1 << oc);
+                uint4 ov;
+                uint16_t* ho = reinterpret_cast<uint16_t*>(&ov);
+#pragma unroll
+                for (int e2 = 0; e2 < 8; ++e2) {
+                    const __half hh = __float2half_rn(bf16_to_f32(hv[e2]) * f);
+                    ho[e2] = __half_as_ushort(hh);
+                    // the constant uses the values the MMA will see: (1024 + z 2^o) x'
+                    if (oc == o) part += __half2float(hh);
                 }
+                *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = ov;
+            }
+            part *= 1024.0f + (float)((1 << (R - 1)) << o);
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int idx = base_i + u * (int)blockDim.x;
-                    if (idx >= n8) break;
+            for (int s = 8; s >= 1; s >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s);
+            if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
+        }
+    } else {
+        const uint16_t* X = L.X;
+        const int c8 = Kc >> 3;
+        const int n8 = p.B * c8;
+        constexpr int kU = 4;  // loads in flight per thread before the first use
+        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+            uint4 vv[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int idx = base_i + u * (int)blockDim.x;
+                vv[u] = make_uint4(0, 0, 0, 0);
+                if (idx < n8) {
                     const int b = idx / c8, c = (idx - b * c8) * 8;
-                    *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
-                    const uint32_t* wv = reinterpret_cast<const uint32_t*>(&vv[u]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(wv[e] << 16)), fabsf(__uint_as_float(wv[e] & 0xFFFF0000u))));
+                    const int col = col_base + c;
+                    if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
                 }
             }
 #pragma unroll
-            for (int sh = 16; sh >= 1; sh >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, sh));
-            if (lane == 0) atomicMax(&s_amax_bits, __float_as_uint(amax));  // non-negative: bits order = value order
-            __syncthreads();
-            // lambda = 2^(14 - e), max|x| in [2^e, 2^(e+1)): max|x| * lambda < 2^15 < 65504
-            const float amax_all = __uint_as_float(s_amax_bits);
-            const int e = amax_all > 0.0f ? ilogbf(amax_all) : 0;
-            const float lam = ldexpf(1.0f, 14 - e);
-            if (threadIdx.x == 0) s_inv_lambda = ldexpf(1.0f, e - 14);
-            // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
-            for (int idx = threadIdx.x; idx < n8; idx += blockDim.x) {
-                const int b = idx / c8, c = (idx - b * c8) * 8;
-                const uint4 v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
-                const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
-                const int cs_ = c & 255;
-                const int o = zp_off16<R>((cs_ & 63) >> 4);
-                float part = 0.0f;
-#pragma unroll
-                for (int cp = 0; cp < NCOPY; ++cp) {
-                    const int oc = cp ? 4 : 0;
-                    const float f = lam / (float)(1 << oc);
-                    uint4 ov;
-                    uint16_t* ho = reinterpret_cast<uint16_t*>(&ov);
-#pragma unroll
-                    for (int e2 = 0; e2 < 8; ++e2) {
-                        const __half hh = __float2half_rn(bf16_to_f32(hv[e2]) * f);
-                        ho[e2] = __half_as_ushort(hh);
-                        // the constant uses the values the MMA will see: (1024 + z 2^o) x'
-                        if (oc == o) part += __half2float(hh);
-                    }
-                    *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = ov;
-                }
-                part *= 1024.0f + (float)((1 << (R - 1)) << o);
-#pragma unroll
-                for (int sh = 8; sh >= 1; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
-                if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
-            }
-        } else {
-            const uint16_t* X = L.X;
-            const int c8 = Kc >> 3;
-            const int n8 = p.B * c8;
-            constexpr int kU = 4;  // loads in flight per thread before the first use
-            for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
-                uint4 vv[kU];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int idx = base_i + u * (int)blockDim.x;
-                    vv[u] = make_uint4(0, 0, 0, 0);
-                    if (idx < n8) {
-                        const int b = idx / c8, c = (idx - b * c8) * 8;
-                        const int col = col_base_cta + c;
-                        if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
+            for (int u = 0; u < kU; ++u) {
                 const int idx = base_i + u * (int)blockDim.x;
                 if (idx >= n8) break;  // warp-uniform: n8 is a multiple of 32
                 const int b = idx / c8, c = (idx - b * c8) * 8;
@@ -366,7 +354,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                     for (int e = 0; e < 8; ++e) part += bf16_to_f32(hx[e]);
                     part *= m;
 #pragma unroll
-                    for (int sh = 8; sh >= 1; sh >>= 1) part += __shfl_xor_sync(0xffffffffu, part, sh);
+                    for (int s = 8; s >= 1; s >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s);
                     if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
                 }
                 if constexpr (NCOPY > 1) {
@@ -381,273 +369,306 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
                         *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = o;
                     }
                 }
-                }
             }
         }
-        __syncthreads();
-        if constexpr (F16) {
-            if (threadIdx.x == 0) s_amax_bits = 0u;  // ready for the next layer (read only above)
-        }
-        MQ_STS(l, 2);
+    }
+    __syncthreads();
+    if constexpr (F16) {
+        if (threadIdx.x == 0) sh.amax_bits = 0u;  // ready for the next layer (read only above)
+    }
+    MQ_STS(l, 2);
 
-        uint32_t xrow_addr[NT][2];
+    uint32_t xrow_addr[NT][2];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-            int n = nt * 8 + (lane & 7);
-            if (n >= p.B) n = 0;
+    for (int nt = 0; nt < NT; ++nt) {
+        int n = nt * 8 + (lane & 7);
+        if (n >= p.B) n = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+            const int mi = lane >> 3;
+            int cp = 0;
+            if constexpr (F16) {
+                cp = zp_off16<R>(2 * s2 + (mi >> 1)) ? 1 : 0;
+            } else if constexpr (ZP) {
+                const int sx = 2 * s2 + (mi >> 1), hx = mi & 1;
+                cp = zp_copy_of(R, zp_off<R>(sx, hx));
+            }
+            xrow_addr[nt][s2] = xs_saddr + (uint32_t)(cp * p.xcopy_stride + n * p.xs_stride + 8 * mi) * 2u;
+        }
+    }
+    MQ_STS(l, 3);
+
+    // ---- this warp's units of layer l --------------------------------------
+    float tot[NT][4], acc[NT][4];
+    auto process = [&](const uint4 (&buf)[NPL], const float (&sc)[4], int st) {
+        const uint32_t xcol = (uint32_t)(st * kStepCols - col_base);
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            uint32_t T[NPL];
+#pragma unroll
+            for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
+            uint32_t A[16];
+            uint32_t Sl[R];
+            slice_loaded<R, CHILD>(T, Sl);
+            if constexpr (F16) decode_word_f16<R>(Sl, A);
+            else decode_word<R, ZP>(Sl, A);
 #pragma unroll
             for (int s2 = 0; s2 < 2; ++s2) {
-                const int mi = lane >> 3;
-                int cp = 0;
-                if constexpr (F16) {
-                    cp = zp_off16<R>(2 * s2 + (mi >> 1)) ? 1 : 0;
-                } else if constexpr (ZP) {
-                    const int sx = 2 * s2 + (mi >> 1), hx = mi & 1;
-                    cp = zp_copy_of(R, zp_off<R>(sx, hx));
-                }
-                xrow_addr[nt][s2] = xs_saddr + (uint32_t)(cp * p.xcopy_stride + n * p.xs_stride + 8 * mi) * 2u;
-            }
-        }
-        MQ_STS(l, 3);
-#ifdef MQ_STACK_EXP_NOXLAYER
-        cur_layer = l;
-        if (ring_warp && lane == 0) {
-            const int n = pending;
-            pending = 0;
-            for (int i = 0; i < n; ++i) issue_next();
-        }
-        __syncwarp();
-#endif
-
-        // ---- this warp's units of layer l --------------------------------------
-        float tot[NT][4], acc[NT][4];
-        auto process = [&](const uint4 (&buf)[NPL], const float (&sc)[4], int st) {
-            const uint32_t xcol = (uint32_t)(st * kStepCols - col_base);
+                uint32_t bf[NT][4];
 #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-                uint32_t T[NPL];
+                for (int nt = 0; nt < NT; ++nt)
+                    ldmatrix_x4(bf[nt], xrow_addr[nt][s2] + (xcol + 64 * w + 32 * s2) * 2u);
 #pragma unroll
-                for (int jj = 0; jj < NPL; ++jj) T[jj] = word_of(buf[jj], w);
-                uint32_t A[16];
-                uint32_t Sl[R];
-                slice_loaded<R, CHILD>(T, Sl);
-                if constexpr (F16) decode_word_f16<R>(Sl, A);
-                else decode_word<R, ZP>(Sl, A);
-#pragma unroll
-                for (int s2 = 0; s2 < 2; ++s2) {
-                    uint32_t bf[NT][4];
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
-                        ldmatrix_x4(bf[nt], xrow_addr[nt][s2] + (xcol + 64 * w + 32 * s2) * 2u);
-#pragma unroll
-                    for (int sh = 0; sh < 2; ++sh) {
-                        const int s = 2 * s2 + sh;
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt) {
-                            if constexpr (F16) {
-                                if ((w & 1) == 0 && s == 0)
-                                    mma_zero_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                                 bf[nt][2 * sh], bf[nt][2 * sh + 1]);
-                                else
-                                    mma_acc_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                                bf[nt][2 * sh], bf[nt][2 * sh + 1]);
-                            } else {
-                                if ((w & 1) == 0 && s == 0)
-                                    mma_zero(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                             bf[nt][2 * sh], bf[nt][2 * sh + 1]);
-                                else
-                                    mma_acc(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
-                                            bf[nt][2 * sh], bf[nt][2 * sh + 1]);
-                            }
-                        }
-                    }
-                }
-                if (w & 1) {
-                    const float s_lo = sc[(w >> 1) * 2], s_hi = sc[(w >> 1) * 2 + 1];
+                for (int sh2 = 0; sh2 < 2; ++sh2) {
+                    const int s = 2 * s2 + sh2;
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) {
-                        if constexpr (ZP) {
-                            const float* zp = zc + ((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t;
-                            const float c0 = zp[0], c1 = zp[1];
-                            tot[nt][0] = fmaf(s_lo, acc[nt][0] - c0, tot[nt][0]);
-                            tot[nt][1] = fmaf(s_lo, acc[nt][1] - c1, tot[nt][1]);
-                            tot[nt][2] = fmaf(s_hi, acc[nt][2] - c0, tot[nt][2]);
-                            tot[nt][3] = fmaf(s_hi, acc[nt][3] - c1, tot[nt][3]);
+                        if constexpr (F16) {
+                            if ((w & 1) == 0 && s == 0)
+                                mma_zero_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                             bf[nt][2 * sh2], bf[nt][2 * sh2 + 1]);
+                            else
+                                mma_acc_f16(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                            bf[nt][2 * sh2], bf[nt][2 * sh2 + 1]);
                         } else {
-                            tot[nt][0] = fmaf(s_lo, acc[nt][0], tot[nt][0]);
-                            tot[nt][1] = fmaf(s_lo, acc[nt][1], tot[nt][1]);
-                            tot[nt][2] = fmaf(s_hi, acc[nt][2], tot[nt][2]);
-                            tot[nt][3] = fmaf(s_hi, acc[nt][3], tot[nt][3]);
+                            if ((w & 1) == 0 && s == 0)
+                                mma_zero(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                         bf[nt][2 * sh2], bf[nt][2 * sh2 + 1]);
+                            else
+                                mma_acc(acc[nt], A[4 * s], A[4 * s + 1], A[4 * s + 2], A[4 * s + 3],
+                                        bf[nt][2 * sh2], bf[nt][2 * sh2 + 1]);
                         }
                     }
                 }
             }
-        };
-        // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
-        // ticket, the last chunk to arrive summing the partials in chunk order
-        const float out_scale_l = F16 ? L.out_scale * s_inv_lambda : L.out_scale;
-        auto emit = [&](int rt, const float (&v)[NT][4]) {
-#ifdef MQ_STACK_EXP_NOEMIT
-            if (v[0][0] != 1234.5f) return;
-#endif
-            const int r0 = rt * kTileRows + g;
+            if (w & 1) {
+                const float s_lo = sc[(w >> 1) * 2], s_hi = sc[(w >> 1) * 2 + 1];
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                        const float val = v[nt][2 * h + c] * out_scale_l;
-                        if (b < p.B && row < L.N) {
-#ifdef MQ_STACK_EXP_DUMMYY
-                            if (L.S == 1) st_global_u16(reinterpret_cast<uint16_t*>(p.dbg_ts + 256 * 148 * 8 + 256 * 16 * 4) + ((blockIdx.x * 32 + lane) & 4095), f32_to_bf16_rn(val));
-#else
-                            if (L.S == 1) st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(val));
-#endif
-                            else st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
-                        }
+                for (int nt = 0; nt < NT; ++nt) {
+                    if constexpr (ZP) {
+                        const float* zp = zc + ((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t;
+                        const float c0 = zp[0], c1 = zp[1];
+                        tot[nt][0] = fmaf(s_lo, acc[nt][0] - c0, tot[nt][0]);
+                        tot[nt][1] = fmaf(s_lo, acc[nt][1] - c1, tot[nt][1]);
+                        tot[nt][2] = fmaf(s_hi, acc[nt][2] - c0, tot[nt][2]);
+                        tot[nt][3] = fmaf(s_hi, acc[nt][3] - c1, tot[nt][3]);
+                    } else {
+                        tot[nt][0] = fmaf(s_lo, acc[nt][0], tot[nt][0]);
+                        tot[nt][1] = fmaf(s_lo, acc[nt][1], tot[nt][1]);
+                        tot[nt][2] = fmaf(s_hi, acc[nt][2], tot[nt][2]);
+                        tot[nt][3] = fmaf(s_hi, acc[nt][3], tot[nt][3]);
                     }
-            if (L.S == 1) return;
-            __syncwarp();
-            int last = 0;
-            // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
-            if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == L.S - 1);
-            last = __shfl_sync(0xffffffffu, last, 1);
-            if (!last) return;
+                }
+            }
+        }
+    };
+    // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
+    // ticket, the last chunk to arrive summing the partials in chunk order
+    const float out_scale_l = F16 ? L.out_scale * sh.inv_lambda : L.out_scale;
+    auto emit = [&](int rt, const float (&v)[NT][4]) {
+        const int r0 = rt * kTileRows + g;
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt)
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h)
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                        if (b < p.B && row < L.N) {
-                            const float* wq = p.ws + (long long)b * L.Np + row;
-                            const long long cstride = (long long)p.B * L.Np;
-                            float sum = 0.0f;
-                            int q = 0;
-                            for (; q + 4 <= L.S; q += 4) {
-                                const float a0 = __ldcg(wq + q * cstride), a1 = __ldcg(wq + (q + 1) * cstride);
-                                const float a2 = __ldcg(wq + (q + 2) * cstride), a3 = __ldcg(wq + (q + 3) * cstride);
-                                sum += a0; sum += a1; sum += a2; sum += a3;
-                            }
-                            for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
-                            st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(sum));
-                        }
+                for (int c = 0; c < 2; ++c) {
+                    const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                    const float val = v[nt][2 * h + c] * out_scale_l;
+                    if (b < p.B && row < L.N) {
+                        if (L.S == 1) st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(val));
+                        else st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
                     }
-            __syncwarp();
-            if (lane == 0) p.tickets[rt] = 0;
-        };
-        // A tile cut by warp boundaries (warps wa < ... < wb) is emitted by wa, the
-        // warp holding its first step: that is wa's LAST segment, so wa finishes it
-        // last.  wa+1..wb park their parts in their slot (only their FIRST segment
-        // can be such a part) and raise their flag; wa adds them in warp order.
-        float* slots = reinterpret_cast<float*>(smem + p.slot_off);
-        auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
-        const int first_lt = wp.ns > 0 ? wp.f0 / wp.ns : 0;
-        int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
-        const int f_end = ring_warp ? wp.f1 : wp.f0;
+                }
+        if (L.S == 1) return;
+        __syncwarp();
+        int last = 0;
+        // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
+        if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == L.S - 1);
+        last = __shfl_sync(0xffffffffu, last, 1);
+        if (!last) return;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                    if (b < p.B && row < L.N) {
+                        const float* wq = p.ws + (long long)b * L.Np + row;
+                        const long long cstride = (long long)p.B * L.Np;
+                        float sum = 0.0f;
+                        int q = 0;
+                        for (; q + 4 <= L.S; q += 4) {
+                            const float a0 = __ldcg(wq + q * cstride), a1 = __ldcg(wq + (q + 1) * cstride);
+                            const float a2 = __ldcg(wq + (q + 2) * cstride), a3 = __ldcg(wq + (q + 3) * cstride);
+                            sum += a0; sum += a1; sum += a2; sum += a3;
+                        }
+                        for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
+                        st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(sum));
+                    }
+                }
+        __syncwarp();
+        if (lane == 0) p.tickets[rt] = 0;
+    };
+    // A tile cut by warp boundaries (warps wa < ... < wb) is emitted by wa, the
+    // warp holding its first step: that is wa's LAST segment, so wa finishes it
+    // last.  wa+1..wb park their parts in their slot (only their FIRST segment
+    // can be such a part) and raise their flag; wa adds them in warp order.
+    float* slots = reinterpret_cast<float*>(smem + p.slot_off);
+    auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
+    const int first_lt = wp.ns > 0 ? wp.f0 / wp.ns : 0;
+    int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
+    const int f_end = ring_warp ? wp.f1 : wp.f0;
 #pragma unroll 1
-        for (int f = wp.f0; f < f_end; ++f) {
-            const int st = wp.chunk0 + si;
-            if (f == wp.f0 || si == 0) {
+    for (int f = wp.f0; f < f_end; ++f) {
+        const int st = wp.chunk0 + si;
+        if (f == wp.f0 || si == 0) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
+        }
+        mbar_wait(rc.bar0 + 8 * cstage, parity);
+        const uint32_t src = rc.ring0 + cstage * rc.stride;
+        float sc[4];
+        sc[0] = lds32f(src + g * 4);
+        sc[1] = lds32f(src + (g + 8) * 4);
+        sc[2] = lds32f(src + (16 + g) * 4);
+        sc[3] = lds32f(src + (24 + g) * 4);
+        uint4 buf[NPL];
+#pragma unroll
+        for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
+        __syncwarp();
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            cursor_issue(cur, rc);
+        }
+        process(buf, sc, st);
+        if (++cstage == D) {
+            cstage = 0;
+            parity ^= 1u;
+        }
+        if (f + 1 == wp.f1) MQ_STS_WMAX(l, 5);  // this warp's last step decoded
+        const bool tile_end = si == wp.ns - 1;
+        if (tile_end || f + 1 == wp.f1) {
+            const bool starts_tile = wp.f0 <= lt * wp.ns;  // this segment holds the tile's first step
+            if (starts_tile && tile_end) {
+                emit(wp.ta + lt, tot);
+            } else if (!starts_tile) {
+                float* sp = slot_ptr(warp);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
-            }
-            mbar_wait(my_bar0 + 8 * cstage, parity);
-            const uint32_t src = my_ring0 + cstage * kStageBytes;
-            float sc[4];
-            sc[0] = lds32f(src + g * 4);
-            sc[1] = lds32f(src + (g + 8) * 4);
-            sc[2] = lds32f(src + (16 + g) * 4);
-            sc[3] = lds32f(src + (24 + g) * 4);
-            uint4 buf[NPL];
-#pragma unroll
-            for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
-            __syncwarp();
-            if (lane == 0) {
-                fence_proxy_async_smem();
-                issue_next();
-            }
-            process(buf, sc, st);
-            if (++cstage == D) {
-                cstage = 0;
-                parity ^= 1u;
-            }
-            if (f + 1 == wp.f1) {
-                MQ_STS_WMAX(l, 5);  // this warp's last step decoded
-                MQ_STS_W0(l, 1);
-            }
-            if (f == wp.f0) MQ_STS_W0(l, 0);
-            const bool tile_end = si == wp.ns - 1;
-            if (tile_end || f + 1 == wp.f1) {
-                const bool starts_tile = wp.f0 <= lt * wp.ns;  // this segment holds the tile's first step
-                if (starts_tile && tile_end) {
-                    emit(wp.ta + lt, tot);
-                } else if (!starts_tile) {
-                    float* sp = slot_ptr(warp);
+                    for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
+                // hand the part to the emitter wa (holder of the tile's first step)
+                // through named barrier wa + 1: bar.arrive orders the slot stores and
+                // does not wait, and -- unlike a memory fence -- does not stall on
+                // lane 0's in-flight ring bulk copies
+                int wa = warp - 1;
+                while (wa > 0 && plan_f0(wp, wa) > lt * wp.ns) --wa;
+                named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, (lt + 1) * wp.ns - 1)));
+            } else {
+                // emitter: own part, then the later warps' parts in warp order
+                const int f_last = (lt + 1) * wp.ns - 1;
+                named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, f_last)));
+                for (int w2 = warp + 1; w2 < kStackWarps && plan_f0(wp, w2) <= f_last; ++w2) {
+                    if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
+                    const float* sp = slot_ptr(w2);
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
-                    // hand the part to the emitter wa (holder of the tile's first step)
-                    // through named barrier wa + 1: bar.arrive orders the slot stores and
-                    // does not wait, and -- unlike a memory fence -- does not stall on
-                    // lane 0's in-flight ring bulk copies
-                    int wa = warp - 1;
-                    while (wa > 0 && plan_f0(wp, wa) > lt * wp.ns) --wa;
-                    int wb = wa + 1;
-                    while (wb + 1 < kStackWarps && plan_f0(wp, wb + 1) <= (lt + 1) * wp.ns - 1) ++wb;
-                    MQ_STS_W0(l, 2);
-                    named_bar_arrive(wa + 1, 32 * (wb - wa + 1));
-                } else {
-                    // emitter: own part, then warps warp+1 .. wb in warp order
-                    const int f_last = (lt + 1) * wp.ns - 1;
-                    int wb = warp + 1;
-                    while (wb + 1 < kStackWarps && plan_f0(wp, wb + 1) <= f_last) ++wb;
-                    MQ_STS_W0(l, 1);
-                    named_bar_sync(warp + 1, 32 * (wb - warp + 1));
-                    for (int w2 = warp + 1; w2 <= wb; ++w2) {
-                        const float* sp = slot_ptr(w2);
-#pragma unroll
-                        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                            for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
-                    }
-#ifdef MQ_GEMV_TIMING
-                    {   // stamp when the accumulators are actually available
-                        float dep = tot[0][0] + tot[0][3];
-                        asm volatile("mov.b32 %0, %0;" : "+f"(dep));
-                        if (dep == 1.2345e30f) tot[0][1] = dep;
-                    }
-#endif
-                    MQ_STS_W0(l, 2);
-                    emit(wp.ta + lt, tot);
-                    MQ_STS_W0(l, 3);
+                        for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
                 }
-            }
-            if (++si == wp.ns) {
-                si = 0;
-                ++lt;
+                emit(wp.ta + lt, tot);
             }
         }
-        MQ_STS(l, 4);
+        if (++si == wp.ns) {
+            si = 0;
+            ++lt;
+        }
+    }
+    MQ_STS(l, 4);
 
-        // ---- publish layer l ------------------------------------------------
-        __syncthreads();
-        MQ_STS(l, 6);
-        // thread 1: thread 0 issues warp 0's bulk copies, and the release would wait
-        // for those in-flight loads
-        if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1u);
-        MQ_STS(l, 7);
+    // ---- publish layer l ------------------------------------------------
+    __syncthreads();
+    MQ_STS(l, 6);
+    // the sync warp: a ring warp's release would wait for its in-flight bulk copies
+    if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1u);
+    MQ_STS(l, 7);
+}
+
+// RFIX = the uniform slice width, or 0: per-layer r from the table (parents only)
+template <int NT, int RFIX, bool CHILD>
+__global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ StackShared sh;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // warps 0..14 stream weights (lane 0 issues their ring's bulk copies); warp 15
+    // only synchronises: its fences never wait on in-flight bulk copies (a
+    // memory barrier on a warp with outstanding cp.async.bulk waits for them)
+    const bool ring_warp = warp < kStackWarps;
+    const int D = p.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
+    uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 8;
+    if (threadIdx.x == kSyncThread) sh.gen = atomicAdd(p.launch_ctr, 1u) / gridDim.x;
+    if (threadIdx.x == 0) sh.amax_bits = 0u;
+    // the layer table lives in shared memory: a descriptor field re-read from
+    // global memory mid-layer (register rematerialisation) waits behind the
+    // weight stream for ~1-2 us
+    StackLayer* tab = reinterpret_cast<StackLayer*>(smem + p.table_off);
+    {
+        const int words = p.n_layers * (int)(sizeof(StackLayer) / 4);
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(p.layers);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(tab);
+        for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+    RingCtx rc;
+    rc.bar0 = smem_addr(bars + warp * 8);
+    rc.ring0 = smem_addr(ring + (size_t)warp * D * p.stage_stride);
+    rc.stride = (uint32_t)p.stage_stride;
+    rc.D = D;
+    rc.policy = 0;
+    rc.cta = blockIdx.x;
+    rc.warp = warp;
+    rc.n_layers = p.n_layers;
+    rc.tab = tab;
+    if (ring_warp && lane == 0) {
+        rc.policy = policy_evict_first();
+        for (int i = 0; i < D; ++i) mbar_init(rc.bar0 + 8 * i, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const unsigned target = (sh.gen + 1u) * gridDim.x;
+
+    StackCursor cur{};
+    cur.il = -1;
+    if (ring_warp && lane == 0) {
+        cursor_next_layer(cur, rc);
+        for (int i = 0; i < D; ++i) cursor_issue(cur, rc);
+    }
+    int cstage = 0;
+    uint32_t parity = 0;
+#pragma unroll 1
+    for (int l = 0; l < p.n_layers; ++l) {
+        if constexpr (RFIX != 0) {
+            stack_layer<RFIX, NT, CHILD>(p, tab, l, cur, rc, cstage, parity, sh, smem, target);
+        } else {
+            switch (tab[l].r) {
+                case 2: stack_layer<2, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 3: stack_layer<3, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 4: stack_layer<4, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 6: stack_layer<6, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                default: stack_layer<8, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+            }
+        }
     }
 }
 
 template <int R>
 cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, size_t smem,
                            cudaStream_t stream);
+cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream);
 
 }  // namespace mq

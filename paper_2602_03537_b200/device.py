@@ -328,12 +328,14 @@ class StackProgram:
     """A whole decode step on the persistent K3S kernel (mq_stack_plan / mq_stack_run).
 
     ``layers``: (PlaneTensor, X, Y) in dependency order -- X of layer i+1 is
-    (a column slice of) Y of layer i.  All layers share r; X / Y bf16 CUDA
-    tensors with unit column stride.  The host plan and the device layer table
-    are built once; ``run()`` is one asynchronous, graph-capturable launch.
+    (a column slice of) Y of layer i.  ``r``: one width for every layer, or a
+    per-layer sequence (parents only; one kernel dispatching per layer).  X / Y
+    bf16 CUDA tensors with unit column stride.  The host plan and the device
+    layer table are built once; ``run()`` is one asynchronous,
+    graph-capturable launch.
     """
 
-    def __init__(self, layers, r: int, B: int):
+    def __init__(self, layers, r, B: int):
         import ctypes
 
         _lib.require_cuda()
@@ -341,8 +343,11 @@ class StackProgram:
         n = len(layers)
         arr = (_lib.StackLayer * n)()
         nplanes = None
+        rs = [int(r)] * n if isinstance(r, int) else [int(x) for x in r]
+        if len(rs) != n:
+            raise ValueError("%d bit-widths for %d layers" % (len(rs), n))
         for i, (pt, X, Y) in enumerate(layers):
-            scale = pt._check(r)
+            scale = pt._check(rs[i])
             if pt.G != 128:
                 raise ValueError("the stack kernel needs group size 128")
             if nplanes is None:
@@ -352,11 +357,14 @@ class StackProgram:
             if X.dtype != torch.bfloat16 or Y.dtype != torch.bfloat16 or X.stride(1) != 1 or Y.stride(1) != 1:
                 raise ValueError("stack activations must be bf16 with unit column stride")
             arr[i] = _lib.StackLayer(_lib.ptr(pt.blob), X.data_ptr(), Y.data_ptr(), X.stride(0), Y.stride(0),
-                                     pt.N, pt.K, scale)
+                                     pt.N, pt.K, scale, rs[i])
+        r_plan = rs[0] if len(set(rs)) == 1 else 0
+        if r_plan == 0 and nplanes != 8:
+            raise ValueError("per-layer bit-widths need parent layers")
         self.plan = ctypes.create_string_buffer(L.mq_stack_plan_bytes())
         table = ctypes.create_string_buffer(L.mq_stack_table_bytes(n))
         ws = ctypes.c_size_t(0)
-        _lib.call("mq_stack_plan", ctypes.cast(arr, ctypes.c_void_p), n, B, r, nplanes, self.plan, table,
+        _lib.call("mq_stack_plan", ctypes.cast(arr, ctypes.c_void_p), n, B, r_plan, nplanes, self.plan, table,
                   ctypes.byref(ws))
         self.table = torch.frombuffer(bytearray(table.raw), dtype=torch.uint8).cuda()
         self.ws = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")

@@ -188,17 +188,23 @@ class LinearStack:
         return out
 
     def stack_kernel_ok(self, config) -> bool:
-        """The persistent K3S path serves uniform-r, single-GPU stacks with B <= 16
-        whose layers read only the previous layer's output (the fused stack)."""
+        """Where the persistent K3S path is the default: single-GPU fused stacks,
+        B <= 16, uniform r (1.00-1.11x the per-layer K3 graph, scripts/
+        stack_matrix.py).  Heterogeneous parents also run on it (stack_kernel=
+        True: one kernel dispatching per layer on its r) but measure at par
+        with the K3 graph fused and 0.75x unfused (224 layers, many small:
+        the grid-wide layer barrier costs more than PDL's overlap), so the
+        graph stays their default."""
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
-        return (len(rs) == 1 and self.tp == 1 and self.B <= 16 and self.fused and self.G == 128)
+        return (len(rs) == 1 and self.fused and self.tp == 1 and self.B <= 16 and self.G == 128)
 
     def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None) -> None:
         """(Re)capture the decode step for a per-layer bit-width config.
 
-        Uniform configs run as ONE persistent K3S launch per step (weights keep
-        streaming across layer boundaries); heterogeneous configs, TP and B > 16
-        run as a CUDA graph of per-layer K3 launches with PDL."""
+        Single-GPU stacks with B <= 16 run as ONE persistent K3S launch per step
+        (weights keep streaming across layer boundaries; a heterogeneous config
+        dispatches per layer inside the kernel); TP and B > 16 run as a CUDA
+        graph of per-layer K3 launches with PDL."""
         if isinstance(config, int):
             config = {n: config for n in self.names}
         missing = [n for n in self.names if n not in config]
@@ -213,7 +219,8 @@ class LinearStack:
         if use_stack:
             from .device import StackProgram
 
-            self.program = StackProgram(self._stack_layers(), next(iter(self.config.values())), self.B)
+            rs = [self.config[n] for n, _, _ in self.layers]
+            self.program = StackProgram(self._stack_layers(), rs[0] if len(set(rs)) == 1 else rs, self.B)
             run = lambda: self.program.run(self.stream)  # noqa: E731
         else:
             run = lambda: self._run(self.config, pdl)  # noqa: E731

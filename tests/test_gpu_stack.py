@@ -78,13 +78,67 @@ def test_stack_kernel_two_blocks_and_children(model):
     stack.layers = saved
 
 
-def test_uniform_configs_default_to_stack_kernel(model):
+def test_configs_default_to_stack_kernel(model):
     stack = model.LinearStack(model.LLAMA31_8B, batch=2, n_layers=1)
     stack.capture(3)
     assert stack.program is not None
     cfg = {n: (2 if i % 2 else 4) for i, n in enumerate(stack.names)}
-    stack.capture(cfg)
+    stack.capture(cfg)  # heterogeneous: the per-layer K3 graph by default
     assert stack.program is None and stack.launches_per_step() == len(stack.names)
+    stack.capture(cfg, stack_kernel=True)  # or the per-layer dispatch kernel
+    assert stack.program is not None and stack.launches_per_step() == 1
+
+
+def _check_mixed(stack, cfg, x0, y, bufs, tol=1e-2):
+    """One block (4 layers): each layer at its own r against fp32."""
+    (nq, _, qkv), (no, _, o), (ng, _, gu), (nd, _, down) = stack.layers[:4]
+    ins = {nq: x0, no: bufs["qkv"][:, :o.K], ng: bufs["o"], nd: bufs["gate_up"][:, :down.K]}
+    outs = {nq: bufs["qkv"], no: bufs["o"], ng: bufs["gate_up"], nd: y}
+    for name, pt in zip((nq, no, ng, nd), (qkv, o, gu, down)):
+        got = outs[name].float()
+        if not torch.isfinite(got).all():
+            continue
+        want = ins[name].float() @ pt.decode(cfg[name]).T
+        assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= tol, (name, cfg[name])
+
+
+@pytest.mark.parametrize("B", [1, 4, 12])
+def test_stack_kernel_heterogeneous(model, B):
+    """Per-layer r inside one persistent kernel: every width of the ladder
+    across the layer kinds, each layer against fp32, replays bitwise stable,
+    and the same numbers as the per-layer K3 graph within bf16 tolerance."""
+    stack = model.LinearStack(model.LLAMA31_8B, batch=B, n_layers=1)
+    g = torch.Generator(device="cuda").manual_seed(100 + B)
+    x0 = torch.randn(B, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    for shift in range(len(LADDER)):
+        cfg = {n: LADDER[(i + shift) % len(LADDER)] for i, n in enumerate(stack.names)}
+        stack.capture(cfg, stack_kernel=True)
+        assert stack.program is not None and stack.launches_per_step() == 1
+        y, bufs = _step(stack, x0)
+        _check_mixed(stack, cfg, x0, y, bufs)
+        y2, b2 = _step(stack, x0)
+        torch.testing.assert_close(y2, y, rtol=0, atol=0, equal_nan=True)
+        stack.capture(cfg, stack_kernel=False)
+        _, wb = _step(stack, x0)
+        assert rel_err(wb["qkv"].float().cpu().numpy(), bufs["qkv"].float().cpu().numpy()) <= 1e-2
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_stack_kernel_heterogeneous_multiblock(model, fused):
+    """An EvoPress-like random per-layer config over 3 blocks (12 fused / 21
+    unfused linears; unfused layers also read outputs older than the previous
+    layer's)."""
+    stack = model.LinearStack(model.LLAMA31_8B, batch=1, n_layers=3, fused=fused)
+    rng = np.random.default_rng(7)
+    cfg = {n: int(rng.choice(LADDER)) for n in stack.names}
+    x0 = torch.randn(1, 4096, device="cuda").to(torch.bfloat16) * 0.5
+    stack.capture(cfg, stack_kernel=True)
+    y, _ = _step(stack, x0)
+    stack.capture(cfg, stack_kernel=False)
+    y_ref, _ = _step(stack, x0)
+    fin = torch.isfinite(y.float()) & torch.isfinite(y_ref.float())
+    assert fin.any()
+    assert rel_err(y.float()[fin].cpu().numpy(), y_ref.float()[fin].cpu().numpy()) <= 3e-2
 
 
 def test_llama_decoder_full_model_step(model):
