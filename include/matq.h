@@ -186,6 +186,35 @@ MQ_API int mq_pack_ref_layout(const uint8_t* codes, int N, int K, int bits, uint
 MQ_API int mq_unpack_ref_layout(const uint64_t* base, const uint32_t* b2, const uint32_t* b3, int N, int K,
                          uint8_t* codes, void* stream);
 
+/* ---- MatGPTQ quantiser searches, float64 ---------- *
+ * A BitWidthSet (grid.py:27-66) is passed as host arrays targets[T]
+ * (distinct, ascending, in [2, 8]; the last is the master width c) and
+ * lams[T] (positive).  Matrices are row-major device float64 with a row
+ * stride; scales are float32 (d_row, ngs) group scales.  Results are
+ * bit-identical to the reference's numpy (same operation order, no FMA
+ * contraction).  All three are asynchronous. */
+
+/* select_codes (gptq.py:104-140): per weight, the master code minimising
+ * sum_t lams[t] * (w - s * mv_t[q])^2; ties to the smallest code. */
+MQ_API int mq_select_codes(const double* W, long long ldw, int d_row, int d_col, const float* scales,
+                           int ngs, int G, const int* targets, const double* lams, int T, uint8_t* codes,
+                           long long ldc, void* stream);
+
+/* fit_grid (grid.py:160-212): the shrink search over alphas[steps] (device,
+ * numpy.linspace(1, shrink_min, steps)) per (row, group) -> float32 scales
+ * (d_row, ceil(d_col / G)). */
+MQ_API int mq_fit_grid(const double* W, long long ldw, int d_row, int d_col, int G, const int* targets,
+                       const double* lams, int T, const double* alphas, int steps, float* scales, void* stream);
+
+/* One column block [lo, hi) of quantize_layer's loop (gptq.py:203-222):
+ * codes[:, lo:hi], the compensated snapshot comp[:, lo:hi], the scaled errors
+ * err (d_row, hi - lo), and Wc's in-block rank-1 updates.  The caller applies
+ * Wc[:, hi:] -= err @ chol[lo:hi, hi:] (a dgemm) before the next block. */
+MQ_API int mq_gptq_block(double* Wc, long long ldw, int d_row, int d_col, int lo, int hi, const float* scales,
+                         int ngs, int G, const double* chol, long long ldch, const int* targets,
+                         const double* lams, int T, uint8_t* codes, long long ldc, double* comp,
+                         long long ldcomp, double* err, long long lde, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,10 @@ _SIGS = {
     "mq_matmul_ref": ([_vp, _i, _i, _vp, _i, _vp, _vp], _i),
     "mq_pack_ref_layout": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp], _i),
     "mq_unpack_ref_layout": ([_vp, _vp, _vp, _i, _i, _vp, _vp], _i),
+    "mq_select_codes": ([_vp, _ll, _i, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _ll, _vp], _i),
+    "mq_fit_grid": ([_vp, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp, _vp], _i),
+    "mq_gptq_block": ([_vp, _ll, _i, _i, _i, _i, _vp, _i, _i, _vp, _ll, _vp, _vp, _i, _vp, _ll, _vp, _ll, _vp,
+                       _ll, _vp], _i),
 }
 
 EXPORTS = tuple(_SIGS)

@@ -694,4 +694,62 @@ int mq_unpack_ref_layout(const uint64_t* base, const uint32_t* b2, const uint32_
                        "mq_unpack_ref_layout");
 }
 
+// ---- MatGPTQ quantiser searches ------------------------------------------
+static int quant_targets(const int* targets, const double* lams, int T, mq::QuantTargets* tg) {
+    if (!targets || !lams || T < 1 || T > 7) return fail(MQ_ERR_INVALID, "bad bit-width set");
+    tg->T = T;
+    for (int t = 0; t < T; ++t) {
+        if (targets[t] < 2 || targets[t] > 8 || (t && targets[t] <= targets[t - 1]))
+            return fail(MQ_ERR_INVALID, "bit-widths must be distinct, sorted and in [2, 8]");
+        if (!(lams[t] > 0.0) || lams[t] > 1.7976931348623157e308)
+            return fail(MQ_ERR_INVALID, "importance weights must be positive and finite");
+        tg->r[t] = targets[t];
+        tg->lam[t] = lams[t];
+    }
+    tg->c = targets[T - 1];
+    return MQ_OK;
+}
+
+int mq_select_codes(const double* W, long long ldw, int d_row, int d_col, const float* scales, int ngs, int G,
+                    const int* targets, const double* lams, int T, uint8_t* codes, long long ldc, void* stream) {
+    mq::QuantTargets tg;
+    if (int st = quant_targets(targets, lams, T, &tg)) return st;
+    if (!W || !scales || !codes) return fail(MQ_ERR_INVALID, "null pointer");
+    if (d_row < 0 || d_col < 0 || G < 1 || ldw < d_col || ldc < d_col || ngs < (d_col + G - 1) / G)
+        return fail(MQ_ERR_INVALID, "bad shape");
+    if ((long long)d_row * d_col == 0) return MQ_OK;
+    return cuda_status(mq::launch_select_codes(W, ldw, d_row, d_col, scales, ngs, G, tg, codes, ldc,
+                                               (cudaStream_t)stream),
+                       "mq_select_codes");
+}
+
+int mq_fit_grid(const double* W, long long ldw, int d_row, int d_col, int G, const int* targets,
+                const double* lams, int T, const double* alphas, int steps, float* scales, void* stream) {
+    mq::QuantTargets tg;
+    if (int st = quant_targets(targets, lams, T, &tg)) return st;
+    if (!W || !alphas || !scales) return fail(MQ_ERR_INVALID, "null pointer");
+    if (d_row < 1 || d_col < 1) return fail(MQ_ERR_INVALID, "weights must be a non-empty matrix");
+    if (steps < 1) return fail(MQ_ERR_INVALID, "steps must be >= 1");
+    if (G < 1 || G > 4096 || ldw < d_col) return fail(MQ_ERR_INVALID, "bad shape");
+    const int ngs = (d_col + G - 1) / G;
+    return cuda_status(mq::launch_fit_grid(W, ldw, d_row, d_col, G, tg, alphas, steps, scales, ngs,
+                                           (cudaStream_t)stream),
+                       "mq_fit_grid");
+}
+
+int mq_gptq_block(double* Wc, long long ldw, int d_row, int d_col, int lo, int hi, const float* scales, int ngs,
+                  int G, const double* chol, long long ldch, const int* targets, const double* lams, int T,
+                  uint8_t* codes, long long ldc, double* comp, long long ldcomp, double* err, long long lde,
+                  void* stream) {
+    mq::QuantTargets tg;
+    if (int st = quant_targets(targets, lams, T, &tg)) return st;
+    if (!Wc || !scales || !chol || !codes || !comp || !err) return fail(MQ_ERR_INVALID, "null pointer");
+    if (d_row < 1 || lo < 0 || hi <= lo || hi > d_col || G < 1 || ldw < d_col || ldch < d_col ||
+        ldc < d_col || ldcomp < d_col || lde < hi - lo || ngs < (d_col + G - 1) / G)
+        return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_gptq_block(Wc, ldw, d_row, lo, hi, scales, ngs, G, chol, ldch, tg, codes, ldc,
+                                             comp, ldcomp, err, lde, (cudaStream_t)stream),
+                       "mq_gptq_block");
+}
+
 }  // extern "C"

@@ -33,6 +33,22 @@ cudaError_t launch_unpack_ref_layout(const unsigned long long* base, const uint3
                                      const uint32_t* b3, int N, int K, uint8_t* codes,
                                      cudaStream_t s);
 
+// MatGPTQ quantiser (matq_quant.cu): the target set of a BitWidthSet
+struct QuantTargets {
+    int T, c;       // number of targets, master bit-width (the largest target)
+    int r[8];       // targets, ascending
+    double lam[8];  // importance weights
+};
+cudaError_t launch_select_codes(const double* W, long long ldw, int d_row, int d_col, const float* scales,
+                                int ngs, int G, const QuantTargets& tg, uint8_t* codes, long long ldc,
+                                cudaStream_t s);
+cudaError_t launch_fit_grid(const double* W, long long ldw, int d_row, int d_col, int G, const QuantTargets& tg,
+                            const double* alphas, int steps, float* scales, int ngs, cudaStream_t s);
+cudaError_t launch_gptq_block(double* Wc, long long ldw, int d_row, int lo, int hi, const float* scales, int ngs,
+                              int G, const double* chol, long long ldch, const QuantTargets& tg, uint8_t* codes,
+                              long long ldc, double* comp, long long ldcomp, double* err, long long lde,
+                              cudaStream_t s);
+
 struct GemmConfig {
     int bn, n_tiles, S, cs, grid;
 };
