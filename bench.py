@@ -273,6 +273,79 @@ def prefill_leg(torch, mq, clocks, batches=(64, 256, 1024), bits=(4, 8), reps=10
 
 
 # ------------------------------------------------------------------ GPU arm --
+def quant_leg(torch, mq, cpu: bool, N=4096, K=4096, G=128, cpu_rows=16):
+    """the MatGPTQ quantiser searches (csrc/matq_quant.cu) on
+    a Llama-3.1-8B-sized layer, targets {2,3,4,6,8}: device time of
+    select_codes / fit_grid (CUDA events, inputs resident) and of
+    quantize_layer through the numpy drop-in API; the oracle (the reference's
+    algorithm in numpy) on a row sample, scaled by rows."""
+    import time
+
+    import numpy as np
+
+    from paper_2602_03537_b200 import _lib
+    from paper_2602_03537_b200.grid import _targets_args
+
+    rng = np.random.default_rng(0)
+    bits = mq.BitWidthSet((2, 3, 4, 6, 8), (1.0, 1.0, 1.0, 1.0, 1.0))
+    W = rng.standard_normal((N, K)) * 0.02
+    Wd = torch.from_numpy(W).cuda()
+    t, w, T = _targets_args(bits)
+    alphas = torch.from_numpy(np.linspace(1.0, 0.5, 51)).cuda()
+    ng = -(-K // G)
+    sc = torch.empty(N, ng, dtype=torch.float32, device="cuda")
+    codes = torch.empty(N, K, dtype=torch.uint8, device="cuda")
+
+    def fit():
+        _lib.call("mq_fit_grid", _lib.ptr(Wd), K, N, K, G, t, w, T, _lib.ptr(alphas), 51, _lib.ptr(sc),
+                  _lib.stream_ptr(None))
+
+    def sel():
+        _lib.call("mq_select_codes", _lib.ptr(Wd), K, N, K, _lib.ptr(sc), ng, G, t, w, T, _lib.ptr(codes), K,
+                  _lib.stream_ptr(None))
+
+    def dev_time(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps / 1e3
+
+    t_fit, t_sel = dev_time(fit), dev_time(sel)
+    grid = mq.QuantGrid(8, G, sc.cpu().numpy())
+    X = rng.standard_normal((K, 256))
+    factor = mq.factor_inverse(mq.build_hessian(X, 0.01), 0.01)
+    mq.quantize_layer(W[:256], factor, mq.QuantGrid(8, G, grid.scales[:256]), bits)  # warm cuBLAS
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mq.quantize_layer(W, factor, grid, bits, block_size=128)
+    t_gq = time.perf_counter() - t0
+    out = {"layer": [N, K], "targets": list(bits.targets), "group_size": G, "fit_steps": 51,
+           "device_s": {"select_codes": t_sel, "fit_grid": t_fit},
+           "api_s": {"quantize_layer": t_gq,
+                     "note": "numpy in/out: includes 2x134 MB H2D and 134 MB D2H of float64"},
+           "weights_per_s": {"select_codes": N * K / t_sel, "fit_grid": N * K / t_fit},
+           "parity": "select_codes / fit_grid bit-exact vs the reference (tests/test_gpu_quant.py)"}
+    if cpu:
+        from oracle import quant_oracle as Q
+
+        c0 = time.perf_counter()
+        Q.select_codes(W[:cpu_rows], grid.scales[:cpu_rows], G, bits.targets, bits.weights)
+        c_sel = (time.perf_counter() - c0) * N / cpu_rows
+        c0 = time.perf_counter()
+        Q.fit_grid(W[:cpu_rows], bits.targets, bits.weights, G)
+        c_fit = (time.perf_counter() - c0) * N / cpu_rows
+        out["cpu_baseline_s"] = {"select_codes": c_sel, "fit_grid": c_fit, "kind": "port", "cores": 1,
+                                 "sample": "%d of %d rows, scaled by rows (numpy oracle)" % (cpu_rows, N)}
+    del Wd, codes, sc
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -287,6 +360,7 @@ def main():
     ap.add_argument("--no-hetero", action="store_true", help="skip the C3 heterogeneous-config leg")
     ap.add_argument("--no-prefill", action="store_true", help="skip the C4 tcgen05 prefill leg")
     ap.add_argument("--no-full", action="store_true", help="skip the full-model decode leg")
+    ap.add_argument("--no-quant", action="store_true", help="skip the quantiser-search leg")
     ap.add_argument("--model", default="Llama-3.1-8B", help="Llama-3.1-8B | Qwen3-14B | Phi-3-Medium")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -544,6 +618,11 @@ def main():
     if not args.no_prefill and world == 1:
         prefill = prefill_leg(torch, mq, clocks)
 
+    # the quantiser's searches
+    quant = None
+    if not args.no_quant and world == 1:
+        quant = quant_leg(torch, mq, cpu=not args.no_cpu)
+
     clk = clocks.summary()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -586,6 +665,7 @@ def main():
         "full_model_decode": full,
         "hetero_c3": hetero,
         "prefill_c4": prefill,
+        "quantizer_8f4": quant,
         "cpu_baseline": cpu,
         "clocks": clk,
         # K3 launches inside the headline timed region (K captured steps)
