@@ -104,19 +104,27 @@ __device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int 
     w.chunk0 = w.kc * L.cs;
     w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
     const int P = w.ntiles * w.ns;
-    w.f0 = (int)((long long)warp * P / kStackWarps);
-    w.f1 = (int)((long long)(warp + 1) * P / kStackWarps);
+    w.f0 = warp * P / kStackWarps;
+    w.f1 = (warp + 1) * P / kStackWarps;
     return w;
 }
 __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
-    return (int)((long long)warp * (w.ntiles * w.ns) / kStackWarps);
+    return warp * (w.ntiles * w.ns) / kStackWarps;
+}
+// The last warp whose range starts at or before step x: the largest v with
+// floor(v P / 15) <= x, i.e. v = ceil(15 (x + 1) / P) - 1 (never an empty warp).
+__device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
+    const int P = w.ntiles * w.ns;
+    return min(kStackWarps - 1, (kStackWarps * (x + 1) + P - 1) / P - 1);
 }
 // Warps after wa holding a part of the tile ending at step f_last: those whose
 // range starts inside the tile and is not empty (a CTA with fewer (tile, step)
 // pairs than warps leaves some warps without work; they never arrive).
 __device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last) {
+    const int vmax = last_warp_at(w, f_last);
+    if (w.ntiles * w.ns >= kStackWarps) return vmax - wa;  // no empty warps
     int n = 0;
-    for (int v = wa + 1; v < kStackWarps && plan_f0(w, v) <= f_last; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
+    for (int v = wa + 1; v <= vmax; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
     return n;
 }
 
@@ -170,6 +178,7 @@ struct StackCursor {
     int il, iff, istage, itile, isi, insteps;
     WarpPlan ip;
     const uint32_t* iblob;
+    const uint32_t* isrc;  // the next step's block
     long long isw;
     uint32_t ibytes;
 };
@@ -185,20 +194,27 @@ __device__ __forceinline__ void cursor_next_layer(StackCursor& c, const RingCtx&
             c.iff = c.ip.f0;
             c.itile = c.ip.ta + c.ip.f0 / c.ip.ns;
             c.isi = c.ip.f0 % c.ip.ns;
+            c.isrc = c.iblob + ((long long)c.itile * c.insteps + c.ip.chunk0 + c.isi) * c.isw;
             return;
         }
     }
 }
+// FIXB: the stage size when every layer's is the same (uniform kernels), else 0
+template <uint32_t FIXB>
 __device__ __forceinline__ void cursor_issue(StackCursor& c, const RingCtx& rc) {  // no-op when done
     if (c.il >= rc.n_layers) return;
-    const uint32_t* src = c.iblob + ((long long)c.itile * c.insteps + c.ip.chunk0 + c.isi) * c.isw;
+    const uint32_t bytes = FIXB ? FIXB : c.ibytes, stride = FIXB ? FIXB : rc.stride;
+    const uint32_t* src = c.isrc;
     if (++c.isi == c.ip.ns) {
         c.isi = 0;
         ++c.itile;
+        c.isrc = c.iblob + ((long long)c.itile * c.insteps + c.ip.chunk0) * c.isw;
+    } else {
+        c.isrc += c.isw;
     }
     const uint32_t bar = rc.bar0 + 8 * c.istage;
-    mbar_expect_tx(bar, c.ibytes);
-    bulk_g2s(rc.ring0 + c.istage * rc.stride, src, c.ibytes, bar, rc.policy);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(rc.ring0 + c.istage * stride, src, bytes, bar, rc.policy);
     if (++c.istage == rc.D) c.istage = 0;
     if (++c.iff == c.ip.f1) cursor_next_layer(c, rc);
 }
@@ -212,13 +228,15 @@ struct StackShared {
 // One layer of the step, slice width R.  Uniform stacks instantiate k_stack
 // with R fixed; heterogeneous stacks (an EvoPress configuration: per-layer r)
 // dispatch here on the layer table's r -- the ring and cursor are shared.
-template <int R, int NT, bool CHILD>
+template <int R, int NT, bool CHILD, bool FIXED>
 __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLayer* tab, int l,
                                             StackCursor& cur, const RingCtx& rc, int& cstage,
                                             uint32_t& parity, StackShared& sh, uint8_t* smem,
                                             unsigned target) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512, kScaleBytes = 128;
+    constexpr uint32_t kStage = kScaleBytes + NPL * kSlab;
+    const uint32_t stride = FIXED ? kStage : rc.stride;
     // fp16 decode (r in {4, 8}, B <= 8): fp16's 10-bit mantissa takes a nibble at
     // offsets 0 and 4 and a whole byte at 0, cutting the decode's ALU work by
     // 15-24% (scripts/micro/decode_rate.cu); activations are staged as fp16
@@ -530,7 +548,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
         }
         mbar_wait(rc.bar0 + 8 * cstage, parity);
-        const uint32_t src = rc.ring0 + cstage * rc.stride;
+        const uint32_t src = rc.ring0 + cstage * stride;
         float sc[4];
         sc[0] = lds32f(src + g * 4);
         sc[1] = lds32f(src + (g + 8) * 4);
@@ -542,7 +560,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
         __syncwarp();
         if (lane == 0) {
             fence_proxy_async_smem();
-            cursor_issue(cur, rc);
+            cursor_issue<FIXED ? kStage : 0u>(cur, rc);
         }
         process(buf, sc, st);
         if (++cstage == D) {
@@ -565,14 +583,14 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 // through named barrier wa + 1: bar.arrive orders the slot stores and
                 // does not wait, and -- unlike a memory fence -- does not stall on
                 // lane 0's in-flight ring bulk copies
-                int wa = warp - 1;
-                while (wa > 0 && plan_f0(wp, wa) > lt * wp.ns) --wa;
+                const int wa = last_warp_at(wp, lt * wp.ns);
                 named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, (lt + 1) * wp.ns - 1)));
             } else {
                 // emitter: own part, then the later warps' parts in warp order
                 const int f_last = (lt + 1) * wp.ns - 1;
                 named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, f_last)));
-                for (int w2 = warp + 1; w2 < kStackWarps && plan_f0(wp, w2) <= f_last; ++w2) {
+                const int vmax = last_warp_at(wp, f_last);
+                for (int w2 = warp + 1; w2 <= vmax; ++w2) {
                     if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
                     const float* sp = slot_ptr(w2);
 #pragma unroll
@@ -646,21 +664,21 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     cur.il = -1;
     if (ring_warp && lane == 0) {
         cursor_next_layer(cur, rc);
-        for (int i = 0; i < D; ++i) cursor_issue(cur, rc);
+        for (int i = 0; i < D; ++i) cursor_issue<0u>(cur, rc);
     }
     int cstage = 0;
     uint32_t parity = 0;
 #pragma unroll 1
     for (int l = 0; l < p.n_layers; ++l) {
         if constexpr (RFIX != 0) {
-            stack_layer<RFIX, NT, CHILD>(p, tab, l, cur, rc, cstage, parity, sh, smem, target);
+            stack_layer<RFIX, NT, CHILD, true>(p, tab, l, cur, rc, cstage, parity, sh, smem, target);
         } else {
             switch (tab[l].r) {
-                case 2: stack_layer<2, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 3: stack_layer<3, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 4: stack_layer<4, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 6: stack_layer<6, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                default: stack_layer<8, NT, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 2: stack_layer<2, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 3: stack_layer<3, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 4: stack_layer<4, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 6: stack_layer<6, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                default: stack_layer<8, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
             }
         }
     }
