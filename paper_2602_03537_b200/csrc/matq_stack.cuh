@@ -94,13 +94,22 @@ constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp withou
 struct WarpPlan {
     int ta, ntiles, ns, chunk0, kc, f0, f1;
 };
+// a / b for 0 <= a < 2^22, 0 < b: float reciprocal + one-step correction
+// (~10 instructions; the compiler's 32/64-bit division sequences cost 20-60,
+// and these sit on every warp's per-layer path)
+__device__ __forceinline__ int udiv_small(int a, int b) {
+    int q = __float2int_rz(__int2float_rn(a) * __frcp_rn(__int2float_rn(b)));
+    q -= (q * b > a);
+    q += ((q + 1) * b <= a);
+    return q;
+}
 __device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int warp) {
     WarpPlan w{};
     if (cta >= L.cpc * L.S) return w;
-    w.kc = cta % L.S;
-    const int j = cta / L.S;
-    w.ta = (int)((long long)j * L.n_rt / L.cpc);
-    w.ntiles = (int)((long long)(j + 1) * L.n_rt / L.cpc) - w.ta;
+    const int j = udiv_small(cta, L.S);
+    w.kc = cta - j * L.S;
+    w.ta = udiv_small(j * L.n_rt, L.cpc);
+    w.ntiles = udiv_small((j + 1) * L.n_rt, L.cpc) - w.ta;
     w.chunk0 = w.kc * L.cs;
     w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
     const int P = w.ntiles * w.ns;
@@ -115,7 +124,7 @@ __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
 // floor(v P / 15) <= x, i.e. v = ceil(15 (x + 1) / P) - 1 (never an empty warp).
 __device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
     const int P = w.ntiles * w.ns;
-    return min(kStackWarps - 1, (kStackWarps * (x + 1) + P - 1) / P - 1);
+    return min(kStackWarps - 1, udiv_small(kStackWarps * (x + 1) + P - 1, P) - 1);
 }
 // Warps after wa holding a part of the tile ending at step f_last: those whose
 // range starts inside the tile and is not empty (a CTA with fewer (tile, step)
@@ -192,8 +201,9 @@ __device__ __forceinline__ void cursor_next_layer(StackCursor& c, const RingCtx&
             c.insteps = L.nsteps;
             c.ibytes = (uint32_t)L.stage_bytes;
             c.iff = c.ip.f0;
-            c.itile = c.ip.ta + c.ip.f0 / c.ip.ns;
-            c.isi = c.ip.f0 % c.ip.ns;
+            const int t0 = udiv_small(c.ip.f0, c.ip.ns);
+            c.itile = c.ip.ta + t0;
+            c.isi = c.ip.f0 - t0 * c.ip.ns;
             c.isrc = c.iblob + ((long long)c.itile * c.insteps + c.ip.chunk0 + c.isi) * c.isw;
             return;
         }
@@ -282,7 +292,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 const int idx = base_i + u * (int)blockDim.x;
                 vv[u] = make_uint4(0, 0, 0, 0);
                 if (idx < n8) {
-                    const int b = idx / c8, c = (idx - b * c8) * 8;
+                    const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                     const int col = col_base + c;
                     if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
                 }
@@ -291,7 +301,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             for (int u = 0; u < kU; ++u) {
                 const int idx = base_i + u * (int)blockDim.x;
                 if (idx >= n8) break;
-                const int b = idx / c8, c = (idx - b * c8) * 8;
+                const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                 *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
                 const uint32_t* wv = reinterpret_cast<const uint32_t*>(&vv[u]);
 #pragma unroll
@@ -310,7 +320,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
         if (threadIdx.x == 0) sh.inv_lambda = ldexpf(1.0f, e - 14);
         // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
         for (int idx = threadIdx.x; idx < n8; idx += blockDim.x) {
-            const int b = idx / c8, c = (idx - b * c8) * 8;
+            const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
             const uint4 v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
             const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
             const int cs_ = c & 255;
@@ -348,7 +358,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 const int idx = base_i + u * (int)blockDim.x;
                 vv[u] = make_uint4(0, 0, 0, 0);
                 if (idx < n8) {
-                    const int b = idx / c8, c = (idx - b * c8) * 8;
+                    const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                     const int col = col_base + c;
                     if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
                 }
@@ -357,7 +367,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             for (int u = 0; u < kU; ++u) {
                 const int idx = base_i + u * (int)blockDim.x;
                 if (idx >= n8) break;  // warp-uniform: n8 is a multiple of 32
-                const int b = idx / c8, c = (idx - b * c8) * 8;
+                const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                 const uint4 v = vv[u];
                 *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
                 if constexpr (ZP) {
@@ -535,7 +545,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // can be such a part) and raise their flag; wa adds them in warp order.
     float* slots = reinterpret_cast<float*>(smem + p.slot_off);
     auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
-    const int first_lt = wp.ns > 0 ? wp.f0 / wp.ns : 0;
+    const int first_lt = wp.ns > 0 ? udiv_small(wp.f0, wp.ns) : 0;
     int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
     const int f_end = ring_warp ? wp.f1 : wp.f0;
 #pragma unroll 1
