@@ -428,7 +428,10 @@ struct StackPlanHost {  // the opaque host plan (mq_stack_plan_bytes)
 struct StackCfg {
     int S, cs, cpc;
 };
-StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXsMaxStack) {
+// pair: CTA pairs (clusters of 2) reduce S = 2 through DSMEM for ~free; S > 2
+// still goes through the global workspace and tickets (~2 us of tail: partial
+// stores, an acq_rel ticket and the last chunk's reloads).
+StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXsMaxStack, bool pair) {
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     StackCfg best_c{nsteps, 1, std::max(1, std::min(sms / nsteps, n_rt))};
     double best = 1e30;
@@ -442,7 +445,8 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
         if (cpc < 1) break;
         const int work = mq::cdiv(n_rt, cpc) * cs;          // busiest CTA
         const double per_warp = (double)mq::cdiv(work, mq::kStackWarps);
-        const double cost = 4.0 * per_warp + (S > 1 ? 3.0 : 0.0) + (work % mq::kStackWarps ? 0.5 : 0.0);
+        const double fix = S == 1 ? 0.0 : (pair && S == 2 ? 0.5 : (pair ? 6.0 : 3.0));
+        const double cost = 4.0 * per_warp + fix + (work % mq::kStackWarps ? 0.5 : 0.0);
         if (cost < best - 1e-9) {
             best = cost;
             best_c = StackCfg{S, cs, cpc};
@@ -471,8 +475,8 @@ MQ_API int mq_debug_stack_timestamps(unsigned long long* out, int n) {
 size_t mq_stack_plan_bytes(void) { return sizeof(StackPlanHost); }
 size_t mq_stack_table_bytes(int n_layers) { return n_layers < 0 ? 0 : sizeof(mq::StackLayer) * (size_t)n_layers; }
 
-int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes, void* plan_host,
-                  void* table_host, size_t* workspace_bytes) {
+static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes,
+                           void* plan_host, void* table_host, size_t* workspace_bytes, bool pair) {
     if (!layers || !plan_host || !table_host || !workspace_bytes || n_layers < 1)
         return fail(MQ_ERR_INVALID, "null pointer or empty stack");
     if (r != 0 && !valid_r(r)) return fail(MQ_ERR_INVALID, "unsupported bits");
@@ -482,7 +486,7 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     mq::StackLayer* T = reinterpret_cast<mq::StackLayer*>(table_host);
     memset(P, 0, sizeof(*P));
     const int nt = B <= 8 ? 1 : 2;
-    int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1;
+    int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1, cl_tiles = 0, nrt_max = 1;
     bool zp_any = false, uniform = true;
     size_t partials = 0, stage_max = 0;
     // staging holds the most copies any layer stages and the ring the largest
@@ -500,11 +504,15 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
         const int npl = (nplanes == ri || ri == 8) ? ri : ri + 1;
         stage_max = std::max(stage_max, (size_t)npl * 512 + 128);
         nsteps_max = std::max(nsteps_max, mq::pad256(std::max(layers[i].K, 1)) / 256);
+        nrt_max = std::max(nrt_max, mq::pad16(std::max(layers[i].N, 1)) / 16);
     }
+    // CTA-pair reduction slots: at most ceil(n_rt / (sms / 2)) tiles per CTA
+    const int cl_max = pair ? mq::cdiv(nrt_max, std::max(1, sm_count() / 2)) : 0;
+    const size_t cl_reserve = cl_max ? (size_t)12 * cl_max + 16 + (size_t)cl_max * 32 * nt * 16 : 0;
     // everything but the activation chunk: table, partial slots, zero-point
     // constants, barriers, a 2-deep ring
     const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
-                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + mq::kStackWarps * 64 + (size_t)2 * mq::kStackWarps * stage_max + 256;
+                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 64 + (size_t)2 * mq::kStackWarps * stage_max + 256;
     const size_t xs_budget = std::min<size_t>(80 * 1024, kSmemFullSm - std::min(other, kSmemFullSm));
     for (int i = 0; i < n_layers; ++i) {
         const mq_stack_layer& in = layers[i];
@@ -520,7 +528,7 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
         uniform = uniform && ri == r_first;
         const bool child = nplanes == ri;
         const int npl = (child || ri == 8) ? ri : ri + 1;
-        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget);
+        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair);
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
         if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
         mq::StackLayer& t = T[i];
@@ -543,6 +551,7 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
         t.r = ri;
         t.stage_bytes = npl * 512 + 128;
         cs_max = std::max(cs_max, c.cs);
+        if (pair && c.S == 2) cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
         if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
     }
     mq::StackParams& p = P->p;
@@ -556,7 +565,11 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
     p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
     p.table_off = p.flag_off;
-    p.xs_bytes = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
+    p.cl_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
+    p.cluster = pair ? 1 : 0;
+    p.cl_tiles = cl_tiles;
+    const size_t cl_bytes = cl_tiles ? ((size_t)12 * cl_tiles + 15 & ~(size_t)15) + (size_t)cl_tiles * 32 * nt * 16 : 0;
+    p.xs_bytes = (int)((p.cl_off + cl_bytes + 15) & ~(size_t)15);
     const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 8;
     const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage_max));
     if (d < 2) return fail(MQ_ERR_INVALID, "stack: activation staging leaves no room for the weight ring");
@@ -571,6 +584,18 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     P->ws_bytes = stack_ws_layout(n_layers, partials, &od, &op);
     *workspace_bytes = P->ws_bytes;
     return MQ_OK;
+}
+
+int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes, void* plan_host,
+                  void* table_host, size_t* workspace_bytes) {
+    const char* env = getenv("MQ_STACK_PAIR");
+    bool pair = sm_count() % 2 == 0 && !(env && env[0] == '0');
+    int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
+    if (st || !pair) return st;
+    const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
+    if (mq::stack_pair_capacity(P->nt, P->r, P->nplanes == P->r, P->smem) >= P->grid) return MQ_OK;
+    // pairs cannot all be resident: plain CTAs, global split-K
+    return stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, false);
 }
 
 int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, size_t workspace_bytes,

@@ -55,6 +55,9 @@ struct StackParams {
     int table_off;     // byte offset of the shared-memory copy of the layer table
     int stages;        // per-warp ring depth
     int stage_stride;  // bytes per ring slot (the largest stage of the stack)
+    int cluster;       // 1: CTA pairs (cluster of 2); S == 2 layers reduce through DSMEM
+    int cl_off;        // byte offset of the pair-reduction area: [cl_tiles mbarriers][cl_tiles use counters][slots]
+    int cl_tiles;      // most row tiles a CTA holds in an S == 2 layer
     float* ws;         // split-K partials (max over layers)
     int* tickets;      // split-K tickets, self-resetting
     unsigned* done;    // [n_layers] monotone completion counters
@@ -164,6 +167,21 @@ __device__ __forceinline__ unsigned ld_acquire_cta(uint32_t saddr) {
     unsigned v;
     asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
     return v;
+}
+// ---- CTA-pair split-K (cluster of 2): chunk 1's CTA ships its finished
+// tile partial into chunk 0's shared memory with st.async, which completes
+// bytes on chunk 0's per-tile mbarrier -- no global partials, no tickets.
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float a, float b, float c, float d, uint32_t rbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(raddr), "f"(a), "f"(b), "f"(c), "f"(d), "r"(rbar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
@@ -493,8 +511,49 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
     // ticket, the last chunk to arrive summing the partials in chunk order
     const float out_scale_l = F16 ? L.out_scale * sh.inv_lambda : L.out_scale;
+    const bool pair = p.cluster && L.S == 2;
     auto emit = [&](int rt, const float (&v)[NT][4]) {
         const int r0 = rt * kTileRows + g;
+        if (pair) {
+            const int li = rt - wp.ta;
+            const uint32_t cl = smem_addr(smem + p.cl_off);
+            const uint32_t bar = cl + 8 * li;
+            const uint32_t slot = cl + ((12u * p.cl_tiles + 15u) & ~15u) + (uint32_t)((li * 32 + lane) * NT * 16);
+            if (wp.kc == 1) {  // chunk 1: ship the scaled partial to chunk 0
+                const uint32_t rbar = mapa_rank(bar, 0), rslot = mapa_rank(slot, 0);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    st_async_v4(rslot + 16 * nt, v[nt][0] * out_scale_l, v[nt][1] * out_scale_l,
+                                v[nt][2] * out_scale_l, v[nt][3] * out_scale_l, rbar);
+                return;
+            }
+            // chunk 0: arm the tile's barrier (its use count gives the phase), wait, add in chunk order
+            unsigned* uses = reinterpret_cast<unsigned*>(smem + p.cl_off + 8 * p.cl_tiles);
+            uint32_t par = 0;
+            if (lane == 0) {
+                par = uses[li] & 1u;
+                uses[li] = uses[li] + 1u;
+                mbar_expect_tx(bar, 32u * NT * 16u);
+            }
+            par = __shfl_sync(0xffffffffu, par, 0);
+            mbar_wait(bar, par);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const uint4 q = lds128(slot + 16 * nt);
+                const float pv[4] = {__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
+                                     __uint_as_float(q.w)};
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                        if (b < p.B && row < L.N)
+                            st_global_u16(L.Y + (long long)b * L.ldy + row,
+                                          f32_to_bf16_rn(v[nt][2 * h + c] * out_scale_l + pv[2 * h + c]));
+                    }
+            }
+            return;
+        }
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -667,7 +726,17 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         for (int i = 0; i < D; ++i) mbar_init(rc.bar0 + 8 * i, 1);
         fence_mbar_init();
     }
+    if (p.cluster && threadIdx.x == kSyncThread) {
+        const uint32_t cl = smem_addr(smem + p.cl_off);
+        unsigned* uses = reinterpret_cast<unsigned*>(smem + p.cl_off + 8 * p.cl_tiles);
+        for (int i = 0; i < p.cl_tiles; ++i) {
+            mbar_init(cl + 8 * i, 1);
+            uses[i] = 0u;
+        }
+        fence_mbar_init();
+    }
     __syncthreads();
+    if (p.cluster) cluster_sync_all();  // the peer's first st.async lands on initialised barriers
     const unsigned target = (sh.gen + 1u) * gridDim.x;
 
     StackCursor cur{};
@@ -698,5 +767,8 @@ template <int R>
 cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, size_t smem,
                            cudaStream_t stream);
 cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream);
+// CTAs of k_stack<nt, r, child> (r = 0: the mixed kernel) that can be co-resident as
+// clusters of 2 with `smem` bytes each, or 0 when unknown
+int stack_pair_capacity(int nt, int r, bool child, size_t smem);
 
 }  // namespace mq

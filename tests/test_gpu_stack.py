@@ -161,3 +161,23 @@ def test_llama_decoder_full_model_step(model):
     dec.decode(toks)
     torch.cuda.synchronize()
     assert not torch.equal(dec.logits, ref)
+
+
+@pytest.mark.parametrize("B", [1, 9])
+def test_stack_kernel_pair_and_global_split_k(model, B, monkeypatch):
+    """CTA pairs (clusters of 2, S = 2 reduced through DSMEM) and plain CTAs
+    (split-K through the global workspace and tickets) both match fp32 per layer."""
+    g = torch.Generator(device="cuda").manual_seed(40 + B)
+    x0 = torch.randn(B, 4096, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for pair in ("1", "0"):
+        monkeypatch.setenv("MQ_STACK_PAIR", pair)
+        stack = model.LinearStack(model.LLAMA31_8B, batch=B, n_layers=1)
+        for r in (2, 4, 8):
+            stack.capture(r, stack_kernel=True)
+            y, bufs = _step(stack, x0)
+            if torch.isfinite(y.float()).all():
+                _check_layers(stack, r, x0, y, bufs)
+            outs.append(bufs["qkv"])
+    for a, b in zip(outs[:3], outs[3:]):
+        assert rel_err(a.float().cpu().numpy(), b.float().cpu().numpy()) <= 1e-2
