@@ -574,6 +574,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage_max));
     if (d < 2) return fail(MQ_ERR_INVALID, "stack: activation staging leaves no room for the weight ring");
     p.stages = std::min(8, d);
+    if (const char* e = getenv("MQ_STACK_MAX_STAGES")) p.stages = std::max(2, std::min(p.stages, atoi(e)));  // tuning
     p.stage_stride = (int)stage_max;
     P->smem = fixed + (size_t)mq::kStackWarps * p.stages * stage_max;
     P->r = uniform ? r_first : 0;  // 0: the per-layer dispatch kernel
