@@ -1,4 +1,7 @@
 // matq_stack.cu -- K3S instantiations and cooperative launcher.
+#include <cstdio>
+#include <cstdlib>
+
 #include "matq_stack.cuh"
 
 namespace mq {
@@ -34,16 +37,21 @@ cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaSt
     attr[1].val.clusterDim.y = 1;
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = p.cluster ? 2 : 1;
-    e = cudaLaunchKernelEx(&cfg, kern, p);
-    if (e != cudaSuccess && p.cluster) {
-        // cooperative + cluster launches are not supported everywhere: the plan
-        // checked that every pair is co-resident (stack_pair_capacity)
-        (void)cudaGetLastError();
+    // CTA pairs launch as clusters without the cooperative attribute (the pair is
+    // not expressible in a cooperative launch under every tool, e.g. ncu's kernel
+    // replay); co-residency of every pair was checked by the plan
+    // (stack_pair_capacity >= grid) and the grid never exceeds one CTA per SM
+    if (p.cluster) {
         cfg.attrs = attr + 1;
         cfg.numAttrs = 1;
-        e = cudaLaunchKernelEx(&cfg, kern, p);
+    } else {
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
     }
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+    if (getenv("MQ_STACK_LAUNCH_DEBUG"))
+        fprintf(stderr, "k_stack launch cluster=%d grid=%d smem=%zu -> %s\n", p.cluster, grid, smem,
+                cudaGetErrorString(e));
     return e;
 }
 

@@ -90,10 +90,17 @@ constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp withou
 // A warp's share of one layer.  CTA c works on K chunk kc = c % S and the
 // contiguous row tiles [ta, ta + ntiles) of that chunk (near-equal split over
 // the chunk's cpc CTAs); its ntiles x ns (tile, step) pairs, flattened
-// tile-major, are split into 16 near-equal contiguous ranges [f0, f1), one per
-// warp.  A tile cut by a warp boundary is summed in warp order through
-// shared memory; a tile cut by a chunk boundary (S > 1) through the split-K
-// workspace and a ticket -- both deterministic.
+// tile-major, are split into 15 contiguous ranges [f0, f1), one per ring warp
+// (sized per SMSP, below).  A tile cut by a warp boundary is summed in warp
+// order through shared memory; a tile cut by a chunk boundary (S > 1) through
+// the CTA pair's shared memory (S = 2) or the split-K workspace and a ticket --
+// all deterministic.
+// SMSP-balanced split: warp w runs on SMSP w % 4, and SMSP 3 also hosts the
+// sync warp, so it has 3 ring warps to the others' 4.  The ALU pipe is per
+// SMSP, so each SMSP gets a quarter of the steps: warps on SMSP 3 take 4 units
+// of work, the rest 3 (U(w) = units before warp w, 48 in all).
+constexpr int kSplitUnits = 48;
+__device__ __forceinline__ int warp_units(int w) { return 3 * w + (w >> 2); }
 struct WarpPlan {
     int ta, ntiles, ns, chunk0, kc, f0, f1;
 };
@@ -116,25 +123,29 @@ __device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int 
     w.chunk0 = w.kc * L.cs;
     w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
     const int P = w.ntiles * w.ns;
-    w.f0 = warp * P / kStackWarps;
-    w.f1 = (warp + 1) * P / kStackWarps;
+    w.f0 = warp_units(warp) * P / kSplitUnits;
+    w.f1 = warp_units(warp + 1) * P / kSplitUnits;
     return w;
 }
 __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
-    return warp * (w.ntiles * w.ns) / kStackWarps;
+    return warp_units(warp) * (w.ntiles * w.ns) / kSplitUnits;
 }
 // The last warp whose range starts at or before step x: the largest v with
-// floor(v P / 15) <= x, i.e. v = ceil(15 (x + 1) / P) - 1 (never an empty warp).
+// floor(U(v) P / 48) <= x, i.e. U(v) <= umax = ceil(48 (x + 1) / P) - 1; v is
+// floor(4 umax / 13) or one more (never an empty warp).
 __device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
     const int P = w.ntiles * w.ns;
-    return min(kStackWarps - 1, udiv_small(kStackWarps * (x + 1) + P - 1, P) - 1);
+    const int umax = udiv_small(kSplitUnits * (x + 1) + P - 1, P) - 1;
+    int v = min(kStackWarps - 1, 4 * umax / 13);
+    if (v < kStackWarps - 1 && warp_units(v + 1) <= umax) ++v;
+    return v;
 }
 // Warps after wa holding a part of the tile ending at step f_last: those whose
 // range starts inside the tile and is not empty (a CTA with fewer (tile, step)
 // pairs than warps leaves some warps without work; they never arrive).
 __device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last) {
     const int vmax = last_warp_at(w, f_last);
-    if (w.ntiles * w.ns >= kStackWarps) return vmax - wa;  // no empty warps
+    if (w.ntiles * w.ns >= 16) return vmax - wa;  // every warp has >= P / 16 >= 1 steps
     int n = 0;
     for (int v = wa + 1; v <= vmax; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
     return n;
