@@ -215,6 +215,21 @@ MQ_API int mq_gptq_block(double* Wc, long long ldw, int d_row, int d_col, int lo
                          const double* lams, int T, uint8_t* codes, long long ldc, double* comp,
                          long long ldcomp, double* err, long long lde, void* stream);
 
+/* ---- full-model decode harness glue (llama.py), bf16 --
+ * Not part of the sliced linear: the row-wise steps between a Llama block's
+ * linears, fused so a block is 4 linears + 3 glue launches + attention.
+ * mq_add_rmsnorm: x += delta (when delta is non-null; x is the bf16 residual
+ *   stream), y = x * rsqrt(mean(x^2) + eps) * w (w float32), per row of h.
+ * mq_rope_kv: rotary embedding (rotate-half, cos/sin bf16 of head_dim / 2) of
+ *   the q and k heads of a fused qkv row; q -> (B, n_heads, head_dim); k and v
+ *   written into (B, n_kv_heads, T, head_dim) caches at position pos.
+ * mq_silu_mul: y = silu(g) * u for rows [g | u] of 2 * inter. */
+MQ_API int mq_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, int h, float eps,
+                          void* stream);
+MQ_API int mq_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache, void* vcache,
+                      int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos, void* stream);
+MQ_API int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -778,4 +778,27 @@ int mq_gptq_block(double* Wc, long long ldw, int d_row, int d_col, int lo, int h
                        "mq_gptq_block");
 }
 
+// ---- full-model harness glue (llama.py) ------------------------------------
+int mq_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, int h, float eps, void* stream) {
+    if (!x || !w || !y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (B < 1 || h < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_add_rmsnorm(x, delta, w, y, B, h, eps, (cudaStream_t)stream), "mq_add_rmsnorm");
+}
+
+int mq_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache, void* vcache, int B,
+               int n_heads, int n_kv_heads, int head_dim, int T, int pos, void* stream) {
+    if (!qkv || !cosv || !sinv || !q || !kcache || !vcache) return fail(MQ_ERR_INVALID, "null pointer");
+    if (B < 1 || n_heads < 1 || n_kv_heads < 1 || head_dim < 2 || (head_dim & 1) || pos < 0 || pos >= T)
+        return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_rope_kv(qkv, cosv, sinv, q, kcache, vcache, B, n_heads, n_kv_heads, head_dim, T,
+                                          pos, (cudaStream_t)stream),
+                       "mq_rope_kv");
+}
+
+int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream) {
+    if (!gu || !y) return fail(MQ_ERR_INVALID, "null pointer");
+    if (B < 1 || inter < 1) return fail(MQ_ERR_INVALID, "bad shape");
+    return cuda_status(mq::launch_silu_mul(gu, y, B, inter, (cudaStream_t)stream), "mq_silu_mul");
+}
+
 }  // extern "C"

@@ -49,6 +49,13 @@ cudaError_t launch_gptq_block(double* Wc, long long ldw, int d_row, int lo, int 
                               long long ldc, double* comp, long long ldcomp, double* err, long long lde,
                               cudaStream_t s);
 
+// full-model harness glue (matq_glue.cu), bf16
+cudaError_t launch_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, int h, float eps,
+                               cudaStream_t s);
+cudaError_t launch_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kc, void* vc, int B,
+                           int nh, int nkv, int hd, int T, int pos, cudaStream_t s);
+cudaError_t launch_silu_mul(const void* gu, void* y, int B, int inter, cudaStream_t s);
+
 struct GemmConfig {
     int bn, n_tiles, S, cs, grid;
 };

@@ -4,10 +4,14 @@ beside the paper's full-model measurement (Llama-3.1-8B-Instruct single-token
 forward: 138.0 / 124.4 / 109.3 tok/s at 2 / 3 / 4 bits on an
 RTX A6000).
 
-Everything around the hot path is plain bf16 torch and is NOT part of the
-deliverable: embedding lookup, RMSNorm, rotary embedding, a KV cache with
-grouped-query attention (torch SDPA), SiLU gating, residuals, and a bf16
-``lm_head``.  The projections (q/k/v fused, o, gate/up fused, down) are int8
+Everything around the hot path is NOT part of the deliverable: embedding
+lookup, RMSNorm, rotary embedding, a KV cache with grouped-query attention
+(torch SDPA), SiLU gating, residuals, and a bf16 ``lm_head``.  ``glue="cuda"``
+(default) runs the row-wise steps as three fused kernels from libmatq
+(residual add + RMSNorm, rotary + KV-cache write, SiLU gating: 3 launches per
+block instead of ~25 torch kernels; attention stays torch SDPA, which beat a
+simple single-query kernel here); ``glue="torch"`` is the plain-torch
+statement of the same step, which the tests compare against.  The projections (q/k/v fused, o, gate/up fused, down) are int8
 parents sliced on the fly by K3 (decode) -- per layer a bit-width, uniform or
 from an EvoPress-style config.  One decode step = one token for every sequence
 in the batch at a fixed context length, replayed as one CUDA graph.
@@ -41,8 +45,10 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
 
 class LlamaDecoder:
     def __init__(self, shape: DecoderShape = LLAMA31_8B, batch: int = 1, context: int = 256,
-                 bits=4, vocab: int = 128256, seed: int = 0, n_layers: int | None = None):
-        self.shape, self.B, self.T = shape, batch, context
+                 bits=4, vocab: int = 128256, seed: int = 0, n_layers: int | None = None, glue: str = "cuda"):
+        if glue not in ("cuda", "torch"):
+            raise ValueError("glue must be 'cuda' or 'torch'")
+        self.shape, self.B, self.T, self.glue = shape, batch, context, glue
         self.n_layers = n_layers or shape.n_layers
         dev = torch.device("cuda")
         g = torch.Generator(device="cuda").manual_seed(seed)
@@ -60,9 +66,12 @@ class LlamaDecoder:
                 blk[kind] = MatLinear(pt, 4, name="layers.%d.%s" % (i, kind))
             blk["ln1"] = torch.ones(h, device=dev)
             blk["ln2"] = torch.ones(h, device=dev)
-            # KV cache filled with random history (context positions 0..T-1)
-            blk["k"] = (torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)).to(torch.bfloat16)
-            blk["v"] = (torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)).to(torch.bfloat16)
+            # KV cache: random history at positions 0..T-1, the decoded token's k/v at T
+            blk["kc"] = torch.zeros(batch, shape.n_kv_heads, context + 1, hd, device=dev, dtype=torch.bfloat16)
+            blk["vc"] = torch.zeros_like(blk["kc"])
+            blk["kc"][:, :, :context] = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
+            blk["vc"][:, :, :context] = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
+            blk["k"], blk["v"] = blk["kc"][:, :, :context], blk["vc"][:, :, :context]
             self.blocks.append(blk)
         self.set_bits(bits)
         inv = 1.0 / (500000.0 ** (torch.arange(0, hd, 2, device=dev, dtype=torch.float32) / hd))
@@ -71,6 +80,11 @@ class LlamaDecoder:
         self.sin = ang.sin().to(torch.bfloat16)
         self.tokens = torch.zeros(batch, dtype=torch.long, device=dev)
         self.logits = torch.empty(batch, vocab, device=dev, dtype=torch.bfloat16)
+        nq = shape.n_heads * hd
+        e = lambda *sz: torch.empty(*sz, device=dev, dtype=torch.bfloat16)  # noqa: E731
+        self.buf = {"x": e(batch, h), "hn": e(batch, h), "qkv": e(batch, nq + 2 * shape.n_kv_heads * hd),
+                    "q": e(batch, shape.n_heads, 1, hd), "o": e(batch, h), "gu": e(batch, 2 * shape.intermediate),
+                    "act": e(batch, shape.intermediate), "d": e(batch, h)}
         self.stream = torch.cuda.Stream()
         self.graph = None
 
@@ -93,6 +107,42 @@ class LlamaDecoder:
         return tot
 
     def _forward(self) -> None:
+        if self.glue == "cuda":
+            self._forward_fused()
+        else:
+            self._forward_torch()
+
+    def _forward_fused(self) -> None:
+        """One decode step: 4 sliced linears (PDL-chained K3) + 3 fused glue
+        kernels (norm, rotary/KV, gating) + SDPA per block."""
+        from . import _lib
+
+        s = self.shape
+        B, hd, T = self.B, s.head_dim, self.T
+        nh, nkv, h = s.n_heads, s.n_kv_heads, s.hidden
+        b = self.buf
+        st = _lib.stream_ptr(None)
+        torch.index_select(self.embed, 0, self.tokens, out=b["x"])
+        delta = None
+        for blk in self.blocks:
+            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta) if delta is not None else None,
+                      _lib.ptr(blk["ln1"]), _lib.ptr(b["hn"]), B, h, 1e-5, st)
+            blk["qkv"].planes.linear(b["hn"], blk["qkv"].bits, out=b["qkv"], pdl=True)
+            _lib.call("mq_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin), _lib.ptr(b["q"]),
+                      _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T, st)
+            att = F.scaled_dot_product_attention(b["q"], blk["kc"], blk["vc"], enable_gqa=True)
+            blk["o"].planes.linear(att.reshape(B, nh * hd), blk["o"].bits, out=b["o"], pdl=True)
+            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(b["o"]), _lib.ptr(blk["ln2"]),
+                      _lib.ptr(b["hn"]), B, h, 1e-5, st)
+            blk["gate_up"].planes.linear(b["hn"], blk["gate_up"].bits, out=b["gu"], pdl=True)
+            _lib.call("mq_silu_mul", _lib.ptr(b["gu"]), _lib.ptr(b["act"]), B, s.intermediate, st)
+            blk["down"].planes.linear(b["act"], blk["down"].bits, out=b["d"], pdl=True)
+            delta = b["d"]
+        _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta), _lib.ptr(self.final_norm),
+                  _lib.ptr(b["hn"]), B, h, 1e-5, st)
+        torch.matmul(b["hn"], self.lm_head.t(), out=self.logits)
+
+    def _forward_torch(self) -> None:
         s = self.shape
         B, hd = self.B, s.head_dim
         nh, nkv = s.n_heads, s.n_kv_heads
