@@ -188,15 +188,16 @@ class LinearStack:
         return out
 
     def stack_kernel_ok(self, config) -> bool:
-        """Where the persistent K3S path is the default: single-GPU fused stacks,
-        B <= 16, uniform r (1.00-1.11x the per-layer K3 graph, scripts/
-        stack_matrix.py).  Heterogeneous parents also run on it (stack_kernel=
-        True: one kernel dispatching per layer on its r) but measure at par
-        with the K3 graph fused and 0.75x unfused (224 layers, many small:
-        the grid-wide layer barrier costs more than PDL's overlap), so the
-        graph stays their default."""
+        """Where the persistent K3S path is the default (single GPU, B <= 16,
+        G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix.txt):
+        uniform stacks, fused or unfused (1.12-1.19x the per-layer K3 graph),
+        and heterogeneous fused stacks (1.10x; one kernel dispatching each layer
+        on its r).  Heterogeneous unfused stacks (224 linears, many of them
+        small) measure at par with the graph (0.99x), which stays their default;
+        stack_kernel=True forces K3S."""
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
-        return (len(rs) == 1 and self.fused and self.tp == 1 and self.B <= 16 and self.G == 128)
+        parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
+        return ((len(rs) == 1 or (self.fused and parents)) and self.tp == 1 and self.B <= 16 and self.G == 128)
 
     def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None) -> None:
         """(Re)capture the decode step for a per-layer bit-width config.

@@ -83,10 +83,15 @@ def test_configs_default_to_stack_kernel(model):
     stack.capture(3)
     assert stack.program is not None
     cfg = {n: (2 if i % 2 else 4) for i, n in enumerate(stack.names)}
-    stack.capture(cfg)  # heterogeneous: the per-layer K3 graph by default
-    assert stack.program is None and stack.launches_per_step() == len(stack.names)
-    stack.capture(cfg, stack_kernel=True)  # or the per-layer dispatch kernel
+    stack.capture(cfg)  # heterogeneous fused: the per-layer dispatch kernel
     assert stack.program is not None and stack.launches_per_step() == 1
+    stack.capture(cfg, stack_kernel=False)  # or the per-layer K3 graph
+    assert stack.program is None and stack.launches_per_step() == len(stack.names)
+    un = model.LinearStack(model.LLAMA31_8B, batch=2, n_layers=1, fused=False)
+    un.capture({n: (2 if i % 2 else 4) for i, n in enumerate(un.names)})  # heterogeneous unfused: graph
+    assert un.program is None
+    un.capture(3)  # uniform unfused: K3S
+    assert un.program is not None
 
 
 def _check_mixed(stack, cfg, x0, y, bufs, tol=1e-2):
