@@ -501,8 +501,10 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         nstage_max = std::max(nstage_max, f16 ? ncopy + 1 : ncopy);
         // k_stack's ZP rule (r = 6: one copy, constants still needed)
         zp_any = zp_any || f16 || (ri != 8 && nt == 1);
-        const int npl = (nplanes == ri || ri == 8) ? ri : ri + 1;
-        stage_max = std::max(stage_max, (size_t)npl * 512 + 128);
+        // budget the ring as if for a parent slice (r + 1 planes) even for children,
+        // so a child stack gets its parent's decomposition (same summation order)
+        const int npl_budget = ri == 8 ? 8 : ri + 1;
+        stage_max = std::max(stage_max, (size_t)npl_budget * 512 + 128);
         nsteps_max = std::max(nsteps_max, mq::pad256(std::max(layers[i].K, 1)) / 256);
         nrt_max = std::max(nrt_max, mq::pad16(std::max(layers[i].N, 1)) / 16);
     }
@@ -513,7 +515,12 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     // constants, barriers, a 2-deep ring
     const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
                          (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 64 + (size_t)2 * mq::kStackWarps * stage_max + 256;
-    const size_t xs_budget = std::min<size_t>(80 * 1024, kSmemFullSm - std::min(other, kSmemFullSm));
+    // the activation chunk's cap: 80 KB keeps B <= 4 stacks on the measured-best
+    // decompositions; B >= 5 would otherwise split K > 2 ways (global split-K
+    // tails) -- the ring needs only 2 stages (scripts/sweep_stages.sh), so give
+    // staging the rest (B = 8, r = 4: 3.17 -> 2.04 ms/step)
+    const size_t xs_cap = B <= 4 ? (size_t)80 * 1024 : (size_t)192 * 1024;
+    const size_t xs_budget = std::min<size_t>(xs_cap, kSmemFullSm - std::min(other, kSmemFullSm));
     for (int i = 0; i < n_layers; ++i) {
         const mq_stack_layer& in = layers[i];
         const int ri = r ? r : in.r;

@@ -754,7 +754,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     cur.il = -1;
     if (ring_warp && lane == 0) {
         cursor_next_layer(cur, rc);
-        for (int i = 0; i < D; ++i) cursor_issue<0u>(cur, rc);
+        // the same slot stride the consumer uses: the stage size in uniform kernels
+        constexpr uint32_t kFix = RFIX ? 128u + 512u * PlaneCount<RFIX ? RFIX : 2, CHILD>::value : 0u;
+        for (int i = 0; i < D; ++i) cursor_issue<kFix>(cur, rc);
     }
     int cstage = 0;
     uint32_t parity = 0;
