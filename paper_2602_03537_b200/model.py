@@ -189,15 +189,21 @@ class LinearStack:
 
     def stack_kernel_ok(self, config) -> bool:
         """Where the persistent K3S path is the default (single GPU, B <= 16,
-        G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix.txt):
-        uniform stacks, fused or unfused (1.12-1.19x the per-layer K3 graph),
-        and heterogeneous fused stacks (1.10x; one kernel dispatching each layer
-        on its r).  Heterogeneous unfused stacks (224 linears, many of them
-        small) measure at par with the graph (0.99x), which stays their default;
-        stack_kernel=True forces K3S."""
+        G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix*.txt):
+        * uniform r: at B <= 4 always (1.12-1.19x the per-layer K3 graph at
+          B = 1, fused or unfused); at B = 8-16 for r <= 4 (up to 1.7x) -- for
+          r >= 6 the graph wins there (r = 8: 0.87x at B = 8, 0.67x at B = 16);
+        * heterogeneous (per-layer r, parents): fused stacks at B <= 4 (1.10x at
+          B = 1).  Unfused ones (224 linears, the k/v ones only 1024 rows)
+          measure at par at B = 1 and the graph wins at larger B.
+        stack_kernel=True / False forces either path."""
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
-        return ((len(rs) == 1 or (self.fused and parents)) and self.tp == 1 and self.B <= 16 and self.G == 128)
+        if len(rs) == 1:
+            ok = self.B <= 4 or max(rs) <= 4
+        else:
+            ok = self.fused and parents and self.B <= 4
+        return (ok and self.tp == 1 and self.B <= 16 and self.G == 128)
 
     def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None) -> None:
         """(Re)capture the decode step for a per-layer bit-width config.
