@@ -52,6 +52,7 @@ struct GemvConfig {
     int slots;  // partial-sum slots per row tile (= S)
     size_t smem;
     int xs_stride, xs_bytes, xcopy_stride, cs_off;
+    int pair, pair_units, pair_off;  // S == 2 on CTA pairs (DSMEM reduction)
 };
 
 constexpr size_t kXsMax = 48 * 1024;        // activations staged per CTA (chunked mode)
@@ -85,6 +86,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     c.nwarps &= ~3;
     const int force_s = honour_overrides ? env_int("MQ_GEMV_SPLIT", 0) : 0;
     const double fixup = 2.0;  // measured: a split-K tile costs ~2 steps (partials, ticket, reduction)
+    // CTA pairs (clusters of 2) reduce S = 2 through DSMEM for ~nothing (MQ_GEMV_PAIR=0: off)
+    const bool pair_ok = env_int("MQ_GEMV_PAIR", 1) != 0 && sm_count() % 2 == 0;
     const int sms = sm_count();
     double best = 1e30;
     for (int S_try = 1; S_try <= std::min(nsteps, 64); ++S_try) {
@@ -108,7 +111,8 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
             const int first = w * cpc;
             if (first < n_rt) max_units += (n_rt - 1 - first) / rt_stride + 1;
         }
-        const double cost = (double)max_units * (cs + (S > 1 ? fixup : 0.0));
+        const double fix = S == 1 ? 0.0 : (pair_ok && S == 2 ? 0.3 : fixup);
+        const double cost = (double)max_units * (cs + fix);
         if (cost < best - 1e-9) {
             best = cost;
             c.S = S;
@@ -127,6 +131,15 @@ GemvConfig choose_gemv_config(int N, int K, int Bx, int npl, bool g128, int r,
     const bool zp = g128 && r != 8 && c.NT == 1;
     const size_t zc_bytes = zp ? (size_t)2 * c.cs * c.NT * 8 * 4 : 0;
     c.xs_bytes = (int)((c.cs_off + zc_bytes + 15) & ~(size_t)15);
+    c.pair = pair_ok && c.S == 2 && c.grid % 2 == 0;
+    if (c.pair) {
+        const int rt_stride = (c.grid / c.S) * c.nwarps;
+        c.pair_units = mq::cdiv(n_rt, rt_stride);
+        c.pair_off = c.xs_bytes;
+        const size_t pb = (((size_t)8 * mq::kMaxWarps * c.pair_units + 15) & ~(size_t)15) +
+                          (size_t)mq::kMaxWarps * c.pair_units * 32 * c.NT * 16;
+        c.xs_bytes = (int)((c.pair_off + pb + 15) & ~(size_t)15);
+    }
     const size_t stage = (size_t)npl * 512 + (g128 ? 128 : 0);
     const size_t fixed = (size_t)c.xs_bytes + mq::kMaxWarps * 8 * 8;
     int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (c.nwarps * stage));
@@ -158,7 +171,7 @@ GemvConfig cached_config(int N, int K, int Bx, int npl, bool g128, int r) {
     static std::mutex mu;
     static std::map<CfgKey, GemvConfig> cache;
     const CfgKey key{N, K, Bx, npl, (int)g128, r, env_int("MQ_GEMV_WARPS", 0), env_int("MQ_GEMV_SPLIT", 0),
-                     env_int("MQ_GEMV_STAGES", 0), 0};
+                     env_int("MQ_GEMV_STAGES", 0), env_int("MQ_GEMV_PAIR", 1)};
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
@@ -367,6 +380,9 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
     p.cs_off = c.cs_off;
     p.xs_bytes = c.xs_bytes;
     p.stages = c.stages;
+    p.pair = c.pair;
+    p.pair_off = c.pair_off;
+    p.pair_units = c.pair_units;
 #ifdef MQ_GEMV_TIMING
     static int dbg_ctr = 0;
     p.dbg_slot = dbg_ctr++ % mq::kTsSlots;

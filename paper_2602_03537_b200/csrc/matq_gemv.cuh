@@ -68,6 +68,9 @@ struct GemvParams {
     int cs_off;               // smem byte offset of the per-group zero-point constants
     int xs_bytes;             // smem bytes of the X staging area (16-aligned)
     int stages;               // per-warp TMA ring depth (<= 8)
+    int pair;                 // S == 2 on CTA pairs (clusters of 2): chunk 1 ships partials by st.async
+    int pair_off;             // smem byte offset of [warps x pair_units mbarriers][slots]
+    int pair_units;           // most row tiles a warp holds
     int dbg_slot;             // MQ_GEMV_TIMING builds: timestamp slot of this launch
     unsigned long long* dbg_ts;
 };
@@ -207,7 +210,13 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
             put(2 * b + 1, c, lo);
         }
     }
+    if (p.pair && lane == 0) {  // chunk 0's per-(warp, unit) barriers (used once per launch)
+        const uint32_t pb = smem_addr(smem + p.pair_off);
+        for (int u = 0; u < p.pair_units; ++u) mbar_init(pb + 8 * (warp * p.pair_units + u), 1);
+        fence_mbar_init();
+    }
     __syncthreads();
+    if (p.pair) cluster_sync_all();  // the peer's st.async lands on initialised barriers
     MQ_TS(2);
 
     // ldmatrix row addresses: matrix mi = lane >> 3 covers k offset 8*mi of a
@@ -378,6 +387,7 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
         else
             reinterpret_cast<uint16_t*>(p.Y)[(long long)b * p.ldy + row] = f32_to_bf16_rn(v);
     };
+    int unit_idx = 0;  // this warp's finished tiles (pair slot index)
     auto finalize = [&](int rt) {
         MQ_TS_MAX(5);
         if constexpr (GS == 0) flush_generic();
@@ -411,6 +421,38 @@ __global__ void __launch_bounds__(NT >= 4 ? 256 : kMaxWarps * 32, 1) k_gemv(cons
                         const int row = r0 + 8 * h, b = bcol[nt][c];
                         if (b < p.B && row < p.N) store_y(b, row, v[nt][h][c]);
                     }
+            return;
+        }
+        if (p.pair) {
+            // chunk 1 ships its partial into chunk 0's slot; chunk 0 adds it (chunk order)
+            const int ui = unit_idx++;
+            const uint32_t pb = smem_addr(smem + p.pair_off);
+            const uint32_t bar = pb + 8 * (warp * p.pair_units + ui);
+            const uint32_t slot = pb + ((8u * (uint32_t)(kMaxWarps * p.pair_units) + 15u) & ~15u) +
+                                  (uint32_t)(((warp * p.pair_units + ui) * 32 + lane) * NT * 16);
+            if (kc == 1) {
+                const uint32_t rbar = mapa_rank(bar, 0), rslot = mapa_rank(slot, 0);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    st_async_v4(rslot + 16 * nt, v[nt][0][0], v[nt][0][1], v[nt][1][0], v[nt][1][1], rbar);
+                return;
+            }
+            if (lane == 0) mbar_expect_tx(bar, 32u * NT * 16u);
+            __syncwarp();
+            mbar_wait(bar, 0);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const uint4 q = lds128(slot + 16 * nt);
+                const float pv[2][2] = {{__uint_as_float(q.x), __uint_as_float(q.y)},
+                                        {__uint_as_float(q.z), __uint_as_float(q.w)}};
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const int row = r0 + 8 * h, b = bcol[nt][c];
+                        if (b < p.B && row < p.N) store_y(b, row, v[nt][h][c] + pv[h][c]);
+                    }
+            }
             return;
         }
 #pragma unroll

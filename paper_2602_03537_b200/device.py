@@ -71,7 +71,7 @@ _WS_NEED: dict[tuple[int, int, int, int], int] = {}
 def _tuning_env() -> tuple:
     e = os.environ
     return (e.get("MQ_GEMV_SPLIT"), e.get("MQ_GEMV_WARPS"), e.get("MQ_GEMV_STAGES"),
-            e.get("MQ_GEMV_STREAM"))
+            e.get("MQ_GEMV_STREAM"), e.get("MQ_GEMV_PAIR"))
 
 
 def gemv_workspace_bytes(N: int, K: int, B: int, flags: int) -> int:
