@@ -84,6 +84,10 @@ __device__ __forceinline__ unsigned long long stack_gtimer() {
 #define MQ_STS(l, ev) do { } while (0)
 #endif
 
+#ifndef MQ_STACK_SPIN_NS
+#define MQ_STACK_SPIN_NS 0
+#endif
+
 constexpr int kStackWarps = 15;                      // ring (work) warps
 constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp without a ring
 
@@ -285,6 +289,9 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     MQ_STS(l, 0);
     if (l > 0 && threadIdx.x == kSyncThread) {
         while (ld_acquire_u32(p.done + l - 1) < target) {
+#if MQ_STACK_SPIN_NS
+            __nanosleep(MQ_STACK_SPIN_NS);  // fewer polls on the counter line while CTAs publish
+#endif
         }
     }
     __syncthreads();
