@@ -75,12 +75,8 @@ __device__ __forceinline__ unsigned long long stack_gtimer() {
     p.dbg_ts[((size_t)(l) * 148 + blockIdx.x) * 8 + (ev)] = stack_gtimer(); } while (0)
 #define MQ_STS_WMAX(l, ev) do { if ((threadIdx.x & 31) == 0 && p.dbg_ts && blockIdx.x < 148) \
     atomicMax(&p.dbg_ts[((size_t)(l) * 148 + blockIdx.x) * 8 + (ev)], stack_gtimer()); } while (0)
-// per-warp stamps of CTA 0: [256 layers][16 warps][4]
-#define MQ_STS_W0(l, ev) do { if ((threadIdx.x & 31) == 0 && p.dbg_ts && blockIdx.x == 0) \
-    p.dbg_ts[256 * 148 * 8 + ((size_t)(l) * 16 + (threadIdx.x >> 5)) * 4 + (ev)] = stack_gtimer(); } while (0)
 #else
 #define MQ_STS_WMAX(l, ev) do { } while (0)
-#define MQ_STS_W0(l, ev) do { } while (0)
 #define MQ_STS(l, ev) do { } while (0)
 #endif
 

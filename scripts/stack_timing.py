@@ -29,14 +29,7 @@ torch.cuda.synchronize()
 print("step %.1f us (%d layers)" % (e0.elapsed_time(e1) * 1e3, 4 * nl))
 buf = np.zeros(256 * 148 * 8 + 256 * 16 * 4, dtype=np.uint64)
 assert L.mq_debug_stack_timestamps(buf.ctypes.data, buf.size) == 0
-pw = buf[256 * 148 * 8:].reshape(256, 16, 4).astype(np.float64)
 ts = buf[: 256 * 148 * 8].reshape(256, 148, 8).astype(np.float64)[: 4 * nl]
-for l in (5, 7):
-    t00 = ts[l, 0, 2]
-    print("CTA 0 layer %d (%s): per warp [first step, last step|emitter wait start, contributor arrive|emit start, emit end] us after staging" % (l, ["qkv", "o", "gate_up", "down"][l % 4]))
-    for w in range(15):
-        v = pw[l, w]
-        print("   w%2d " % w + " ".join("%6.2f" % ((x - t00) / 1e3) if x > 0 else "   -  " for x in v))
 # ev5 is an atomicMax over warps (0 when a CTA had no work for the layer): fall back to ev4
 ts[:, :, 5] = np.where(ts[:, :, 5] > 0, ts[:, :, 5], ts[:, :, 4])
 t0 = ts[0, :, 0].min()
