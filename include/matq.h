@@ -160,6 +160,12 @@ MQ_API int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int 
                          void* plan_host, void* table_host, size_t* workspace_bytes);
 MQ_API int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace,
                         size_t workspace_bytes, void* stream);
+/* The persistent kernel's step counter (64-bit; launch_ctr = launches * grid,
+ * every layer's completion counter equal to it between steps).  set = 1 writes
+ * *launches, set = 0 reads it (MQ_ERR_INVALID if the counters disagree).
+ * Synchronous.  For tests and long-running servers that want to re-base it. */
+MQ_API int mq_stack_epoch(const void* plan_host, void* workspace, size_t workspace_bytes,
+                          unsigned long long* launches, int set, void* stream);
 
 /* ---- format-layer helpers behind the drop-in Python API --------------- */
 
@@ -205,6 +211,16 @@ MQ_API int mq_select_codes(const double* W, long long ldw, int d_row, int d_col,
  * (d_row, ceil(d_col / G)). */
 MQ_API int mq_fit_grid(const double* W, long long ldw, int d_row, int d_col, int G, const int* targets,
                        const double* lams, int T, const double* alphas, int steps, float* scales, void* stream);
+
+/* rtn (grid.py:114-125): codes[i] = clip(round_half_away(w[i] / scale[i] +
+ * 2^(c-1)), 0, 2^c - 1) as int64 over n broadcast elements (the caller
+ * broadcasts w and scale); MQ_ERR_CODE_RANGE with "non-finite weight" when any
+ * w is not finite.  Synchronises the stream (the error flag is read back). */
+MQ_API int mq_rtn_f64(const double* w, const double* scale, long long n, int c, long long* codes, int* err_dev,
+                      void* stream);
+/* round_half_away (grid.py:108-111): nearest integer, halves away from zero,
+ * float64 -> float64.  Asynchronous. */
+MQ_API int mq_round_half_away_f64(const double* x, long long n, double* out, void* stream);
 
 /* One column block [lo, hi) of quantize_layer's loop (gptq.py:203-222):
  * codes[:, lo:hi], the compensated snapshot comp[:, lo:hi], the scaled errors

@@ -11,7 +11,10 @@ C ABI, include/matq.h); there is no CPU fallback.
 
 from . import _lib  # noqa: F401  (fails loudly if libmatq.so is missing)
 from .device import PlaneTensor, StackProgram, algorithmic_bytes, reserve_workspace
-from .grid import BitWidthSet, GridError, QuantGrid, base_scale, dequant, dequant_value, fit_grid
+from .checkpoint import Checkpoint, CheckpointError, SlicedModel, read_checkpoint, write_checkpoint
+from .config import mutate_level_switch
+from .grid import (BitWidthSet, GridError, QuantGrid, base_scale, dequant, dequant_value, fit_grid, round_half_away,
+                   rtn)
 from .gptq import (CalibBatch, HessianFactor, QuantizeError, build_hessian, factor_inverse, quantize_layer,
                    select_codes)
 from .matmul import (MatmulError, MatmulTask, PackedLayer, bench, matmul_packed,

@@ -60,6 +60,7 @@ _SIGS = {
     "mq_stack_table_bytes": ([_i], _sz),
     "mq_stack_plan": ([_vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_stack_run": ([_vp, _vp, _vp, _sz, _vp], _i),
+    "mq_stack_epoch": ([_vp, _vp, _sz, _vp, _i, _vp], _i),
     "mq_slice_elementwise": ([_vp, _ll, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_f64": ([_vp, _i, _i, _vp, _i, _i, _i, _i, _vp, _vp, _vp], _i),
     "mq_dequant_value_f64": ([_vp, _vp, _ll, _i, _i, _vp, _vp, _vp], _i),
@@ -67,6 +68,8 @@ _SIGS = {
     "mq_pack_ref_layout": ([_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp], _i),
     "mq_unpack_ref_layout": ([_vp, _vp, _vp, _i, _i, _vp, _vp], _i),
     "mq_select_codes": ([_vp, _ll, _i, _i, _vp, _i, _i, _vp, _vp, _i, _vp, _ll, _vp], _i),
+    "mq_rtn_f64": ([_vp, _vp, _ll, _i, _vp, _vp, _vp], _i),
+    "mq_round_half_away_f64": ([_vp, _ll, _vp, _vp], _i),
     "mq_fit_grid": ([_vp, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp, _vp], _i),
     "mq_add_rmsnorm": ([_vp, _vp, _vp, _vp, _i, _i, _f, _vp], _i),
     "mq_rope_kv": ([_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp], _i),
@@ -78,6 +81,8 @@ _SIGS = {
 EXPORTS = tuple(_SIGS)
 
 for _name, (_args, _res) in _SIGS.items():
+    if os.environ.get("MQ_LIB_PATH") and not hasattr(_L, _name):
+        continue  # an older tuning build (MQ_LIB_PATH) may predate an entry point
     _fn = getattr(_L, _name)
     _fn.argtypes = _args
     _fn.restype = _res

@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <vector>
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -472,10 +473,29 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
 }
 
 size_t stack_ws_layout(int n_layers, size_t partial_bytes, size_t* off_done, size_t* off_partials) {
-    // [tickets 64 KB][done counters n + launch counter][partials]
+    // [tickets 64 KB][done counters n + launch counter][published max |y| n][partials]
     *off_done = kTicketBytes;
-    *off_partials = kTicketBytes + (((size_t)(n_layers + 1) * 4 + 255) & ~(size_t)255);
+    *off_partials = kTicketBytes + (((size_t)(2 * n_layers + 1) * 8 + 255) & ~(size_t)255);
     return *off_partials + partial_bytes;
+}
+
+// fp16 staging in one pass: layer i's X must lie entirely inside the output of
+// an earlier layer j (same row stride, every row's columns within j's N) that
+// no layer between j and i overwrote in part -- then j's published max |y|
+// bounds max |x|.  Returns j or -1.
+int stack_amax_src(const mq_stack_layer* layers, int i, int B) {
+    const mq_stack_layer& in = layers[i];
+    auto lo = [](const void* p) { return reinterpret_cast<uintptr_t>(p); };
+    const uintptr_t x0 = lo(in.X), x1 = x0 + 2 * ((size_t)(B - 1) * in.ldx + in.K);
+    for (int j = i - 1; j >= 0; --j) {
+        const mq_stack_layer& o = layers[j];
+        const uintptr_t y0 = lo(o.Y), y1 = y0 + 2 * ((size_t)(B - 1) * o.ldy + o.N);
+        if (x1 <= y0 || y1 <= x0) continue;  // no overlap: look further back
+        const size_t e = (x0 - y0) / 2;  // X's first element inside Y (row 0: both have B rows)
+        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 2 == 0 && e + (size_t)in.K <= (size_t)o.N;
+        return inside ? j : -1;  // the latest writer overlapping X decides
+    }
+    return -1;
 }
 }  // namespace
 
@@ -530,7 +550,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     // everything but the activation chunk: table, partial slots, zero-point
     // constants, barriers, a 2-deep ring
     const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
-                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 64 + (size_t)2 * mq::kStackWarps * stage_max + 256;
+                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 128 + (size_t)2 * mq::kStackWarps * stage_max + 256;
     // the activation chunk's cap: 80 KB keeps B <= 4 stacks on the measured-best
     // decompositions; B >= 5 would otherwise split K > 2 ways (global split-K
     // tails) -- the ring needs only 2 stages (scripts/sweep_stages.sh), so give
@@ -573,6 +593,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         t.out_scale = in.out_scale;
         t.r = ri;
         t.stage_bytes = npl * 512 + 128;
+        t.amax_src = (ri == 4 || ri == 8) && nt == 1 ? stack_amax_src(layers, i, B) : -1;
+        if (t.amax_src >= 0) T[t.amax_src].pub_amax = 1;
         cs_max = std::max(cs_max, c.cs);
         if (pair && c.S == 2) cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
         if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
@@ -593,7 +615,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     p.cl_tiles = cl_tiles;
     const size_t cl_bytes = cl_tiles ? ((size_t)12 * cl_tiles + 15 & ~(size_t)15) + (size_t)cl_tiles * 32 * nt * 16 : 0;
     p.xs_bytes = (int)((p.cl_off + cl_bytes + 15) & ~(size_t)15);
-    const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 8;
+    const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 16;  // full + empty barriers
     const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage_max));
     if (d < 2) return fail(MQ_ERR_INVALID, "stack: activation staging leaves no room for the weight ring");
     p.stages = std::min(8, d);
@@ -617,9 +639,17 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
     if (st || !pair) return st;
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
-    if (mq::stack_pair_capacity(P->nt, P->r, P->nplanes == P->r, P->smem) >= P->grid) return MQ_OK;
-    // pairs cannot all be resident: plain CTAs, global split-K
-    return stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, false);
+    if (mq::stack_pair_capacity(P->nt, P->r, P->nplanes == P->r, P->smem) >= P->grid &&
+        mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, true) == cudaSuccess)
+        return MQ_OK;
+    // pairs cannot all be resident (or the driver rejects a cooperative cluster
+    // launch): plain cooperative CTAs, global split-K
+    st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, false);
+    if (st) return st;
+    if (mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, false) != cudaSuccess)
+        return fail(MQ_ERR_CUDA, "mq_stack_plan: the persistent kernel cannot be launched cooperatively "
+                                 "(%d CTAs, %zu B shared memory)", P->grid, P->smem);
+    return MQ_OK;
 }
 
 int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, size_t workspace_bytes,
@@ -634,8 +664,9 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
     char* w = reinterpret_cast<char*>(workspace);
     p.layers = reinterpret_cast<const mq::StackLayer*>(table_dev);
     p.tickets = reinterpret_cast<int*>(w);
-    p.done = reinterpret_cast<unsigned*>(w + od);
+    p.done = reinterpret_cast<unsigned long long*>(w + od);
     p.launch_ctr = p.done + p.n_layers;
+    p.amax = p.launch_ctr + 1;
     p.ws = reinterpret_cast<float*>(w + op);
 #ifdef MQ_GEMV_TIMING
     static unsigned long long* sbuf = nullptr;
@@ -654,6 +685,39 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
         default: e = mq::launch_stack_r<8>(p, P->nt, child, P->grid, P->smem, (cudaStream_t)stream); break;
     }
     return cuda_status(e, "mq_stack_run");
+}
+
+// The step counter behind the layer barriers: launch_ctr = launches * grid and
+// every done[l] = launches * grid between steps.  set = 1 writes `*launches`
+// (tests seed it near 2^32 to show the 64-bit counters do not wrap), set = 0
+// reads it back.  Synchronous.
+int mq_stack_epoch(const void* plan_host, void* workspace, size_t workspace_bytes, unsigned long long* launches,
+                   int set, void* stream) {
+    if (!plan_host || !workspace || !launches) return fail(MQ_ERR_INVALID, "null pointer");
+    const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
+    if (workspace_bytes < P->ws_bytes)
+        return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
+    size_t od, op;
+    stack_ws_layout(P->p.n_layers, 0, &od, &op);
+    unsigned long long* ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(workspace) + od);
+    const int n = P->p.n_layers + 1;
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<unsigned long long> h((size_t)n);
+    cudaError_t e;
+    if (set) {
+        for (auto& v : h) v = *launches * (unsigned long long)P->grid;
+        e = cudaMemcpyAsync(ctr, h.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        return cuda_status(e, "mq_stack_epoch");
+    }
+    e = cudaMemcpyAsync(h.data(), ctr, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_stack_epoch");
+    for (int i = 0; i < n; ++i)
+        if (h[i] != h[0] || h[i] % (unsigned long long)P->grid)
+            return fail(MQ_ERR_INVALID, "stack counters inconsistent (layer %d: %llu vs %llu)", i, h[i], h[0]);
+    *launches = h[0] / (unsigned long long)P->grid;
+    return MQ_OK;
 }
 
 static int sync_and_check(cudaError_t launch, int* err_dev, cudaStream_t s, const char* where,
@@ -784,6 +848,25 @@ int mq_fit_grid(const double* W, long long ldw, int d_row, int d_col, int G, con
     return cuda_status(mq::launch_fit_grid(W, ldw, d_row, d_col, G, tg, alphas, steps, scales, ngs,
                                            (cudaStream_t)stream),
                        "mq_fit_grid");
+}
+
+int mq_rtn_f64(const double* w, const double* scale, long long n, int c, long long* codes, int* err_dev,
+               void* stream) {
+    if (c < 2 || c > 8) return fail(MQ_ERR_INVALID, "bit-width must lie in [2, 8]");
+    if (n < 0 || (n > 0 && (!w || !scale || !codes || !err_dev))) return fail(MQ_ERR_INVALID, "null pointer");
+    if (n == 0) return MQ_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(err_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return cuda_status(e, "mq_rtn_f64");
+    return sync_and_check(mq::launch_rtn(w, scale, n, c, 1, nullptr, codes, err_dev, s), err_dev, s, "mq_rtn_f64",
+                          "non-finite weight");
+}
+
+int mq_round_half_away_f64(const double* x, long long n, double* out, void* stream) {
+    if (n < 0 || (n > 0 && (!x || !out))) return fail(MQ_ERR_INVALID, "null pointer");
+    if (n == 0) return MQ_OK;
+    return cuda_status(mq::launch_rtn(x, nullptr, n, 2, 0, out, nullptr, nullptr, (cudaStream_t)stream),
+                       "mq_round_half_away_f64");
 }
 
 int mq_gptq_block(double* Wc, long long ldw, int d_row, int d_col, int lo, int hi, const float* scales, int ngs,

@@ -48,6 +48,8 @@ cudaError_t launch_gptq_block(double* Wc, long long ldw, int d_row, int lo, int 
                               int G, const double* chol, long long ldch, const QuantTargets& tg, uint8_t* codes,
                               long long ldc, double* comp, long long ldcomp, double* err, long long lde,
                               cudaStream_t s);
+cudaError_t launch_rtn(const double* w, const double* s, long long n, int c, int mode, double* out_f,
+                       long long* out_q, int* err, cudaStream_t st);
 
 // full-model harness glue (matq_glue.cu), bf16
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, int h, float eps,

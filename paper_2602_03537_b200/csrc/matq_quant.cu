@@ -23,6 +23,7 @@
 // (grid.py:150-157 via slicing.py:31-54), built per CTA in shared memory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "matq_internal.h"
@@ -253,6 +254,35 @@ int quant_grid(long long units, int wpb) {
     return (int)(want < cap ? (want > 0 ? want : 1) : cap);
 }
 
+// rtn / round_half_away (grid.py:108-125), elementwise over broadcast operands:
+// x = w / s + z (two correctly rounded float64 ops, as numpy), halves away from
+// zero, clipped to [0, 2^c - 1] (mode 1) or just rounded (mode 0, round_half_away
+// of w itself).  A non-finite w raises flag 1 (rtn's "non-finite weight").
+__global__ void k_rtn(const double* __restrict__ w, const double* __restrict__ s, long long n, int c, int mode,
+                      double* __restrict__ out_f, long long* __restrict__ out_q, int* __restrict__ err) {
+    const double z = (double)(1 << (c - 1)), qmax = (double)((1 << c) - 1);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double wi = w[i];
+        if (mode == 0) {
+            out_f[i] = wi >= 0.0 ? floor(__dadd_rn(wi, 0.5)) : ceil(__dsub_rn(wi, 0.5));
+            continue;
+        }
+        if (!isfinite(wi)) {
+            atomicExch(err, 1);
+            out_q[i] = 0;
+            continue;
+        }
+        const double x = __dadd_rn(__ddiv_rn(wi, s[i]), z);
+        double q = x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5));
+        q = q < 0.0 ? 0.0 : (q > qmax ? qmax : q);  // NaN (0/0 scale) stays NaN -> flag below
+        if (q != q) {
+            atomicExch(err, 1);
+            q = 0.0;
+        }
+        out_q[i] = (long long)q;
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_select_codes(const double* W, long long ldw, int d_row, int d_col, const float* scales,
@@ -288,6 +318,14 @@ cudaError_t launch_gptq_block(double* Wc, long long ldw, int d_row, int lo, int 
     const size_t sm = sizeof(double) * tg.T * ((size_t)1 << tg.c);
     k_gptq_block<<<quant_grid(d_row, 4), 128, sm, s>>>(Wc, ldw, d_row, lo, hi, scales, ngs, G, chol, ldch, tg,
                                                      codes, ldc, comp, ldcomp, err, lde);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rtn(const double* w, const double* s, long long n, int c, int mode, double* out_f,
+                       long long* out_q, int* err, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 16);
+    k_rtn<<<grid, 256, 0, st>>>(w, s, n, c, mode, out_f, out_q, err);
     return cudaGetLastError();
 }
 

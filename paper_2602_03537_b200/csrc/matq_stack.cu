@@ -19,6 +19,19 @@ cudaError_t set_smem(size_t smem) {
     return cudaSuccess;
 }
 
+// Every CTA must be resident: the layer barriers spin.  The launch is
+// cooperative (the driver then guarantees co-residency or fails the launch),
+// with the cluster dimension added for CTA pairs.  MQ_STACK_NOCOOP=1 drops the
+// cooperative attribute from pair launches -- a profiling knob only: ncu's
+// kernel replay rejects cooperative cluster launches.
+bool stack_nocoop() {
+    static const int v = [] {
+        const char* e = getenv("MQ_STACK_NOCOOP");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 template <int NT, int R, bool CHILD>
 cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaStream_t stream) {
     auto kern = k_stack<NT, R, CHILD>;
@@ -30,28 +43,25 @@ cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaSt
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the layer barriers spin
-    attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = 2;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    // CTA pairs launch as clusters without the cooperative attribute (the pair is
-    // not expressible in a cooperative launch under every tool, e.g. ncu's kernel
-    // replay); co-residency of every pair was checked by the plan
-    // (stack_pair_capacity >= grid) and the grid never exceeds one CTA per SM
-    if (p.cluster) {
-        cfg.attrs = attr + 1;
-        cfg.numAttrs = 1;
-    } else {
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
+    int n = 0;
+    if (!(p.cluster && stack_nocoop())) {
+        attr[n].id = cudaLaunchAttributeCooperative;
+        attr[n].val.cooperative = 1;
+        ++n;
     }
+    if (p.cluster) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = 2;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
     e = cudaLaunchKernelEx(&cfg, kern, p);
     if (getenv("MQ_STACK_LAUNCH_DEBUG"))
-        fprintf(stderr, "k_stack launch cluster=%d grid=%d smem=%zu -> %s\n", p.cluster, grid, smem,
-                cudaGetErrorString(e));
+        fprintf(stderr, "k_stack launch cluster=%d coop=%d grid=%d smem=%zu -> %s\n", p.cluster,
+                !(p.cluster && stack_nocoop()), grid, smem, cudaGetErrorString(e));
     return e;
 }
 
@@ -93,6 +103,27 @@ cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, s
 cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream) {
     if (nt == 1) return launch_one_stack<1, 0, false>(p, grid, smem, stream);
     return launch_one_stack<2, 0, false>(p, grid, smem, stream);
+}
+
+// Plan-time probe: launch the planned kernel with the planned attributes and no
+// layers (it returns at entry) and report whether the driver accepts it.
+cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster) {
+    StackParams p{};
+    p.n_layers = 0;
+    p.cluster = cluster ? 1 : 0;
+    cudaError_t e = r == 0 ? launch_stack_mixed(p, nt, grid, smem, 0) : cudaSuccess;
+    if (r != 0) {
+        switch (r) {
+            case 2: e = launch_stack_r<2>(p, nt, child, grid, smem, 0); break;
+            case 3: e = launch_stack_r<3>(p, nt, child, grid, smem, 0); break;
+            case 4: e = launch_stack_r<4>(p, nt, child, grid, smem, 0); break;
+            case 6: e = launch_stack_r<6>(p, nt, child, grid, smem, 0); break;
+            default: e = launch_stack_r<8>(p, nt, child, grid, smem, 0); break;
+        }
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+    if (e != cudaSuccess) (void)cudaGetLastError();
+    return e;
 }
 
 int stack_pair_capacity(int nt, int r, bool child, size_t smem) {

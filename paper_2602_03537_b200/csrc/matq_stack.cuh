@@ -40,6 +40,9 @@ struct __align__(8) StackLayer {
     float out_scale;
     int r;            // slice width (the mixed kernel dispatches on it)
     int stage_bytes;  // one ring stage: 128 B of scales + the planes read at r
+    int amax_src;     // fp16 staging: the earlier layer whose output holds all of X (its max |y| is
+                      // published), or -1 (external X: the staging measures max |x| in a first pass)
+    int pub_amax;     // publish max |y| of this layer's output (a later fp16 layer reads it)
 };
 
 struct StackParams {
@@ -60,8 +63,9 @@ struct StackParams {
     int cl_tiles;      // most row tiles a CTA holds in an S == 2 layer
     float* ws;         // split-K partials (max over layers)
     int* tickets;      // split-K tickets, self-resetting
-    unsigned* done;    // [n_layers] monotone completion counters
-    unsigned* launch_ctr;
+    unsigned long long* done;  // [n_layers] monotone completion counters (64-bit: never wrap)
+    unsigned long long* launch_ctr;
+    unsigned long long* amax;  // [n_layers] (step tag << 32) | float bits of max |y|, atomicMax-published
     unsigned long long* dbg_ts;  // MQ_GEMV_TIMING builds: [n_layers][148][8] globaltimer stamps
 };
 
@@ -80,12 +84,16 @@ __device__ __forceinline__ unsigned long long stack_gtimer() {
 #define MQ_STS(l, ev) do { } while (0)
 #endif
 
+#ifndef MQ_PROD_SLEEP_NS
+#define MQ_PROD_SLEEP_NS 0
+#endif
 #ifndef MQ_STACK_SPIN_NS
 #define MQ_STACK_SPIN_NS 0
 #endif
 
-constexpr int kStackWarps = 15;                      // ring (work) warps
-constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp without a ring
+constexpr int kStackWarps = 15;                      // consumer (decode + MMA) warps
+constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one producer warp issuing every ring's bulk copies
+constexpr int kConsumerThreads = kStackWarps * 32;
 
 // A warp's share of one layer.  CTA c works on K chunk kc = c % S and the
 // contiguous row tiles [ta, ta + ntiles) of that chunk (near-equal split over
@@ -96,11 +104,14 @@ constexpr int kStackThreads = (kStackWarps + 1) * 32;  // + one sync warp withou
 // the CTA pair's shared memory (S = 2) or the split-K workspace and a ticket --
 // all deterministic.
 // SMSP-balanced split: warp w runs on SMSP w % 4, and SMSP 3 also hosts the
-// sync warp, so it has 3 ring warps to the others' 4.  The ALU pipe is per
-// SMSP, so each SMSP gets a quarter of the steps: warps on SMSP 3 take 4 units
-// of work, the rest 3 (U(w) = units before warp w, 48 in all).
-constexpr int kSplitUnits = 48;
-__device__ __forceinline__ int warp_units(int w) { return 3 * w + (w >> 2); }
+// producer warp, so it has 3 consumer warps to the others' 4.  The ALU pipe is
+// per SMSP: consumer warps on SMSPs 0-2 take 3 units of work, those on SMSP 3
+// MQ_SMSP3_UNITS (U(w) = units before warp w, kSplitUnits in all).
+#ifndef MQ_SMSP3_UNITS
+#define MQ_SMSP3_UNITS 3
+#endif
+constexpr int kSplitUnits = 3 * kStackWarps + (MQ_SMSP3_UNITS - 3) * (kStackWarps / 4);
+__device__ __forceinline__ int warp_units(int w) { return 3 * w + (MQ_SMSP3_UNITS - 3) * (w >> 2); }
 struct WarpPlan {
     int ta, ntiles, ns, chunk0, kc, f0, f1;
 };
@@ -131,13 +142,14 @@ __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
     return warp_units(warp) * (w.ntiles * w.ns) / kSplitUnits;
 }
 // The last warp whose range starts at or before step x: the largest v with
-// floor(U(v) P / 48) <= x, i.e. U(v) <= umax = ceil(48 (x + 1) / P) - 1; v is
-// floor(4 umax / 13) or one more (never an empty warp).
+// floor(U(v) P / kSplitUnits) <= x, i.e. U(v) <= umax = ceil(kSplitUnits (x + 1) / P) - 1
+// (never an empty warp); the estimate 4 umax / (9 + U3) is off by at most one.
 __device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
     const int P = w.ntiles * w.ns;
     const int umax = udiv_small(kSplitUnits * (x + 1) + P - 1, P) - 1;
-    int v = min(kStackWarps - 1, 4 * umax / 13);
-    if (v < kStackWarps - 1 && warp_units(v + 1) <= umax) ++v;
+    int v = min(kStackWarps - 1, 4 * umax / (9 + MQ_SMSP3_UNITS));
+    while (v > 0 && warp_units(v) > umax) --v;
+    while (v < kStackWarps - 1 && warp_units(v + 1) <= umax) ++v;
     return v;
 }
 // Warps after wa holding a part of the tile ending at step f_last: those whose
@@ -145,7 +157,9 @@ __device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
 // pairs than warps leaves some warps without work; they never arrive).
 __device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last) {
     const int vmax = last_warp_at(w, f_last);
-    if (w.ntiles * w.ns >= 16) return vmax - wa;  // every warp has >= P / 16 >= 1 steps
+    constexpr int kMinUnits = MQ_SMSP3_UNITS < 3 ? MQ_SMSP3_UNITS : 3;
+    // every warp has >= floor(P kMinUnits / kSplitUnits) >= 1 steps
+    if (w.ntiles * w.ns * kMinUnits >= kSplitUnits) return vmax - wa;
     int n = 0;
     for (int v = wa + 1; v <= vmax; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
     return n;
@@ -153,8 +167,8 @@ __device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last)
 
 // Publish: bar.sync orders the CTA's writes before thread 0's release at gpu
 // scope (cumulative), which the waiters' ld.acquire.gpu synchronises with.
-__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 // Explicit global stores: Y's pointer comes from the shared-memory layer table,
 // so a plain store would be GENERIC -- and a generic store is ordered behind the
@@ -179,26 +193,50 @@ __device__ __forceinline__ unsigned ld_acquire_cta(uint32_t saddr) {
     asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr) : "memory");
     return v;
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+// the consumer warps only (the producer warp runs ahead across layers): named
+// barrier 0 with the consumer thread count (1..15 are the tile hand-off barriers)
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 0, %0;" ::"n"(kConsumerThreads) : "memory");
+}
+// every lane of a consumer warp arrives (count 32): its reads of the slot are
+// released to the producer's next bulk copy into it
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t r;
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(r) : "r"(bar), "r"(parity) : "memory");
+    return r != 0;
+}
 
-constexpr int kSyncThread = kStackWarps * 32;
+constexpr int kSyncThread = 0;  // consumer warp 0, lane 0: layer barrier wait + publish
 
-// Per-warp weight ring: the issue cursor (lane 0) walks (layer, flattened step)
-// of this warp across layer boundaries; each layer's stage is its own size
-// (scales + its plane count) in slots of the plan's largest stage.
+// Per-consumer weight ring: the producer warp's lane c walks consumer c's
+// (layer, flattened step) sequence across layer boundaries and issues each
+// step's bulk copy into the next free slot of c's ring; each layer's stage is
+// its own size (scales + its plane count) in slots of the plan's largest stage.
+// Slot s of ring c has a full barrier (count 1 + transaction bytes, completed by
+// the TMA engine) and an empty barrier (count 32: every lane of consumer c
+// arrives once it has read the slot).
 struct RingCtx {
-    uint32_t bar0, ring0, stride;
+    uint32_t full0, empty0, ring0, stride;  // this ring's barriers and slots
     int D;
     uint64_t policy;
-    int cta, warp, n_layers;
+    int cta, warp, n_layers;  // warp = the consumer this ring feeds
     const StackLayer* tab;
 };
 struct StackCursor {
     int il, iff, istage, itile, isi, insteps;
+    uint32_t cyc;  // completed passes over the ring's slots
     WarpPlan ip;
     const uint32_t* iblob;
     const uint32_t* isrc;  // the next step's block
@@ -206,7 +244,7 @@ struct StackCursor {
     uint32_t ibytes;
 };
 __device__ __forceinline__ void cursor_next_layer(StackCursor& c, const RingCtx& rc) {
-    for (++c.il; c.il < rc.n_layers; ++c.il) {  // the next layer with work for this warp
+    for (++c.il; c.il < rc.n_layers; ++c.il) {  // the next layer with work for this consumer
         const StackLayer& L = rc.tab[c.il];
         c.ip = warp_plan(L, rc.cta, rc.warp);
         if (c.ip.f1 > c.ip.f0) {
@@ -223,10 +261,11 @@ __device__ __forceinline__ void cursor_next_layer(StackCursor& c, const RingCtx&
         }
     }
 }
-// FIXB: the stage size when every layer's is the same (uniform kernels), else 0
+// Issue the cursor's next step into slot c.istage (the caller checked that the
+// slot is free).  FIXB: the stage size when every layer's is the same (uniform
+// kernels), else 0.
 template <uint32_t FIXB>
-__device__ __forceinline__ void cursor_issue(StackCursor& c, const RingCtx& rc) {  // no-op when done
-    if (c.il >= rc.n_layers) return;
+__device__ __forceinline__ void cursor_issue(StackCursor& c, const RingCtx& rc) {
     const uint32_t bytes = FIXB ? FIXB : c.ibytes, stride = FIXB ? FIXB : rc.stride;
     const uint32_t* src = c.isrc;
     if (++c.isi == c.ip.ns) {
@@ -236,17 +275,48 @@ __device__ __forceinline__ void cursor_issue(StackCursor& c, const RingCtx& rc) 
     } else {
         c.isrc += c.isw;
     }
-    const uint32_t bar = rc.bar0 + 8 * c.istage;
+    const uint32_t bar = rc.full0 + 8 * c.istage;
     mbar_expect_tx(bar, bytes);
     bulk_g2s(rc.ring0 + c.istage * stride, src, bytes, bar, rc.policy);
-    if (++c.istage == rc.D) c.istage = 0;
+    if (++c.istage == rc.D) {
+        c.istage = 0;
+        ++c.cyc;
+    }
     if (++c.iff == c.ip.f1) cursor_next_layer(c, rc);
 }
 
+// The producer warp: lane c < 15 feeds consumer c.  A slot is reused once its
+// consumer's previous pass released it (empty barrier phase cyc - 1).  Lanes
+// advance independently; a round in which no lane can issue backs off briefly
+// so the polling does not take issue slots from the consumers on this SMSP.
+template <uint32_t FIXB>
+__device__ __noinline__ void stack_producer(RingCtx rc) {
+    const int lane = threadIdx.x & 31;
+    StackCursor cur{};
+    cur.il = -1;
+    if (lane < kStackWarps) cursor_next_layer(cur, rc);
+    else cur.il = rc.n_layers;
+    for (;;) {
+        const bool live = cur.il < rc.n_layers;
+        if (!__any_sync(0xffffffffu, live)) break;
+        bool issued = false;
+        if (live && (cur.cyc == 0 || mbar_test(rc.empty0 + 8 * cur.istage, (cur.cyc - 1) & 1u))) {
+            cursor_issue<FIXB>(cur, rc);
+            issued = true;
+        }
+#if MQ_PROD_SLEEP_NS
+        if (!__any_sync(0xffffffffu, issued)) __nanosleep(MQ_PROD_SLEEP_NS);
+#else
+        (void)issued;
+#endif
+    }
+}
+
 struct StackShared {
-    unsigned gen;
+    unsigned long long gen;
     unsigned amax_bits;  // F16: the chunk's max |x| (float bits)
     float inv_lambda;    // F16: 1 / the activation scale
+    int amax_ok;         // F16: amax_bits came from the producing layer (one staging pass)
 };
 
 // One layer of the step, slice width R.  Uniform stacks instantiate k_stack
@@ -254,9 +324,8 @@ struct StackShared {
 // dispatch here on the layer table's r -- the ring and cursor are shared.
 template <int R, int NT, bool CHILD, bool FIXED>
 __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLayer* tab, int l,
-                                            StackCursor& cur, const RingCtx& rc, int& cstage,
-                                            uint32_t& parity, StackShared& sh, uint8_t* smem,
-                                            unsigned target) {
+                                            const RingCtx& rc, int& cstage, uint32_t& parity,
+                                            StackShared& sh, uint8_t* smem, unsigned long long target) {
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     constexpr uint32_t kSlab = 512, kScaleBytes = 128;
     constexpr uint32_t kStage = kScaleBytes + NPL * kSlab;
@@ -270,43 +339,57 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     constexpr int NCOPY = F16 ? (R == 4 ? 2 : 1) : (ZP ? zp_ncopies(R) : 1);
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool ring_warp = warp < kStackWarps;
     const int g = lane >> 2, t = lane & 3;
     const int D = rc.D;
     const uint32_t xs_saddr = smem_addr(xs);
     float* zc = reinterpret_cast<float*>(smem + p.cs_off);  // [2 cs groups][NT * 8] zero-point constants
 
     const StackLayer& L = tab[l];
-    const WarpPlan wp = ring_warp ? warp_plan(L, rc.cta, warp) : warp_plan(L, rc.cta, 0);
+    const WarpPlan wp = warp_plan(L, rc.cta, warp);
     const int Kc = L.cs * kStepCols;
     const int col_base = wp.chunk0 * kStepCols;  // every warp of the CTA shares its chunk
 
     // ---- wait for the producer of this layer's activations ---------------
     MQ_STS(l, 0);
-    if (l > 0 && threadIdx.x == kSyncThread) {
-        while (ld_acquire_u32(p.done + l - 1) < target) {
+    if (threadIdx.x == kSyncThread) {
+        if (l > 0) {
+            while (ld_acquire_u64(p.done + l - 1) < target) {
 #if MQ_STACK_SPIN_NS
-            __nanosleep(MQ_STACK_SPIN_NS);  // fewer polls on the counter line while CTAs publish
+                __nanosleep(MQ_STACK_SPIN_NS);  // fewer polls on the counter line while CTAs publish
 #endif
+            }
+        }
+        if constexpr (F16) {
+            // the producing layer published max |y| for this step: one staging pass
+            int ok = 0;
+            if (L.amax_src >= 0) {
+                const unsigned long long v = __ldcg(p.amax + L.amax_src);
+                ok = (unsigned)(v >> 32) == (unsigned)(sh.gen + 1ull);
+                if (ok) sh.amax_bits = (unsigned)v;
+            }
+            sh.amax_ok = ok;
         }
     }
-    __syncthreads();
+    consumer_sync();
     MQ_STS(l, 1);
 
     // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
     if constexpr (F16) {
-        // pass 1: raw bf16 into the staging tail + the chunk's max |x|
+        // pass 1 (X not produced inside this step): raw bf16 into the staging tail
+        // + the chunk's max |x|; else the published max |y| and straight to pass 2
         const uint16_t* X = L.X;
         const int c8 = Kc >> 3;
         const int n8 = p.B * c8;
         uint16_t* tmp = xs + NCOPY * p.xcopy_stride;
+        const bool one_pass = sh.amax_ok != 0;
+        if (!one_pass) {
         float amax = 0.0f;
         constexpr int kU = 4;
-        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * kConsumerThreads) {
             uint4 vv[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * (int)blockDim.x;
+                const int idx = base_i + u * kConsumerThreads;
                 vv[u] = make_uint4(0, 0, 0, 0);
                 if (idx < n8) {
                     const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
@@ -316,7 +399,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             }
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * (int)blockDim.x;
+                const int idx = base_i + u * kConsumerThreads;
                 if (idx >= n8) break;
                 const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                 *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
@@ -329,16 +412,23 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 #pragma unroll
         for (int s = 16; s >= 1; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
         if (lane == 0) atomicMax(&sh.amax_bits, __float_as_uint(amax));  // non-negative: bits order = value order
-        __syncthreads();
+        consumer_sync();
+        }
         // lambda = 2^(14 - e), max|x| in [2^e, 2^(e+1)): max|x| * lambda < 2^15 < 65504
         const float amax_all = __uint_as_float(sh.amax_bits);
         const int e = amax_all > 0.0f ? ilogbf(amax_all) : 0;
         const float lam = ldexpf(1.0f, 14 - e);
         if (threadIdx.x == 0) sh.inv_lambda = ldexpf(1.0f, e - 14);
         // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
-        for (int idx = threadIdx.x; idx < n8; idx += blockDim.x) {
+        for (int idx = threadIdx.x; idx < n8; idx += kConsumerThreads) {
             const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-            const uint4 v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
+            uint4 v;
+            if (one_pass) {
+                v = make_uint4(0, 0, 0, 0);
+                if (col_base + c < L.K) v = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col_base + c));
+            } else {
+                v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
+            }
             const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
             const int cs_ = c & 255;
             const int o = zp_off16<R>((cs_ & 63) >> 4);
@@ -368,11 +458,11 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
         const int c8 = Kc >> 3;
         const int n8 = p.B * c8;
         constexpr int kU = 4;  // loads in flight per thread before the first use
-        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * (int)blockDim.x) {
+        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * kConsumerThreads) {
             uint4 vv[kU];
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * (int)blockDim.x;
+                const int idx = base_i + u * kConsumerThreads;
                 vv[u] = make_uint4(0, 0, 0, 0);
                 if (idx < n8) {
                     const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
@@ -382,7 +472,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             }
 #pragma unroll
             for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * (int)blockDim.x;
+                const int idx = base_i + u * kConsumerThreads;
                 if (idx >= n8) break;  // warp-uniform: n8 is a multiple of 32
                 const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
                 const uint4 v = vv[u];
@@ -417,7 +507,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             }
         }
     }
-    __syncthreads();
+    consumer_sync();
     if constexpr (F16) {
         if (threadIdx.x == 0) sh.amax_bits = 0u;  // ready for the next layer (read only above)
     }
@@ -445,8 +535,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 
     // ---- this warp's units of layer l --------------------------------------
     float tot[NT][4], acc[NT][4];
-    auto process = [&](const uint4 (&buf)[NPL], const float (&sc)[4], int st) {
-        const uint32_t xcol = (uint32_t)(st * kStepCols - col_base);
+    auto process = [&](const uint4 (&buf)[NPL], const float (&sc)[4], uint32_t xcol) {
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
             uint32_t T[NPL];
@@ -511,8 +600,18 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // ticket, the last chunk to arrive summing the partials in chunk order
     const float out_scale_l = F16 ? L.out_scale * sh.inv_lambda : L.out_scale;
     const bool pair = p.cluster && L.S == 2;
+    // max |y| of the bf16 values this warp stored for a tile -> the layer's
+    // published maximum (a later fp16 layer stages its X in one pass with it)
+    auto publish_amax = [&](float m) {
+        if (!L.pub_amax) return;
+#pragma unroll
+        for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+        if (lane == 0)
+            atomicMax(p.amax + l, ((unsigned long long)(unsigned)(sh.gen + 1ull) << 32) | __float_as_uint(m));
+    };
     auto emit = [&](int rt, const float (&v)[NT][4]) {
         const int r0 = rt * kTileRows + g;
+        float ymax = 0.0f;
         if (pair) {
             const int li = rt - wp.ta;
             const uint32_t cl = smem_addr(smem + p.cl_off);
@@ -546,11 +645,14 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                         const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                        if (b < p.B && row < L.N)
-                            st_global_u16(L.Y + (long long)b * L.ldy + row,
-                                          f32_to_bf16_rn(v[nt][2 * h + c] * out_scale_l + pv[2 * h + c]));
+                        if (b < p.B && row < L.N) {
+                            const uint16_t yb = f32_to_bf16_rn(v[nt][2 * h + c] * out_scale_l + pv[2 * h + c]);
+                            st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
+                            ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
+                        }
                     }
             }
+            publish_amax(ymax);
             return;
         }
 #pragma unroll
@@ -562,11 +664,19 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                     const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
                     const float val = v[nt][2 * h + c] * out_scale_l;
                     if (b < p.B && row < L.N) {
-                        if (L.S == 1) st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(val));
-                        else st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
+                        if (L.S == 1) {
+                            const uint16_t yb = f32_to_bf16_rn(val);
+                            st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
+                            ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
+                        } else {
+                            st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
+                        }
                     }
                 }
-        if (L.S == 1) return;
+        if (L.S == 1) {
+            publish_amax(ymax);
+            return;
+        }
         __syncwarp();
         int last = 0;
         // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
@@ -591,9 +701,12 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                             sum += a0; sum += a1; sum += a2; sum += a3;
                         }
                         for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
-                        st_global_u16(L.Y + (long long)b * L.ldy + row, f32_to_bf16_rn(sum));
+                        const uint16_t yb = f32_to_bf16_rn(sum);
+                        st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
+                        ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
                     }
                 }
+        publish_amax(ymax);
         __syncwarp();
         if (lane == 0) p.tickets[rt] = 0;
     };
@@ -605,71 +718,70 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
     const int first_lt = wp.ns > 0 ? udiv_small(wp.f0, wp.ns) : 0;
     int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
-    const int f_end = ring_warp ? wp.f1 : wp.f0;
+    // segment by segment: the steps of one row tile inside [f0, f1)
 #pragma unroll 1
-    for (int f = wp.f0; f < f_end; ++f) {
-        const int st = wp.chunk0 + si;
-        if (f == wp.f0 || si == 0) {
+    for (int f = wp.f0; f < wp.f1;) {
+        const int seg = min(wp.ns - si, wp.f1 - f);
+        const bool starts_tile = si == 0;  // this segment holds the tile's first step
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
+        uint32_t xcol = (uint32_t)(si * kStepCols);  // column of the step inside the staged chunk
+#pragma unroll 1
+        for (int k = 0; k < seg; ++k) {
+            mbar_wait(rc.full0 + 8 * cstage, parity);
+            const uint32_t src = rc.ring0 + cstage * stride;
+            float sc[4];
+            sc[0] = lds32f(src + g * 4);
+            sc[1] = lds32f(src + (g + 8) * 4);
+            sc[2] = lds32f(src + (16 + g) * 4);
+            sc[3] = lds32f(src + (24 + g) * 4);
+            uint4 buf[NPL];
+#pragma unroll
+            for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
+            mbar_arrive(rc.empty0 + 8 * cstage);  // the slot is read: the producer may refill it
+            if (++cstage == D) {
+                cstage = 0;
+                parity ^= 1u;
+            }
+            process(buf, sc, xcol);
+            xcol += kStepCols;
+        }
+        f += seg;
+        si += seg;
+        if (f == wp.f1) MQ_STS_WMAX(l, 5);  // this warp's last step decoded
+        const bool tile_end = si == wp.ns;
+        if (starts_tile && tile_end) {
+            emit(wp.ta + lt, tot);
+        } else if (!starts_tile) {
+            float* sp = slot_ptr(warp);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                for (int i = 0; i < 4; ++i) tot[nt][i] = 0.0f;
-        }
-        mbar_wait(rc.bar0 + 8 * cstage, parity);
-        const uint32_t src = rc.ring0 + cstage * stride;
-        float sc[4];
-        sc[0] = lds32f(src + g * 4);
-        sc[1] = lds32f(src + (g + 8) * 4);
-        sc[2] = lds32f(src + (16 + g) * 4);
-        sc[3] = lds32f(src + (24 + g) * 4);
-        uint4 buf[NPL];
-#pragma unroll
-        for (int jj = 0; jj < NPL; ++jj) buf[jj] = lds128(src + kScaleBytes + jj * kSlab + lane * 16);
-        __syncwarp();
-        if (lane == 0) {
-            fence_proxy_async_smem();
-            cursor_issue<FIXED ? kStage : 0u>(cur, rc);
-        }
-        process(buf, sc, st);
-        if (++cstage == D) {
-            cstage = 0;
-            parity ^= 1u;
-        }
-        if (f + 1 == wp.f1) MQ_STS_WMAX(l, 5);  // this warp's last step decoded
-        const bool tile_end = si == wp.ns - 1;
-        if (tile_end || f + 1 == wp.f1) {
-            const bool starts_tile = wp.f0 <= lt * wp.ns;  // this segment holds the tile's first step
-            if (starts_tile && tile_end) {
-                emit(wp.ta + lt, tot);
-            } else if (!starts_tile) {
-                float* sp = slot_ptr(warp);
+                for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
+            // hand the part to the emitter wa (holder of the tile's first step)
+            // through named barrier wa + 1: bar.arrive orders the slot stores and
+            // does not wait
+            const int wa = last_warp_at(wp, lt * wp.ns);
+            named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, (lt + 1) * wp.ns - 1)));
+        } else {
+            // emitter (its range ends inside the tile): own part, then the later
+            // warps' parts in warp order
+            const int f_last = (lt + 1) * wp.ns - 1;
+            named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, f_last)));
+            const int vmax = last_warp_at(wp, f_last);
+            for (int w2 = warp + 1; w2 <= vmax; ++w2) {
+                if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
+                const float* sp = slot_ptr(w2);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
-                // hand the part to the emitter wa (holder of the tile's first step)
-                // through named barrier wa + 1: bar.arrive orders the slot stores and
-                // does not wait, and -- unlike a memory fence -- does not stall on
-                // lane 0's in-flight ring bulk copies
-                const int wa = last_warp_at(wp, lt * wp.ns);
-                named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, (lt + 1) * wp.ns - 1)));
-            } else {
-                // emitter: own part, then the later warps' parts in warp order
-                const int f_last = (lt + 1) * wp.ns - 1;
-                named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, f_last)));
-                const int vmax = last_warp_at(wp, f_last);
-                for (int w2 = warp + 1; w2 <= vmax; ++w2) {
-                    if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
-                    const float* sp = slot_ptr(w2);
-#pragma unroll
-                    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
-                }
-                emit(wp.ta + lt, tot);
+                    for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
             }
+            emit(wp.ta + lt, tot);
         }
-        if (++si == wp.ns) {
+        if (tile_end) {
             si = 0;
             ++lt;
         }
@@ -677,10 +789,10 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     MQ_STS(l, 4);
 
     // ---- publish layer l ------------------------------------------------
-    __syncthreads();
+    consumer_sync();
     MQ_STS(l, 6);
-    // the sync warp: a ring warp's release would wait for its in-flight bulk copies
-    if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1u);
+    // consumers have no bulk copies in flight, so the release is not delayed by the weight stream
+    if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1ull);
     MQ_STS(l, 7);
 }
 
@@ -689,16 +801,16 @@ template <int NT, int RFIX, bool CHILD>
 __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ StackShared sh;
+    if (p.n_layers == 0) return;  // plan-time launch probe
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // warps 0..14 stream weights (lane 0 issues their ring's bulk copies); warp 15
-    // only synchronises: its fences never wait on in-flight bulk copies (a
-    // memory barrier on a warp with outstanding cp.async.bulk waits for them)
-    const bool ring_warp = warp < kStackWarps;
+    // warps 0..14 decode + MMA (consumers); warp 15 issues every ring's bulk
+    // copies (producer), so no consumer ever has a bulk copy in flight
     const int D = p.stages;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);
-    uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 8;
-    if (threadIdx.x == kSyncThread) sh.gen = atomicAdd(p.launch_ctr, 1u) / gridDim.x;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);   // [15][8]
+    uint64_t* empty = full + kStackWarps * 8;                           // [15][8]
+    uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 16;
+    if (threadIdx.x == kSyncThread) sh.gen = atomicAdd(p.launch_ctr, 1ull) / gridDim.x;
     if (threadIdx.x == 0) sh.amax_bits = 0u;
     // the layer table lives in shared memory: a descriptor field re-read from
     // global memory mid-layer (register rematerialisation) waits behind the
@@ -710,19 +822,25 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         uint32_t* dst = reinterpret_cast<uint32_t*>(tab);
         for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldg(src + i);
     }
+    const bool producer = warp == kStackWarps;
+    const int ring_of = producer ? (lane < kStackWarps ? lane : 0) : warp;  // the ring this thread serves
     RingCtx rc;
-    rc.bar0 = smem_addr(bars + warp * 8);
-    rc.ring0 = smem_addr(ring + (size_t)warp * D * p.stage_stride);
+    rc.full0 = smem_addr(full + ring_of * 8);
+    rc.empty0 = smem_addr(empty + ring_of * 8);
+    rc.ring0 = smem_addr(ring + (size_t)ring_of * D * p.stage_stride);
     rc.stride = (uint32_t)p.stage_stride;
     rc.D = D;
     rc.policy = 0;
     rc.cta = blockIdx.x;
-    rc.warp = warp;
+    rc.warp = ring_of;
     rc.n_layers = p.n_layers;
     rc.tab = tab;
-    if (ring_warp && lane == 0) {
+    if (producer && lane < kStackWarps) {
         rc.policy = policy_evict_first();
-        for (int i = 0; i < D; ++i) mbar_init(rc.bar0 + 8 * i, 1);
+        for (int i = 0; i < D; ++i) {
+            mbar_init(rc.full0 + 8 * i, 1);
+            mbar_init(rc.empty0 + 8 * i, 32);
+        }
         fence_mbar_init();
     }
     if (p.cluster && threadIdx.x == kSyncThread) {
@@ -736,29 +854,27 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     }
     __syncthreads();
     if (p.cluster) cluster_sync_all();  // the peer's first st.async lands on initialised barriers
-    const unsigned target = (sh.gen + 1u) * gridDim.x;
 
-    StackCursor cur{};
-    cur.il = -1;
-    if (ring_warp && lane == 0) {
-        cursor_next_layer(cur, rc);
+    if (producer) {
         // the same slot stride the consumer uses: the stage size in uniform kernels
         constexpr uint32_t kFix = RFIX ? 128u + 512u * PlaneCount<RFIX ? RFIX : 2, CHILD>::value : 0u;
-        for (int i = 0; i < D; ++i) cursor_issue<kFix>(cur, rc);
+        stack_producer<kFix>(rc);
+        return;
     }
+    const unsigned long long target = (sh.gen + 1ull) * gridDim.x;
     int cstage = 0;
     uint32_t parity = 0;
 #pragma unroll 1
     for (int l = 0; l < p.n_layers; ++l) {
         if constexpr (RFIX != 0) {
-            stack_layer<RFIX, NT, CHILD, true>(p, tab, l, cur, rc, cstage, parity, sh, smem, target);
+            stack_layer<RFIX, NT, CHILD, true>(p, tab, l, rc, cstage, parity, sh, smem, target);
         } else {
             switch (tab[l].r) {
-                case 2: stack_layer<2, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 3: stack_layer<3, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 4: stack_layer<4, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                case 6: stack_layer<6, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
-                default: stack_layer<8, NT, false, false>(p, tab, l, cur, rc, cstage, parity, sh, smem, target); break;
+                case 2: stack_layer<2, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 3: stack_layer<3, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 4: stack_layer<4, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 6: stack_layer<6, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                default: stack_layer<8, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
             }
         }
     }
@@ -771,5 +887,7 @@ cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t sm
 // CTAs of k_stack<nt, r, child> (r = 0: the mixed kernel) that can be co-resident as
 // clusters of 2 with `smem` bytes each, or 0 when unknown
 int stack_pair_capacity(int nt, int r, bool child, size_t smem);
+// launch the planned configuration with no layers: does the driver accept it?
+cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster);
 
 }  // namespace mq

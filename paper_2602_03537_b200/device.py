@@ -143,10 +143,19 @@ class PlaneTensor:
                   _lib.ptr(blob), _lib.ptr(ts), _lib.stream_ptr())
         return cls(blob, ts, N, K, group_size, nbits, nbits, scales_are_effective)
 
-    @classmethod
-    def random_parent(cls, N: int, K: int, group_size: int = 128, seed: int = 0,
-                      scale_range=(0.005, 0.02)) -> "PlaneTensor":
-        """Synthetic int8 parent generated on device (bench / model proxies)."""
+    @staticmethod
+    def random_parent_codes(N: int, K: int, group_size: int = 128, seed: int = 0,
+                            scale_range=(0.005, 0.02), signed_rows: bool = False
+                            ) -> tuple[torch.Tensor, torch.Tensor]:
+        """The (codes uint8 (N, K), scales fp32 (N, ng)) random_parent packs, on device.
+
+        Codes are uniform over [0, 255] (the reference's random_task,
+        matmul.py:129-131).  Rounding slices of uniform codes are biased (mean
+        s - z is -7.9 code units at r = 2, -1.9 at r = 3), which a chain of
+        128 linears amplifies into an exponential blow-up of the activations'
+        common mode; ``signed_rows`` gives every row's scales a random sign so
+        that bias cancels across rows (the chained model proxies use it; the
+        work per weight is unchanged)."""
         _lib.require_cuda()
         g = torch.Generator(device="cuda")
         g.manual_seed(seed)
@@ -155,6 +164,16 @@ class PlaneTensor:
         ng = -(-K // group_size)
         lo, hi = scale_range
         scales = torch.rand((N, ng), generator=g, device="cuda", dtype=torch.float32) * (hi - lo) + lo
+        if signed_rows:
+            sign = torch.randint(0, 2, (N, 1), generator=g, device="cuda", dtype=torch.int32) * 2 - 1
+            scales = scales * sign.to(torch.float32)
+        return codes, scales
+
+    @classmethod
+    def random_parent(cls, N: int, K: int, group_size: int = 128, seed: int = 0,
+                      scale_range=(0.005, 0.02), signed_rows: bool = False) -> "PlaneTensor":
+        """Synthetic int8 parent generated on device (bench / model proxies)."""
+        codes, scales = cls.random_parent_codes(N, K, group_size, seed, scale_range, signed_rows)
         out = cls.from_codes(codes, 8, scales, group_size)
         del codes
         return out
@@ -374,3 +393,13 @@ class StackProgram:
     def run(self, stream=None) -> None:
         _lib.call("mq_stack_run", self.plan, _lib.ptr(self.table), _lib.ptr(self.ws), self.ws.numel(),
                   _lib.stream_ptr(stream))
+
+    def launches(self, set_to: int | None = None) -> int:
+        """The step counter behind the layer barriers (mq_stack_epoch): read it,
+        or re-base it to ``set_to`` (synchronous)."""
+        import ctypes
+
+        v = ctypes.c_ulonglong(0 if set_to is None else int(set_to))
+        _lib.call("mq_stack_epoch", self.plan, _lib.ptr(self.ws), self.ws.numel(), ctypes.byref(v),
+                  0 if set_to is None else 1, _lib.stream_ptr())
+        return int(v.value)

@@ -62,7 +62,7 @@ class LlamaDecoder:
             for kind in ("qkv", "o", "gate_up", "down"):
                 N, K = full_layer_dims(shape, kind)
                 pt = PlaneTensor.random_parent(N, K, seed=seed * 7919 + i * 4 + ("qkv", "o", "gate_up", "down").index(kind),
-                                               scale_range=_gain_matched_scales(K))
+                                               scale_range=_gain_matched_scales(K), signed_rows=True)
                 blk[kind] = MatLinear(pt, 4, name="layers.%d.%s" % (i, kind))
             blk["ln1"] = torch.ones(h, device=dev)
             blk["ln2"] = torch.ones(h, device=dev)

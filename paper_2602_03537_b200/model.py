@@ -108,13 +108,17 @@ class LinearStack:
         self.fused = fused
         kinds = KINDS if fused else KINDS_UNFUSED
         self.layers: list[tuple[str, str, PlaneTensor]] = []
+        # (seed, scale_range, signed_rows) of each layer's synthetic parent: PlaneTensor.random_parent
+        # regenerates the same codes and scales from them (the parity tests do)
+        self.parent_seeds: list[tuple[int, tuple[float, float]]] = []
         for i in range(self.n_layers):
             for kind in kinds:
                 N, K = tp_layer_dims(shape, kind, tp, rank)
-                pt = PlaneTensor.random_parent(N, K, group_size,
-                                               seed=seed * 1000003 + (i * 8 + kinds.index(kind)) * 8 + rank,
-                                               scale_range=_gain_matched_scales(K * tp if kind in ("o", "down") else K))
+                sd = seed * 1000003 + (i * 8 + kinds.index(kind)) * 8 + rank
+                sr = _gain_matched_scales(K * tp if kind in ("o", "down") else K)
+                pt = PlaneTensor.random_parent(N, K, group_size, seed=sd, scale_range=sr, signed_rows=True)
                 self.layers.append(("layers.%d.%s" % (i, kind), kind, pt))
+                self.parent_seeds.append((sd, sr, True))
         h = shape.hidden
         dev = torch.device("cuda", torch.cuda.current_device())
         self.x = torch.zeros((batch, h), dtype=torch.bfloat16, device=dev)
