@@ -102,11 +102,25 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
 
 
-def workload_config(model: str, n_blocks: int, bits: int, batch: int, world: int) -> dict:
-    """The config both arms report (same workload, same keys)."""
-    from paper_2602_03537_b200.model import KINDS, SHAPES, tp_layer_dims
+def _shapes():
+    """paper_2602_03537_b200/shapes.py loaded by path: the reference arm shares
+    the workload definition without importing the package (which maps libmatq.so)."""
+    import importlib.util
 
-    dims = ", ".join("%s %dx%d" % ((k,) + tp_layer_dims(SHAPES[model], k, 1)) for k in KINDS)
+    if "_mq_shapes" not in sys.modules:
+        spec = importlib.util.spec_from_file_location(
+            "_mq_shapes", os.path.join(ROOT, "paper_2602_03537_b200", "shapes.py"))
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["_mq_shapes"] = mod
+        spec.loader.exec_module(mod)
+    return sys.modules["_mq_shapes"]
+
+
+def workload_config(model: str, n_blocks: int, bits: int, batch: int, world: int) -> dict:
+    """The config both arms report (same workload, same keys, same values)."""
+    sh = _shapes()
+    shape = sh.SHAPES[model]
+    dims = ", ".join("%s %dx%d" % ((k,) + sh.full_layer_dims(shape, k)) for k in sh.KINDS)
     return {"workload": "%s linear stack decode: %d blocks x {%s}, int8 parent sliced to r bits "
                         "(rounding MSB slice), G=128" % (model, n_blocks, dims),
             "model": model, "bits": bits, "batch": batch, "group_size": 128,
@@ -118,12 +132,16 @@ class CpuReference:
     """One Llama-3.1-8B block (qkv, o, gate_up, down) on the host cores.
 
     r in {2,3,4}: the reference's compiled nq_gemv/nq_gemm (oracle/_ref, driven
-    as kernels/_core.pyx:24-64 drives it), rows spread over `threads` host
-    threads (the kernel walks rows independently, packed_kernels.c:88; ctypes
-    releases the GIL).  r in {6,8}: the reference has no packed kernel
+    as kernels/_core.pyx:24-64 drives it); with threads > 1 the rows are spread
+    over host threads (the kernel walks rows independently, packed_kernels.c:88;
+    ctypes releases the GIL), threads = 1 is the reference as shipped (one
+    core, _core.pyx:47-63).  r in {6,8}: the reference has no packed kernel
     (matmul.py:55-56); its bench baseline, a dense fp32 GEMV on the
     dequantised child (matmul.py:164-165), is used instead.
     Preparation (slice + pack) is untimed, as in the reference bench.
+    ``step_seconds`` runs a whole decode step: the block's four linears once per
+    model block (32 for Llama-3.1-8B; the blocks share shapes, so one block's
+    weights are reused -- 110 MB at r = 4, beyond any host LLC).
     """
 
     def __init__(self, r: int, batch: int, threads: int, model: str = "Llama-3.1-8B"):
@@ -131,14 +149,15 @@ class CpuReference:
         from concurrent.futures import ThreadPoolExecutor
 
         from oracle import oracle as O
-        from paper_2602_03537_b200.model import KINDS, SHAPES, tp_layer_dims
 
+        sh = _shapes()
+        shape = sh.SHAPES[model]
         self.r, self.threads, self.O = r, threads, O
-        self.n_blocks = SHAPES[model].n_layers
+        self.n_blocks = shape.n_layers
         rng = np.random.default_rng(0)
         self.layers = []
-        for kind in KINDS:
-            N, K = tp_layer_dims(SHAPES[model], kind, 1)
+        for kind in sh.KINDS:
+            N, K = sh.full_layer_dims(shape, kind)
             parent = rng.integers(0, 256, size=(N, K), dtype=np.uint8)
             scales = rng.uniform(0.005, 0.02, size=(N, K // 128)).astype(np.float32)
             child = O.slice_codes(parent, 8, r)
@@ -152,13 +171,20 @@ class CpuReference:
                 self.layers.append(("dense", N, W, None, None, None, X))
             del parent, child
         self.ref = O.RefKernels() if r <= 4 else None
-        self.pool = ThreadPoolExecutor(max_workers=threads)
+        self.pool = ThreadPoolExecutor(max_workers=threads) if threads > 1 else None
         self.kind = "reference" if r <= 4 else "port"
         self.backend = (self.ref.backend_name() if self.ref
                         else "dense-fp32 GEMV (oracle C; the reference bench's baseline)")
 
     def _layer(self, ly):
         kind, N = ly[0], ly[1]
+        if self.pool is None:
+            if kind == "packed":
+                _, _, base, b2, b3, seff, X = ly
+                self.ref.packed_matmul(base, b2, b3, seff, X, self.r, 128)
+            else:
+                self.O.dense_gemm(ly[6], ly[2])
+            return
         step = -(-N // max(1, self.threads * 4))
         bounds = [(lo, min(N, lo + step)) for lo in range(0, N, step)]
         if kind == "packed":
@@ -177,11 +203,25 @@ class CpuReference:
             self._layer(ly)
         return time.perf_counter() - t0
 
+    def step_seconds(self) -> float:
+        """One decode step: every block's four linears (no extrapolation)."""
+        t0 = time.perf_counter()
+        for _ in range(self.n_blocks):
+            for ly in self.layers:
+                self._layer(ly)
+        return time.perf_counter() - t0
+
     def close(self):
-        self.pool.shutdown()
+        if self.pool is not None:
+            self.pool.shutdown()
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation of the path
+    (oracle/_ref = its packed_kernels.c, compiled unmodified; r in {6, 8}: its
+    bench's dense fp32 baseline), all host threads, on the GPU arm's workload,
+    config, metric and unit.  Every timed step is a whole decode step (32
+    blocks x 4 linears).  Nothing from paper_2602_03537_b200 is imported."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -189,27 +229,138 @@ def run_reference(args):
     r = args.bits
     ref = CpuReference(r, args.batch, threads, args.model)
     samples = []
+    t_all = time.perf_counter()
     for i in range(args.warmup + args.steps):
-        t = ref.block_seconds()
+        t = ref.step_seconds() if i >= args.warmup else ref.block_seconds()  # warm-up: one block
         if i >= args.warmup:
             samples.append(t)
     ref.close()
-    kind, backend = ref.kind, ref.backend
-    per_block = statistics.median(samples)
-    tok_s = args.batch / (ref.n_blocks * per_block)
+    total = sum(samples)
+    tok_s = args.batch * len(samples) / total
     line = {
         "impl": "reference", "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ref.n_blocks * per_block * 1e3,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(samples) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "fp32",
         "data": "synthetic",
         "config": workload_config(args.model, ref.n_blocks, r, args.batch, args.gpus),
-        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": "one full transformer block (4 linears, all rows) per step, "
-                                   "x32 blocks; backend %s" % backend},
+        "cpu_baseline": {"value": tok_s, "unit": UNIT, "cores": threads, "kind": ref.kind,
+                         "sample": "every timed step is one whole decode step: %d blocks x 4 linears, all "
+                                   "rows (one block's weights reused per block); warm-up steps run one "
+                                   "block; backend %s, rows split over %d threads" % (
+                                       ref.n_blocks, ref.backend, threads)},
         "e2e": {"value": tok_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t_all,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def c1_leg(torch, mq, clocks, peak, cpu: bool, bits=(8, 4, 2), N=4096, K=4096, reps=10):
+    """BASELINE C1, the case the reference's own bench runs (matmul.py:123-192,
+    cli.py:237-245): one 4096x4096 linear, int8 parent sliced to r, G = 128,
+    B = 1.  L2-cold: 40 weight replicas (each launch reads >= 6.5 MiB; 40 x
+    that >= 2 x the 126 MB L2) cycled inside one CUDA graph of K3 launches
+    (PDL).  Beside it, the reference's compiled kernel on 1 core (r in {4, 2};
+    r = 8: its bench's dense fp32 GEMV), median of 7 after 1 warm-up
+    (matmul.py:138-145)."""
+    import numpy as np
+
+    from paper_2602_03537_b200.device import algorithmic_bytes
+
+    nrep = 40
+    pts = [mq.PlaneTensor.random_parent(N, K, 128, seed=1000 + i) for i in range(nrep)]
+    X = torch.randn(1, K, device="cuda").to(torch.bfloat16)
+    Y = torch.empty(1, N, device="cuda", dtype=torch.bfloat16)
+    s = torch.cuda.Stream()
+    out = {}
+    for r in bits:
+        with torch.cuda.stream(s):
+            for pt in pts:
+                pt.gemv(X, r, out=Y, pdl=True, stream=s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for pt in pts:
+                pt.gemv(X, r, out=Y, pdl=True, stream=s)
+        with torch.cuda.stream(s):
+            for _ in range(3):
+                g.replay()
+        s.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks.active(True)
+        e0.record(s)
+        with torch.cuda.stream(s):
+            for _ in range(reps):
+                g.replay()
+        e1.record(s)
+        e1.synchronize()
+        clocks.active(False)
+        t = e0.elapsed_time(e1) / 1e3 / (reps * nrep)
+        nb = algorithmic_bytes(N, K, 1, r, pts[0].planes_read(r), 128)
+        rec = {"us": t * 1e6, "GBps": nb / t / 1e9, "frac": nb / t / 1e9 / peak, "bytes": nb,
+               "ideal_r_bytes": algorithmic_bytes(N, K, 1, r, r, 128)}
+        if cpu:
+            from oracle import oracle as O
+
+            rng = np.random.default_rng(0)
+            parent = rng.integers(0, 256, size=(N, K), dtype=np.uint8)
+            scales = rng.uniform(0.005, 0.02, size=(N, K // 128)).astype(np.float32)
+            xs = rng.standard_normal((1, K)).astype(np.float32)
+            child = O.slice_codes(parent, 8, r)
+            seff = O.scale_eff(scales, 8, r)
+            if r <= 4:
+                ref = O.RefKernels()
+                base, b2, b3 = O.pack_child(child, r)
+                fn = lambda: ref.packed_matmul(base, b2, b3, seff, xs, r, 128)  # noqa: E731
+                kind = "reference (%s)" % ref.backend_name()
+            else:
+                W = O.dense_f32(child, seff, 128, r)
+                fn = lambda: O.dense_gemm(xs, W)  # noqa: E731
+                kind = "port (dense fp32 GEMV, the reference bench baseline)"
+            fn()
+            ts = []
+            for _ in range(7):
+                t0 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t0)
+            rec["cpu_us"] = statistics.median(ts) * 1e6
+            rec["cpu_kind"] = kind
+            rec["cpu_cores"] = 1
+            rec["vs_cpu"] = rec["cpu_us"] / rec["us"]
+        out["r%d" % r] = rec
+        del g
+    del pts
+    torch.cuda.empty_cache()
+    return {"shape": [N, K], "batch": 1, "group_size": 128,
+            "l2": "cold: 40 replicas cycled in one graph", "per_bits": out}
+
+
+def sweep_leg(torch, stack, clocks, peak, batches, configs, steps=10, warmup=3):
+    """Decode batch sweep of a LinearStack (BASELINE C2 uniform r / C3
+    heterogeneous): the default dispatch (K3S or the per-layer K3 graph)."""
+    out = {}
+    for B in batches:
+        stack.set_batch(B)
+        for label, cfg in configs:
+            stack.capture(cfg)
+            for _ in range(warmup):
+                stack.step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            clocks.active(True)
+            e0.record(stack.stream)
+            for _ in range(steps):
+                stack.step()
+            e1.record(stack.stream)
+            e1.synchronize()
+            clocks.active(False)
+            t = e0.elapsed_time(e1) / 1e3 / steps
+            nb = stack.step_bytes(stack.config)
+            out["B%d_%s" % (B, label)] = {
+                "tok_s": B / t, "ms_per_step": t * 1e3, "GBps": nb / t / 1e9, "frac": nb / t / 1e9 / peak,
+                "path": "K3S" if stack.launches_per_step() == 1 else "K3 graph"}
+    stack.set_batch(1)
+    return out
 
 
 def prefill_leg(torch, mq, clocks, batches=(64, 256, 1024), bits=(4, 8), reps=10):
@@ -361,10 +512,26 @@ def main():
     ap.add_argument("--no-prefill", action="store_true", help="skip the C4 tcgen05 prefill leg")
     ap.add_argument("--no-full", action="store_true", help="skip the full-model decode leg")
     ap.add_argument("--no-quant", action="store_true", help="skip the quantiser-search leg")
+    ap.add_argument("--no-c1", action="store_true", help="skip the C1 single-layer leg")
+    ap.add_argument("--no-c2", action="store_true", help="skip the C2 / C3 batch sweeps")
     ap.add_argument("--model", default="Llama-3.1-8B", help="Llama-3.1-8B | Qwen3-14B | Phi-3-Medium")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch this command under torch.distributed.run
+        import socket
+        import subprocess
+
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+               str(args.gpus), "--master-addr", "127.0.0.1", "--master-port", str(port),
+               os.path.abspath(__file__)] + sys.argv[1:]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")  # rank / channel / NVLS lines go to stderr
+        return subprocess.call(cmd, env=env)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -541,6 +708,11 @@ def main():
                 stack.layers[i] = (n, kind, pt)
             torch.cuda.empty_cache()
 
+    # C2: uniform r, decode batch 1-16
+    c2 = None
+    if not args.no_c2 and world == 1:
+        c2 = sweep_leg(torch, stack, clocks, peak, (1, 2, 4, 8, 16), [("r%d" % b, b) for b in LADDER])
+
     # C3: heterogeneous per-layer bit-widths (EvoPress-style budget-exact 3.5-bit
     # config over the unfused linears, the reference's own moves), CUDA graph of
     # the unfused stack: one launch per linear, each at its own r (faster here
@@ -573,6 +745,9 @@ def main():
                   "stack_GBps": hb / (hsec / args.steps) / 1e9,
                   "stack_frac": hb / (hsec / args.steps) / 1e9 / peak,
                   "config": "budget_config(3.5, seed=0, mutations=200) over 224 unfused linears"}
+        if not args.no_c2:
+            hetero["batch_sweep"] = sweep_leg(torch, hs, clocks, peak, (1, 8, 16, 32),
+                                              [("hetero3.5", cfg.assignment)])
         del hs
         torch.cuda.empty_cache()
 
@@ -613,6 +788,13 @@ def main():
         del dec
         torch.cuda.empty_cache()
 
+    # C1: one 4096x4096 linear (the reference bench's case), L2-cold
+    c1 = None
+    if not args.no_c1 and world == 1:
+        stack.graph = None
+        torch.cuda.empty_cache()
+        c1 = c1_leg(torch, mq, clocks, peak, cpu=not args.no_cpu)
+
     # C4: prefill on the tcgen05 path (K4), Qwen3-14B linear shapes, per layer
     prefill = None
     if not args.no_prefill and world == 1:
@@ -626,15 +808,17 @@ def main():
     clk = clocks.summary()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        ref = CpuReference(r, args.batch, threads, args.model)
+        # the reference as shipped: its compiled kernel on ONE core (_core.pyx:47-63 is
+        # single-threaded, matmul.py:164 threadpool_limits(1)); one whole decode step
+        ref = CpuReference(r, args.batch, 1, args.model)
         ref.block_seconds()  # warm-up
-        per_block = statistics.median(ref.block_seconds() for _ in range(3))
+        secs = ref.step_seconds()
         ref.close()
-        cpu = {"value": args.batch / (ref.n_blocks * per_block), "unit": UNIT, "cores": threads,
-               "kind": ref.kind,
-               "sample": "one full Llama-3.1-8B block (4 linears, all rows) at r=%d, median of 3, "
-                         "x32 blocks; %s" % (r, ref.backend)}
+        cpu = {"value": args.batch / secs, "unit": UNIT, "cores": 1, "kind": ref.kind,
+               "host_cores": os.cpu_count(),
+               "sample": "one whole decode step (%d blocks x 4 linears, all rows, one block's weights "
+                         "reused per block) at r=%d on 1 of %d host cores; %s" % (
+                             ref.n_blocks, r, os.cpu_count() or 1, ref.backend)}
 
     head = results[args.bits]
     bytes_tok = head["bytes_per_step"] * world / args.batch
@@ -643,13 +827,13 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init int8 parents, N(0,1) bf16 activations)",
-        "config": dict(workload_config(args.model, n_blocks, args.bits, args.batch, world), **{
-                   "mode": "P (parent resident, sliced on the fly)",
-                   "l2": "inputs > L2 (%.1f GB of planes read per step vs 126 MB L2)" % (
-                       head["bytes_per_step"] / 1e9),
-                   "graph": ("CUDA graph of 1 K3S launch/step (persistent whole-step kernel)"
-                             if stack.launches_per_step() == 1 else
-                             "CUDA graph, %d K3 launches/step, PDL" % stack.launches_per_step())}),
+        "config": workload_config(args.model, n_blocks, args.bits, args.batch, world),
+        "run": {"mode": "P (parent resident, sliced on the fly)",
+                "l2": "inputs > L2 (%.1f GB of planes read per step vs 126 MB L2)" % (
+                    head["bytes_per_step"] / 1e9),
+                "graph": ("CUDA graph of 1 K3S launch/step (persistent whole-step kernel)"
+                          if stack.launches_per_step() == 1 else
+                          "CUDA graph, %d K3 launches/step, PDL" % stack.launches_per_step())},
         "per_bits": {str(b): {"tok_s": v["tok_s"], "ms_per_step": v["ms_per_step"],
                               "GB_per_step": v["bytes_per_step"] / 1e9,
                               "stack_GBps": v["bytes_per_step"] / (v["ms_per_step"] / 1e3) / 1e9,
@@ -663,6 +847,8 @@ def main():
         "roofline": roof,
         "roofline_k3_gate_up": roof_k3,
         "full_model_decode": full,
+        "c1_single_linear": c1,
+        "c2_batch_sweep": c2,
         "hetero_c3": hetero,
         "prefill_c4": prefill,
         "quantizer_8f4": quant,

@@ -19,66 +19,23 @@ NCCL all-reduce of the (B, hidden) partial.  ``tp = 1`` has no collective.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
-
 import torch
 
 from . import _lib
 from .device import LADDER, PlaneTensor, algorithmic_bytes, reserve_workspace
-
-
-@dataclass(frozen=True)
-class DecoderShape:
-    name: str
-    hidden: int
-    intermediate: int
-    n_heads: int
-    n_kv_heads: int
-    head_dim: int
-    n_layers: int
-
-    @property
-    def qkv_out(self) -> int:
-        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
-
-    @property
-    def q_out(self) -> int:
-        return self.n_heads * self.head_dim
-
-
-LLAMA31_8B = DecoderShape("Llama-3.1-8B", 4096, 14336, 32, 8, 128, 32)
-QWEN3_14B = DecoderShape("Qwen3-14B", 5120, 17408, 40, 8, 128, 40)
-PHI3_MEDIUM = DecoderShape("Phi-3-Medium", 5120, 17920, 40, 10, 128, 40)
-SHAPES = {s.name: s for s in (LLAMA31_8B, QWEN3_14B, PHI3_MEDIUM)}
-
-KINDS = ("qkv", "o", "gate_up", "down")
-# unfused linears (heterogeneous configs assign r per q / k / v / gate / up, BASELINE C3)
-KINDS_UNFUSED = ("q", "k", "v", "o", "gate", "up", "down")
-
-
-def layer_names(shape: DecoderShape, fused: bool = True) -> list[str]:
-    kinds = KINDS if fused else KINDS_UNFUSED
-    return ["layers.%d.%s" % (i, k) for i in range(shape.n_layers) for k in kinds]
-
-
-def full_layer_dims(shape: DecoderShape, kind: str) -> tuple[int, int]:
-    """(N, K) of an unsharded linear (fused qkv / gate_up, or unfused)."""
-    h, inter, hd = shape.hidden, shape.intermediate, shape.head_dim
-    dims = {"qkv": (shape.qkv_out, h), "o": (h, shape.q_out), "gate_up": (2 * inter, h),
-            "down": (h, inter), "q": (shape.q_out, h), "k": (shape.n_kv_heads * hd, h),
-            "v": (shape.n_kv_heads * hd, h), "gate": (inter, h), "up": (inter, h)}
-    return dims[kind]
+from .shapes import (KINDS, KINDS_UNFUSED, LLAMA31_8B, PHI3_MEDIUM, QWEN3_14B, SHAPES,  # noqa: F401
+                     DecoderShape, full_layer_dims, layer_names)
 
 
 def tp_layer_dims(shape: DecoderShape, kind: str, tp: int, rank: int = 0) -> tuple[int, int]:
-    """(N, K) of rank ``rank``'s shard (tp.shard_plan: rows for column-parallel,
-    whole scale groups of K for row-parallel)."""
-    N, K = full_layer_dims(shape, kind)
+    """(N, K) of rank ``rank``'s shard (tp.decoder_plan: q heads + their kv
+    heads / gate + up rows for column-parallel, whole scale groups of K for
+    row-parallel)."""
     if tp == 1:
-        return N, K
-    from .tp import shard_plan
+        return full_layer_dims(shape, kind)
+    from .tp import decoder_plan
 
-    return shard_plan(kind, N, K, tp, rank).shape
+    return decoder_plan(shape, kind, tp, rank).shape
 
 
 def _gain_matched_scales(K: int):
@@ -119,20 +76,31 @@ class LinearStack:
                 pt = PlaneTensor.random_parent(N, K, group_size, seed=sd, scale_range=sr, signed_rows=True)
                 self.layers.append(("layers.%d.%s" % (i, kind), kind, pt))
                 self.parent_seeds.append((sd, sr, True))
-        h = shape.hidden
+        self.stream = torch.cuda.Stream()
+        self.set_batch(batch)
+        self.graph = None
+        self.program = None
+        self.config: dict[str, int] = {}
+
+    def set_batch(self, batch: int) -> None:
+        """(Re)allocate the activation buffers for decode batch ``batch``; the
+        resident weights are untouched.  Drops any captured step."""
+        if batch < 1 or batch > 32:
+            raise ValueError("decode batch must lie in [1, 32]")
+        self.B = batch
+        kinds = KINDS if self.fused else KINDS_UNFUSED
+        h = self.shape.hidden
         dev = torch.device("cuda", torch.cuda.current_device())
+        self.graph = None
+        self.program = None
         self.x = torch.zeros((batch, h), dtype=torch.bfloat16, device=dev)
         self.bufs = {}
         for name, kind, pt in self.layers[:len(kinds)]:
             self.bufs[kind] = torch.zeros((batch, pt.N), dtype=torch.bfloat16, device=dev)
         self.x_host = torch.zeros((batch, h), dtype=torch.bfloat16, pin_memory=True)
         self.y_host = torch.zeros((batch, h), dtype=torch.bfloat16, pin_memory=True)
-        self.stream = torch.cuda.Stream()
         need = max(pt.workspace_bytes(batch) for _, _, pt in self.layers)
         reserve_workspace(need, stream=self.stream)
-        self.graph = None
-        self.program = None
-        self.config: dict[str, int] = {}
 
     # ------------------------------------------------------------------
     @property
