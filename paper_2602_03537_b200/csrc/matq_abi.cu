@@ -437,6 +437,7 @@ struct StackPlanHost {  // the opaque host plan (mq_stack_plan_bytes)
     int r, nplanes, nt, grid;
     size_t smem;
     size_t ws_bytes;
+    size_t ll_bytes;
 };
 // K3S per-layer decomposition: K chunks S (activation staging bounded by
 // kXsMax), the chunk's row tiles split contiguously over cpc = sms / S CTAs,
@@ -472,18 +473,20 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
     return best_c;
 }
 
-size_t stack_ws_layout(int n_layers, size_t partial_bytes, size_t* off_done, size_t* off_partials) {
-    // [tickets 64 KB][done counters n + launch counter][published max |y| n][partials]
+// workspace: [tickets 64 KB][done counters n + launch counter][LL words][partials]
+size_t stack_ws_layout(int n_layers, size_t ll_bytes, size_t partial_bytes, size_t* off_done, size_t* off_ll,
+                       size_t* off_partials) {
     *off_done = kTicketBytes;
-    *off_partials = kTicketBytes + (((size_t)(2 * n_layers + 1) * 8 + 255) & ~(size_t)255);
+    *off_ll = kTicketBytes + (((size_t)(n_layers + 1) * 8 + 255) & ~(size_t)255);
+    *off_partials = *off_ll + ((ll_bytes + 255) & ~(size_t)255);
     return *off_partials + partial_bytes;
 }
 
-// fp16 staging in one pass: layer i's X must lie entirely inside the output of
-// an earlier layer j (same row stride, every row's columns within j's N) that
-// no layer between j and i overwrote in part -- then j's published max |y|
-// bounds max |x|.  Returns j or -1.
-int stack_amax_src(const mq_stack_layer* layers, int i, int B) {
+// Which earlier layer produces layer i's X?  The latest layer j whose Y overlaps
+// X decides: X must lie entirely inside Y_j (same row stride, even element
+// offset) -- then layer i polls j's LL words -- else the stack cannot order the
+// two (-2).  -1: no earlier layer writes X (activations from outside the step).
+int stack_x_producer(const mq_stack_layer* layers, int i, int B, size_t* elem_off) {
     const mq_stack_layer& in = layers[i];
     auto lo = [](const void* p) { return reinterpret_cast<uintptr_t>(p); };
     const uintptr_t x0 = lo(in.X), x1 = x0 + 2 * ((size_t)(B - 1) * in.ldx + in.K);
@@ -492,10 +495,16 @@ int stack_amax_src(const mq_stack_layer* layers, int i, int B) {
         const uintptr_t y0 = lo(o.Y), y1 = y0 + 2 * ((size_t)(B - 1) * o.ldy + o.N);
         if (x1 <= y0 || y1 <= x0) continue;  // no overlap: look further back
         const size_t e = (x0 - y0) / 2;  // X's first element inside Y (row 0: both have B rows)
-        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 2 == 0 && e + (size_t)in.K <= (size_t)o.N;
-        return inside ? j : -1;  // the latest writer overlapping X decides
+        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 4 == 0 && e + (size_t)in.K <= (size_t)o.N;
+        *elem_off = e;
+        return inside ? j : -2;
     }
     return -1;
+}
+bool stack_overlap(const void* a, int lda, int na, const void* b, int ldb, int nb, int B) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(a), a1 = a0 + 2 * ((size_t)(B - 1) * lda + na);
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(b), b1 = b0 + 2 * ((size_t)(B - 1) * ldb + nb);
+    return !(a1 <= b0 || b1 <= a0);
 }
 }  // namespace
 
@@ -524,7 +533,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     const int nt = B <= 8 ? 1 : 2;
     int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1, cl_tiles = 0, nrt_max = 1;
     bool zp_any = false, uniform = true;
-    size_t partials = 0, stage_max = 0;
+    size_t partials = 0, stage_max = 0, ll_bytes = 0;
+    std::vector<int> war((size_t)n_layers, -1);
     // staging holds the most copies any layer stages and the ring the largest
     // stage: every layer's K chunk is sized for both, so any layer fits
     for (int i = 0; i < n_layers; ++i) {
@@ -576,6 +586,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
         mq::StackLayer& t = T[i];
         memset(&t, 0, sizeof(t));
+        if (war[(size_t)i] == i) t.ext_pub = 1;
         t.blob = in.blob;
         t.step_words = L.step_words;
         t.X = reinterpret_cast<const uint16_t*>(in.X);
@@ -593,23 +604,46 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         t.out_scale = in.out_scale;
         t.r = ri;
         t.stage_bytes = npl * 512 + 128;
-        t.amax_src = (ri == 4 || ri == 8) && nt == 1 ? stack_amax_src(layers, i, B) : -1;
-        if (t.amax_src >= 0) T[t.amax_src].pub_amax = 1;
+        t.xll = -1;
+        t.yll = -1;
+        t.war_wait = -1;
+        size_t e = 0;
+        const int j = stack_x_producer(layers, i, B, &e);
+        if (j == -2)
+            return fail(MQ_ERR_INVALID, "layer %d reads part of an earlier layer's output in another layout", i);
+        if (j >= 0) {
+            if (T[j].yll < 0) {  // j's output gets LL words: [B][pad16(N_j) / 2]
+                T[j].yll = (long long)(ll_bytes / 8);
+                T[j].ldyll = T[j].Np / 2;
+                ll_bytes += (size_t)B * T[j].ldyll * 8;
+            }
+            t.xll = T[j].yll + (long long)(e / 2);
+            t.ldxll = T[j].ldyll;
+        } else {
+            // activations from outside the step: a later layer overwriting them waits
+            // until every CTA staged them
+            for (int k = i; k < n_layers; ++k)
+                if (stack_overlap(in.X, in.ldx, in.K, layers[k].Y, layers[k].ldy, layers[k].N, B)) {
+                    t.ext_pub = 1;
+                    war[(size_t)k] = std::max(war[(size_t)k], i);
+                }
+        }
         cs_max = std::max(cs_max, c.cs);
         if (pair && c.S == 2) cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
         if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
     }
+    for (int i = 0; i < n_layers; ++i) T[i].war_wait = war[(size_t)i];
     mq::StackParams& p = P->p;
     p.n_layers = n_layers;
     p.B = B;
     p.xs_stride = cs_max * 256 + 8;
     p.xcopy_stride = B * p.xs_stride;
     p.cs_off = (int)(((size_t)nstage_max * p.xcopy_stride * 2 + 15) & ~(size_t)15);
-    const size_t zc_bytes = zp_any ? (size_t)2 * cs_max * nt * 8 * 4 : 0;
+    // [2 groups per step][nt * 8 rows] floats; fp16 layers {c / lambda, 1 / lambda} pairs
+    const size_t zc_bytes = zp_any ? (size_t)2 * cs_max * nt * 8 * 4 * 2 : 0;
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
-    p.flag_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
-    p.table_off = p.flag_off;
+    p.table_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
     p.cl_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
     p.cluster = pair ? 1 : 0;
     p.cl_tiles = cl_tiles;
@@ -626,8 +660,9 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     P->nplanes = nplanes;
     P->nt = nt;
     P->grid = sm_count();
-    size_t od, op;
-    P->ws_bytes = stack_ws_layout(n_layers, partials, &od, &op);
+    size_t od, ol, op;
+    P->ll_bytes = ll_bytes;
+    P->ws_bytes = stack_ws_layout(n_layers, ll_bytes, partials, &od, &ol, &op);
     *workspace_bytes = P->ws_bytes;
     return MQ_OK;
 }
@@ -659,14 +694,14 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
     if (workspace_bytes < P->ws_bytes)
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
     mq::StackParams p = P->p;
-    size_t od, op;
-    stack_ws_layout(p.n_layers, 0, &od, &op);
+    size_t od, ol, op;
+    stack_ws_layout(p.n_layers, P->ll_bytes, 0, &od, &ol, &op);
     char* w = reinterpret_cast<char*>(workspace);
     p.layers = reinterpret_cast<const mq::StackLayer*>(table_dev);
     p.tickets = reinterpret_cast<int*>(w);
     p.done = reinterpret_cast<unsigned long long*>(w + od);
     p.launch_ctr = p.done + p.n_layers;
-    p.amax = p.launch_ctr + 1;
+    p.ll = reinterpret_cast<unsigned long long*>(w + ol);
     p.ws = reinterpret_cast<float*>(w + op);
 #ifdef MQ_GEMV_TIMING
     static unsigned long long* sbuf = nullptr;
@@ -687,36 +722,41 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
     return cuda_status(e, "mq_stack_run");
 }
 
-// The step counter behind the layer barriers: launch_ctr = launches * grid and
-// every done[l] = launches * grid between steps.  set = 1 writes `*launches`
-// (tests seed it near 2^32 to show the 64-bit counters do not wrap), set = 0
-// reads it back.  Synchronous.
+// The step counter: launch_ctr = launches * grid between steps (it also gives
+// the LL tag of each step), done[l] the external-staging counters.  set = 1
+// writes `*launches` to all of them and clears the LL words, so a re-based
+// counter can never meet a stale tag (tests seed it near 2^32 to show the
+// 64-bit counters do not wrap); set = 0 reads it back.  Synchronous.
 int mq_stack_epoch(const void* plan_host, void* workspace, size_t workspace_bytes, unsigned long long* launches,
                    int set, void* stream) {
     if (!plan_host || !workspace || !launches) return fail(MQ_ERR_INVALID, "null pointer");
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
     if (workspace_bytes < P->ws_bytes)
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
-    size_t od, op;
-    stack_ws_layout(P->p.n_layers, 0, &od, &op);
+    size_t od, ol, op;
+    stack_ws_layout(P->p.n_layers, P->ll_bytes, 0, &od, &ol, &op);
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(workspace) + od);
     const int n = P->p.n_layers + 1;
     cudaStream_t s = (cudaStream_t)stream;
     std::vector<unsigned long long> h((size_t)n);
+    const unsigned long long grid = (unsigned long long)P->grid;
     cudaError_t e;
     if (set) {
-        for (auto& v : h) v = *launches * (unsigned long long)P->grid;
+        for (auto& v : h) v = *launches * grid;
         e = cudaMemcpyAsync(ctr, h.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess && P->ll_bytes)
+            e = cudaMemsetAsync(reinterpret_cast<char*>(workspace) + ol, 0, P->ll_bytes, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         return cuda_status(e, "mq_stack_epoch");
     }
     e = cudaMemcpyAsync(h.data(), ctr, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_status(e, "mq_stack_epoch");
+    const unsigned long long lc = h[(size_t)n - 1];
     for (int i = 0; i < n; ++i)
-        if (h[i] != h[0] || h[i] % (unsigned long long)P->grid)
-            return fail(MQ_ERR_INVALID, "stack counters inconsistent (layer %d: %llu vs %llu)", i, h[i], h[0]);
-    *launches = h[0] / (unsigned long long)P->grid;
+        if (h[i] > lc || h[i] % grid)
+            return fail(MQ_ERR_INVALID, "stack counters inconsistent (layer %d: %llu vs %llu)", i, h[i], lc);
+    *launches = lc / grid;
     return MQ_OK;
 }
 

@@ -32,17 +32,20 @@ namespace mq {
 struct __align__(8) StackLayer {
     const uint32_t* blob;
     long long step_words;
-    const uint16_t* X;  // bf16 [B][ldx]
+    const uint16_t* X;  // bf16 [B][ldx] (read when xll is null: activations from outside the step)
     uint16_t* Y;        // bf16 [B][ldy]
-    int ldx, ldy;
+    long long xll;  // word offset in StackParams::ll of the producing layer's LL output at X's first
+                    // column, or -1 (X from outside the step: plain loads)
+    long long yll;  // word offset of this layer's LL output [B][ldyll], or -1 (no later layer reads it)
+    int ldx, ldy, ldxll, ldyll;     // ldxll / ldyll in 8-byte words
     int N, Np, K, nsteps, n_rt;
     int S, cs, cpc;  // K chunks, steps per chunk, CTAs per chunk
     float out_scale;
     int r;            // slice width (the mixed kernel dispatches on it)
     int stage_bytes;  // one ring stage: 128 B of scales + the planes read at r
-    int amax_src;     // fp16 staging: the earlier layer whose output holds all of X (its max |y| is
-                      // published), or -1 (external X: the staging measures max |x| in a first pass)
-    int pub_amax;     // publish max |y| of this layer's output (a later fp16 layer reads it)
+    int ext_pub;      // X comes from outside the step and a later layer overwrites it: count the
+                      // CTAs that finished staging it (done[l])
+    int war_wait;     // this layer overwrites layer war_wait's external X: wait until every CTA staged it, or -1
 };
 
 struct StackParams {
@@ -54,7 +57,6 @@ struct StackParams {
     int cs_off;        // byte offset of the zero-point constants
     int xs_bytes;      // bytes of the staging area (activations + constants + partial slots)
     int slot_off;      // byte offset of the per-warp partial-tile slots [16][32 lanes][NT * 4]
-    int flag_off;      // (unused)
     int table_off;     // byte offset of the shared-memory copy of the layer table
     int stages;        // per-warp ring depth
     int stage_stride;  // bytes per ring slot (the largest stage of the stack)
@@ -63,9 +65,9 @@ struct StackParams {
     int cl_tiles;      // most row tiles a CTA holds in an S == 2 layer
     float* ws;         // split-K partials (max over layers)
     int* tickets;      // split-K tickets, self-resetting
-    unsigned long long* done;  // [n_layers] monotone completion counters (64-bit: never wrap)
+    unsigned long long* done;  // [n_layers] monotone external-staging counters (64-bit: never wrap)
     unsigned long long* launch_ctr;
-    unsigned long long* amax;  // [n_layers] (step tag << 32) | float bits of max |y|, atomicMax-published
+    unsigned long long* ll;      // LL activation words of every producing layer (workspace)
     unsigned long long* dbg_ts;  // MQ_GEMV_TIMING builds: [n_layers][148][8] globaltimer stamps
 };
 
@@ -89,6 +91,9 @@ __device__ __forceinline__ unsigned long long stack_gtimer() {
 #endif
 #ifndef MQ_STACK_SPIN_NS
 #define MQ_STACK_SPIN_NS 0
+#endif
+#ifndef MQ_LL_SPIN_NS
+#define MQ_LL_SPIN_NS 0
 #endif
 
 constexpr int kStackWarps = 15;                      // consumer (decode + MMA) warps
@@ -314,10 +319,190 @@ __device__ __noinline__ void stack_producer(RingCtx rc) {
 
 struct StackShared {
     unsigned long long gen;
-    unsigned amax_bits;  // F16: the chunk's max |x| (float bits)
-    float inv_lambda;    // F16: 1 / the activation scale
-    int amax_ok;         // F16: amax_bits came from the producing layer (one staging pass)
+    uint32_t tag;  // this step's LL tag, in [1, 2^32 - 1]
 };
+
+// LL (low-latency) activation hand-off between layers.  A layer whose output a
+// later layer reads also stores it as 8-byte words {bf16 y[2i], bf16 y[2i+1],
+// tag} (tag = this step's id); the consumer polls its words until every tag
+// matches.  The data IS the flag (the LL protocol of NCCL): 8-byte accesses are
+// single-copy atomic, so no grid barrier, no release/acquire fence and no
+// counter polling sit between two layers, and a CTA starts layer l+1 as soon as
+// the words of ITS K chunk exist.
+__device__ __forceinline__ void st_ll(unsigned long long* p, uint32_t data, uint32_t tag) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(((unsigned long long)tag << 32) | data)
+                 : "memory");
+}
+__device__ __forceinline__ void ld_ll2(const unsigned long long* p, unsigned long long& a, unsigned long long& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+
+// Stage X[:, chunk] into shared memory (consumer threads).  An octet of lanes
+// takes one (batch row, 128-column group); each lane 16 columns.  From LL words
+// (polled) or plain bf16 (X from outside the step).  Per mode:
+//   F16  (r in {4, 8}, B <= 8): fp16 copies x * lambda_g * 2^-o with a power of
+//        two lambda_g = 2^(14 - e) per (row, group), max|x| in [2^e, 2^(e+1))
+//        (exact unless subnormal), and per (group, row) {c / lambda_g, 1 / lambda_g}
+//        for the output: tot += s * (acc / lambda_g - c / lambda_g);
+//   ZP   (bf16, r != 8, one n-tile): copies x * 2^-o and the zero-point constant;
+//   else a plain copy.
+template <int R, int NT, bool F16, bool ZP, int NCOPY>
+__device__ __forceinline__ void stack_stage(const StackParams& p, const StackLayer& L, uint16_t* xs, float* zc,
+                                            int col_base, int Kc, uint32_t tag) {
+    constexpr int kOctets = kConsumerThreads / 8;
+    const int ol = threadIdx.x & 7;
+    const int ngroups = Kc >> 7;
+    const int ntask = p.B * ngroups;
+    // warp-uniform trip count (full-mask shuffles: a partial mask after the
+    // divergent polling loop costs the compiler's divergent-shuffle path);
+    // octets past the last task run the shuffles on zeros and store nothing
+    const int oct0 = (threadIdx.x >> 5) * 4;
+    for (int base = oct0; base < ntask; base += kOctets) {
+        const int task = base + ((threadIdx.x >> 3) & 3);
+        const bool active = task < ntask;
+        const int b = active ? udiv_small(task, ngroups) : 0, grp = task - b * ngroups;
+        const int c0 = (grp << 7) + (ol << 4);  // column inside the chunk
+        const int col = col_base + c0;
+        uint32_t w[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = 0u;
+        const bool lo_ok = active && col < L.K, hi_ok = active && col + 8 < L.K;  // K % 8 == 0
+        if (L.xll >= 0) {
+            const unsigned long long* src = p.ll + L.xll + (long long)b * L.ldxll + (col >> 1);
+            unsigned long long v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = (unsigned long long)tag << 32;
+            for (;;) {
+                if (lo_ok) {
+                    ld_ll2(src, v[0], v[1]);
+                    ld_ll2(src + 2, v[2], v[3]);
+                }
+                if (hi_ok) {
+                    ld_ll2(src + 4, v[4], v[5]);
+                    ld_ll2(src + 6, v[6], v[7]);
+                }
+                bool ok = true;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) ok = ok && (uint32_t)(v[i] >> 32) == tag;
+                if (ok) break;
+#if MQ_LL_SPIN_NS
+                __nanosleep(MQ_LL_SPIN_NS);  // fewer L2 polls while the producing CTAs finish
+#endif
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w[i] = (uint32_t)v[i];
+        } else {
+            const uint16_t* src = L.X + (long long)b * L.ldx + col;
+            if (lo_ok) {
+                const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src));
+                w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+            }
+            if (hi_ok) {
+                const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src + 8));
+                w[4] = a.x; w[5] = a.y; w[6] = a.z; w[7] = a.w;
+            }
+        }
+        __syncwarp();
+        uint16_t* dst = xs + b * p.xs_stride + c0;
+        float x[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            x[2 * i] = __uint_as_float(w[i] << 16);
+            x[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+        if constexpr (F16) {
+            float m = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) m = fmaxf(m, fabsf(x[i]));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+            m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+            // lambda = 2^(14 - e): max|x| lambda < 2^15 < 65504 (fp16 max); e from the
+            // exponent field (m = 0: e = 0; clamped so lambda and 1 / lambda stay normal)
+            const int e = m > 0.0f ? max(-100, (int)((__float_as_uint(m) >> 23) & 0xFF) - 127) : 0;
+            const float lam = __uint_as_float((uint32_t)(127 + 14 - e) << 23);
+            const float il = __uint_as_float((uint32_t)(127 - 14 + e) << 23);
+            const int o = zp_off16<R>(((c0 & 255) & 63) >> 4);  // one field offset per 16 columns
+            float part = 0.0f;
+#pragma unroll
+            for (int cp = 0; cp < NCOPY; ++cp) {
+                const int oc = cp ? 4 : 0;
+                const float f = lam / (float)(1 << oc);
+                float y[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) y[i] = x[i] * f;  // exact in fp16 unless subnormal
+                uint32_t hw[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const __half2 h2 = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
+                    hw[i] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                if (active) {
+                    uint4* d = reinterpret_cast<uint4*>(dst + cp * p.xcopy_stride);
+                    d[0] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    d[1] = make_uint4(hw[4], hw[5], hw[6], hw[7]);
+                }
+                // the constant uses the values the MMA sees: (1024 + z 2^o) x' (pairwise sum)
+                if (oc == o) {
+#pragma unroll
+                    for (int st = 8; st >= 1; st >>= 1)
+#pragma unroll
+                        for (int i = 0; i < st; ++i) y[i] += y[i + st];
+                    part = y[0];
+                }
+            }
+            part *= 1024.0f + (float)((1 << (R - 1)) << o);
+            part += __shfl_xor_sync(0xffffffffu, part, 4);
+            part += __shfl_xor_sync(0xffffffffu, part, 2);
+            part += __shfl_xor_sync(0xffffffffu, part, 1);
+            if (active && ol == 0) {
+                float* z = zc + ((c0 >> 7) * (NT * 8) + b) * 2;
+                z[0] = part * il;
+                z[1] = il;
+            }
+        } else {
+            if (active) {
+                uint4* d = reinterpret_cast<uint4*>(dst);
+                d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+            if constexpr (ZP) {
+                // zero-point constant of the 128-column group: sum (128 2^-o + z) x; each
+                // 8 columns share the field offset o
+                float part = 0.0f;
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int cs_ = (c0 + 8 * h) & 255;
+                    const int o = zp_off<R>((cs_ & 63) >> 4, (cs_ & 15) >> 3);
+                    const float mo = 128.0f / (float)(1 << o) + (float)(1 << (R - 1));
+                    const float sx = ((x[8 * h] + x[8 * h + 1]) + (x[8 * h + 2] + x[8 * h + 3])) +
+                                     ((x[8 * h + 4] + x[8 * h + 5]) + (x[8 * h + 6] + x[8 * h + 7]));
+                    part += sx * mo;
+                }
+                part += __shfl_xor_sync(0xffffffffu, part, 4);
+                part += __shfl_xor_sync(0xffffffffu, part, 2);
+                part += __shfl_xor_sync(0xffffffffu, part, 1);
+                if (active && ol == 0) zc[(c0 >> 7) * (NT * 8) + b] = part;
+            }
+            if constexpr (NCOPY > 1) {
+                if (active) {
+#pragma unroll
+                    for (int cp = 1; cp < NCOPY; ++cp) {
+                        const float f = 1.0f / (float)(1 << zp_copy_off(R, cp));
+                        uint32_t o2[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            o2[i] = (uint32_t)f32_to_bf16_rn(x[2 * i] * f) |
+                                    ((uint32_t)f32_to_bf16_rn(x[2 * i + 1] * f) << 16);
+                        uint4* dc = reinterpret_cast<uint4*>(dst + cp * p.xcopy_stride);
+                        dc[0] = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+                        dc[1] = make_uint4(o2[4], o2[5], o2[6], o2[7]);
+                    }
+                }
+            }
+        }
+    }
+}
 
 // One layer of the step, slice width R.  Uniform stacks instantiate k_stack
 // with R fixed; heterogeneous stacks (an EvoPress configuration: per-layer r)
@@ -349,167 +534,27 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     const int Kc = L.cs * kStepCols;
     const int col_base = wp.chunk0 * kStepCols;  // every warp of the CTA shares its chunk
 
-    // ---- wait for the producer of this layer's activations ---------------
+    // ---- stage X[:, chunk]: polls the producing layer's LL words ------------
+    // (the previous layer's readers of the staging area are done: the
+    // consumer_sync that ends every layer)
     MQ_STS(l, 0);
-    if (threadIdx.x == kSyncThread) {
-        if (l > 0) {
-            while (ld_acquire_u64(p.done + l - 1) < target) {
-#if MQ_STACK_SPIN_NS
-                __nanosleep(MQ_STACK_SPIN_NS);  // fewer polls on the counter line while CTAs publish
-#endif
-            }
-        }
-        if constexpr (F16) {
-            // the producing layer published max |y| for this step: one staging pass
-            int ok = 0;
-            if (L.amax_src >= 0) {
-                const unsigned long long v = __ldcg(p.amax + L.amax_src);
-                ok = (unsigned)(v >> 32) == (unsigned)(sh.gen + 1ull);
-                if (ok) sh.amax_bits = (unsigned)v;
-            }
-            sh.amax_ok = ok;
-        }
-    }
-    consumer_sync();
     MQ_STS(l, 1);
-
-    // ---- stage X[:, chunk] (+ scaled copies for zero-point folding) --------
-    if constexpr (F16) {
-        // pass 1 (X not produced inside this step): raw bf16 into the staging tail
-        // + the chunk's max |x|; else the published max |y| and straight to pass 2
-        const uint16_t* X = L.X;
-        const int c8 = Kc >> 3;
-        const int n8 = p.B * c8;
-        uint16_t* tmp = xs + NCOPY * p.xcopy_stride;
-        const bool one_pass = sh.amax_ok != 0;
-        if (!one_pass) {
-        float amax = 0.0f;
-        constexpr int kU = 4;
-        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * kConsumerThreads) {
-            uint4 vv[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * kConsumerThreads;
-                vv[u] = make_uint4(0, 0, 0, 0);
-                if (idx < n8) {
-                    const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-                    const int col = col_base + c;
-                    if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * kConsumerThreads;
-                if (idx >= n8) break;
-                const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-                *reinterpret_cast<uint4*>(tmp + b * p.xs_stride + c) = vv[u];
-                const uint32_t* wv = reinterpret_cast<const uint32_t*>(&vv[u]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    amax = fmaxf(amax, fmaxf(fabsf(__uint_as_float(wv[e] << 16)), fabsf(__uint_as_float(wv[e] & 0xFFFF0000u))));
-            }
-        }
-#pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, s));
-        if (lane == 0) atomicMax(&sh.amax_bits, __float_as_uint(amax));  // non-negative: bits order = value order
-        consumer_sync();
-        }
-        // lambda = 2^(14 - e), max|x| in [2^e, 2^(e+1)): max|x| * lambda < 2^15 < 65504
-        const float amax_all = __uint_as_float(sh.amax_bits);
-        const int e = amax_all > 0.0f ? ilogbf(amax_all) : 0;
-        const float lam = ldexpf(1.0f, 14 - e);
-        if (threadIdx.x == 0) sh.inv_lambda = ldexpf(1.0f, e - 14);
-        // pass 2: fp16 copies x * lambda * 2^-o (exact unless subnormal) + zero-point constants
-        for (int idx = threadIdx.x; idx < n8; idx += kConsumerThreads) {
-            const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-            uint4 v;
-            if (one_pass) {
-                v = make_uint4(0, 0, 0, 0);
-                if (col_base + c < L.K) v = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col_base + c));
-            } else {
-                v = *reinterpret_cast<const uint4*>(tmp + b * p.xs_stride + c);
-            }
-            const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
-            const int cs_ = c & 255;
-            const int o = zp_off16<R>((cs_ & 63) >> 4);
-            float part = 0.0f;
-#pragma unroll
-            for (int cp = 0; cp < NCOPY; ++cp) {
-                const int oc = cp ? 4 : 0;
-                const float f = lam / (float)(1 << oc);
-                uint4 ov;
-                uint16_t* ho = reinterpret_cast<uint16_t*>(&ov);
-#pragma unroll
-                for (int e2 = 0; e2 < 8; ++e2) {
-                    const __half hh = __float2half_rn(bf16_to_f32(hv[e2]) * f);
-                    ho[e2] = __half_as_ushort(hh);
-                    // the constant uses the values the MMA will see: (1024 + z 2^o) x'
-                    if (oc == o) part += __half2float(hh);
-                }
-                *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = ov;
-            }
-            part *= 1024.0f + (float)((1 << (R - 1)) << o);
-#pragma unroll
-            for (int s = 8; s >= 1; s >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s);
-            if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
-        }
-    } else {
-        const uint16_t* X = L.X;
-        const int c8 = Kc >> 3;
-        const int n8 = p.B * c8;
-        constexpr int kU = 4;  // loads in flight per thread before the first use
-        for (int base_i = threadIdx.x; base_i < n8; base_i += kU * kConsumerThreads) {
-            uint4 vv[kU];
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * kConsumerThreads;
-                vv[u] = make_uint4(0, 0, 0, 0);
-                if (idx < n8) {
-                    const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-                    const int col = col_base + c;
-                    if (col < L.K) vv[u] = __ldcg(reinterpret_cast<const uint4*>(X + (long long)b * L.ldx + col));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int idx = base_i + u * kConsumerThreads;
-                if (idx >= n8) break;  // warp-uniform: n8 is a multiple of 32
-                const int b = udiv_small(idx, c8), c = (idx - b * c8) * 8;
-                const uint4 v = vv[u];
-                *reinterpret_cast<uint4*>(xs + b * p.xs_stride + c) = v;
-                if constexpr (ZP) {
-                    // zero-point constant of the 128-column group: sum (128 2^-o + z) x over the
-                    // group; the 8 columns here share the field offset o (16 lanes = 1 group)
-                    const int cs_ = c & 255;
-                    const int o = zp_off<R>((cs_ & 63) >> 4, (cs_ & 15) >> 3);
-                    const float m = 128.0f / (float)(1 << o) + (float)(1 << (R - 1));
-                    const uint16_t* hx = reinterpret_cast<const uint16_t*>(&v);
-                    float part = 0.0f;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) part += bf16_to_f32(hx[e]);
-                    part *= m;
-#pragma unroll
-                    for (int s = 8; s >= 1; s >>= 1) part += __shfl_xor_sync(0xffffffffu, part, s);
-                    if ((lane & 15) == 0) zc[(c >> 7) * (NT * 8) + b] = part;
-                }
-                if constexpr (NCOPY > 1) {
-                    const uint16_t* hv = reinterpret_cast<const uint16_t*>(&v);
-#pragma unroll
-                    for (int cp = 1; cp < NCOPY; ++cp) {
-                        uint4 o;
-                        uint16_t* ho = reinterpret_cast<uint16_t*>(&o);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            ho[e] = f32_to_bf16_rn(bf16_to_f32(hv[e]) * (1.0f / (float)(1 << zp_copy_off(R, cp))));
-                        *reinterpret_cast<uint4*>(xs + cp * p.xcopy_stride + b * p.xs_stride + c) = o;
-                    }
-                }
-            }
+    stack_stage<R, NT, F16, ZP, NCOPY>(p, L, xs, zc, col_base, Kc, sh.tag);
+    if (threadIdx.x == kSyncThread && L.war_wait >= 0 && L.war_wait < l) {
+        // this layer overwrites a buffer an earlier layer read from outside the
+        // step: every CTA must have staged it (almost always long done)
+        while (ld_acquire_u64(p.done + L.war_wait) < target) {
         }
     }
     consumer_sync();
-    if constexpr (F16) {
-        if (threadIdx.x == 0) sh.amax_bits = 0u;  // ready for the next layer (read only above)
+    if (L.ext_pub) {
+        if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1ull);
+        if (L.war_wait == l) {  // writes over its own external X: every CTA staged it first
+            if (threadIdx.x == kSyncThread)
+                while (ld_acquire_u64(p.done + l) < target) {
+                }
+            consumer_sync();
+        }
     }
     MQ_STS(l, 2);
 
@@ -579,7 +624,15 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 const float s_lo = sc[(w >> 1) * 2], s_hi = sc[(w >> 1) * 2 + 1];
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    if constexpr (ZP) {
+                    if constexpr (F16) {
+                        // {c / lambda_g, 1 / lambda_g} per batch row (stack_stage)
+                        const float4 z = *reinterpret_cast<const float4*>(
+                            zc + (((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t) * 2);
+                        tot[nt][0] = fmaf(s_lo, fmaf(z.y, acc[nt][0], -z.x), tot[nt][0]);
+                        tot[nt][1] = fmaf(s_lo, fmaf(z.w, acc[nt][1], -z.z), tot[nt][1]);
+                        tot[nt][2] = fmaf(s_hi, fmaf(z.y, acc[nt][2], -z.x), tot[nt][2]);
+                        tot[nt][3] = fmaf(s_hi, fmaf(z.w, acc[nt][3], -z.z), tot[nt][3]);
+                    } else if constexpr (ZP) {
                         const float* zp = zc + ((int)(xcol >> 7) + (w >> 1)) * (NT * 8) + nt * 8 + 2 * t;
                         const float c0 = zp[0], c1 = zp[1];
                         tot[nt][0] = fmaf(s_lo, acc[nt][0] - c0, tot[nt][0]);
@@ -598,20 +651,41 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     };
     // write a finished 16-row tile: Y (S == 1) or the chunk's split-K partial +
     // ticket, the last chunk to arrive summing the partials in chunk order
-    const float out_scale_l = F16 ? L.out_scale * sh.inv_lambda : L.out_scale;
+    const float out_scale_l = L.out_scale;
     const bool pair = p.cluster && L.S == 2;
-    // max |y| of the bf16 values this warp stored for a tile -> the layer's
-    // published maximum (a later fp16 layer stages its X in one pass with it)
-    auto publish_amax = [&](float m) {
-        if (!L.pub_amax) return;
+    // the final values of a tile (row r0 + 8h, batch nt * 8 + 2t + c in v[nt][2h + c]):
+    // plain bf16 Y and, when a later layer reads it, the LL words (row pairs)
+    auto store_final = [&](int rt, const float (&v)[NT][4]) {
+        const int r0 = rt * kTileRows + g;
+        uint16_t yb[NT][4];
 #pragma unroll
-        for (int s = 16; s >= 1; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
-        if (lane == 0)
-            atomicMax(p.amax + l, ((unsigned long long)(unsigned)(sh.gen + 1ull) << 32) | __float_as_uint(m));
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                    yb[nt][2 * h + c] = f32_to_bf16_rn(v[nt][2 * h + c]);
+                    if (b < p.B && row < L.N) st_global_u16(L.Y + (long long)b * L.ldy + row, yb[nt][2 * h + c]);
+                }
+        if (L.yll >= 0) {
+            // even g: rows (g, g+1) from its h = 0 value and lane g+1's; odd g: rows (g+7, g+8)
+            const bool odd = (g & 1) != 0;
+            const int start = rt * kTileRows + (odd ? g + 7 : g);
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint32_t send = odd ? yb[nt][c] : yb[nt][2 + c];
+                    const uint32_t recv = __shfl_xor_sync(0xffffffffu, send, 4);
+                    const uint32_t word = odd ? (recv | ((uint32_t)yb[nt][2 + c] << 16))
+                                              : ((uint32_t)yb[nt][c] | (recv << 16));
+                    const int b = nt * 8 + 2 * t + c;
+                    if (b < p.B && start < L.N) st_ll(p.ll + L.yll + (long long)b * L.ldyll + (start >> 1), word, sh.tag);
+                }
+        }
     };
     auto emit = [&](int rt, const float (&v)[NT][4]) {
-        const int r0 = rt * kTileRows + g;
-        float ymax = 0.0f;
         if (pair) {
             const int li = rt - wp.ta;
             const uint32_t cl = smem_addr(smem + p.cl_off);
@@ -635,26 +709,28 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             }
             par = __shfl_sync(0xffffffffu, par, 0);
             mbar_wait(bar, par);
+            float fin[NT][4];
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 const uint4 q = lds128(slot + 16 * nt);
-                const float pv[4] = {__uint_as_float(q.x), __uint_as_float(q.y), __uint_as_float(q.z),
-                                     __uint_as_float(q.w)};
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                        if (b < p.B && row < L.N) {
-                            const uint16_t yb = f32_to_bf16_rn(v[nt][2 * h + c] * out_scale_l + pv[2 * h + c]);
-                            st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
-                            ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
-                        }
-                    }
+                fin[nt][0] = v[nt][0] * out_scale_l + __uint_as_float(q.x);
+                fin[nt][1] = v[nt][1] * out_scale_l + __uint_as_float(q.y);
+                fin[nt][2] = v[nt][2] * out_scale_l + __uint_as_float(q.z);
+                fin[nt][3] = v[nt][3] * out_scale_l + __uint_as_float(q.w);
             }
-            publish_amax(ymax);
+            store_final(rt, fin);
             return;
         }
+        if (L.S == 1) {
+            float fin[NT][4];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) fin[nt][i] = v[nt][i] * out_scale_l;
+            store_final(rt, fin);
+            return;
+        }
+        const int r0 = rt * kTileRows + g;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -662,27 +738,16 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
-                    const float val = v[nt][2 * h + c] * out_scale_l;
-                    if (b < p.B && row < L.N) {
-                        if (L.S == 1) {
-                            const uint16_t yb = f32_to_bf16_rn(val);
-                            st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
-                            ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
-                        } else {
-                            st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, val);
-                        }
-                    }
+                    if (b < p.B && row < L.N)
+                        st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, v[nt][2 * h + c] * out_scale_l);
                 }
-        if (L.S == 1) {
-            publish_amax(ymax);
-            return;
-        }
         __syncwarp();
         int last = 0;
         // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
         if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == L.S - 1);
         last = __shfl_sync(0xffffffffu, last, 1);
         if (!last) return;
+        float fin[NT][4];
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -690,10 +755,10 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
                     const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
+                    float sum = 0.0f;
                     if (b < p.B && row < L.N) {
                         const float* wq = p.ws + (long long)b * L.Np + row;
                         const long long cstride = (long long)p.B * L.Np;
-                        float sum = 0.0f;
                         int q = 0;
                         for (; q + 4 <= L.S; q += 4) {
                             const float a0 = __ldcg(wq + q * cstride), a1 = __ldcg(wq + (q + 1) * cstride);
@@ -701,12 +766,10 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                             sum += a0; sum += a1; sum += a2; sum += a3;
                         }
                         for (; q < L.S; ++q) sum += __ldcg(wq + q * cstride);
-                        const uint16_t yb = f32_to_bf16_rn(sum);
-                        st_global_u16(L.Y + (long long)b * L.ldy + row, yb);
-                        ymax = fmaxf(ymax, fabsf(bf16_to_f32(yb)));
                     }
+                    fin[nt][2 * h + c] = sum;
                 }
-        publish_amax(ymax);
+        store_final(rt, fin);
         __syncwarp();
         if (lane == 0) p.tickets[rt] = 0;
     };
@@ -788,11 +851,9 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     }
     MQ_STS(l, 4);
 
-    // ---- publish layer l ------------------------------------------------
+    // ---- end of layer l: the staging area and the partial slots are free again
     consumer_sync();
     MQ_STS(l, 6);
-    // consumers have no bulk copies in flight, so the release is not delayed by the weight stream
-    if (threadIdx.x == kSyncThread) red_release_add(p.done + l, 1ull);
     MQ_STS(l, 7);
 }
 
@@ -810,8 +871,10 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.xs_bytes);   // [15][8]
     uint64_t* empty = full + kStackWarps * 8;                           // [15][8]
     uint8_t* ring = smem + p.xs_bytes + kStackWarps * 8 * 16;
-    if (threadIdx.x == kSyncThread) sh.gen = atomicAdd(p.launch_ctr, 1ull) / gridDim.x;
-    if (threadIdx.x == 0) sh.amax_bits = 0u;
+    if (threadIdx.x == kSyncThread) {
+        sh.gen = atomicAdd(p.launch_ctr, 1ull) / gridDim.x;
+        sh.tag = (uint32_t)(sh.gen % 0xFFFFFFFFull) + 1u;  // never 0 (zeroed buffers); consecutive steps differ
+    }
     // the layer table lives in shared memory: a descriptor field re-read from
     // global memory mid-layer (register rematerialisation) waits behind the
     // weight stream for ~1-2 us
