@@ -438,6 +438,7 @@ struct StackPlanHost {  // the opaque host plan (mq_stack_plan_bytes)
     size_t smem;
     size_t ws_bytes;
     size_t ll_bytes;
+    size_t tk_bytes;
 };
 // K3S per-layer decomposition: K chunks S (activation staging bounded by
 // kXsMax), the chunk's row tiles split contiguously over cpc = sms / S CTAs,
@@ -473,11 +474,11 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
     return best_c;
 }
 
-// workspace: [tickets 64 KB][done counters n + launch counter][LL words][partials]
+// workspace: [tickets (per layer, self-resetting)][done counters n + launch counter][LL words][partials]
 size_t stack_ws_layout(int n_layers, size_t ll_bytes, size_t partial_bytes, size_t* off_done, size_t* off_ll,
-                       size_t* off_partials) {
-    *off_done = kTicketBytes;
-    *off_ll = kTicketBytes + (((size_t)(n_layers + 1) * 8 + 255) & ~(size_t)255);
+                       size_t* off_partials, size_t ticket_bytes) {
+    *off_done = (ticket_bytes + 255) & ~(size_t)255;
+    *off_ll = *off_done + (((size_t)(n_layers + 1) * 8 + 255) & ~(size_t)255);
     *off_partials = *off_ll + ((ll_bytes + 255) & ~(size_t)255);
     return *off_partials + partial_bytes;
 }
@@ -534,6 +535,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1, cl_tiles = 0, nrt_max = 1;
     bool zp_any = false, uniform = true;
     size_t partials = 0, stage_max = 0, ll_bytes = 0;
+    int n_tickets = 0, n_pair_layers = 0;
     std::vector<int> war((size_t)n_layers, -1);
     // staging holds the most copies any layer stages and the ring the largest
     // stage: every layer's K chunk is sized for both, so any layer fits
@@ -555,8 +557,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         nrt_max = std::max(nrt_max, mq::pad16(std::max(layers[i].N, 1)) / 16);
     }
     // CTA-pair reduction slots: at most ceil(n_rt / (sms / 2)) tiles per CTA
-    const int cl_max = pair ? mq::cdiv(nrt_max, std::max(1, sm_count() / 2)) : 0;
-    const size_t cl_reserve = cl_max ? (size_t)12 * cl_max + 16 + (size_t)cl_max * 32 * nt * 16 : 0;
+    const int cl_max = pair ? 2 * mq::cdiv(nrt_max, std::max(1, sm_count() / 2)) : 0;  // two buffers
+    const size_t cl_reserve = cl_max ? (size_t)32 * cl_max + (size_t)cl_max * 32 * nt * 16 : 0;
     // everything but the activation chunk: table, partial slots, zero-point
     // constants, barriers, a 2-deep ring
     const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
@@ -583,7 +585,6 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         const int npl = (child || ri == 8) ? ri : ri + 1;
         const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair);
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
-        if (c.S > 1 && L.n_rt > kMaxTickets) return fail(MQ_ERR_INVALID, "layer %d: N too large", i);
         mq::StackLayer& t = T[i];
         memset(&t, 0, sizeof(t));
         if (war[(size_t)i] == i) t.ext_pub = 1;
@@ -629,10 +630,22 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
                 }
         }
         cs_max = std::max(cs_max, c.cs);
-        if (pair && c.S == 2) cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
-        if (c.S > 1) partials = std::max(partials, (size_t)c.S * B * L.Np * sizeof(float));
+        if (pair && c.S == 2) {
+            cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
+            t.cl_base = n_pair_layers++ & 1;  // buffer index; scaled to slots below
+        }
+        if (c.S > 1 && !(pair && c.S == 2)) {  // this layer's own partials and tickets
+            t.ws_off = (long long)(partials / sizeof(float));
+            partials += (size_t)c.S * B * L.Np * sizeof(float);
+            t.tk_off = n_tickets;
+            n_tickets += L.n_rt;
+        }
     }
-    for (int i = 0; i < n_layers; ++i) T[i].war_wait = war[(size_t)i];
+    for (int i = 0; i < n_layers; ++i) {
+        T[i].war_wait = war[(size_t)i];
+        T[i].cl_base *= cl_tiles;  // two slot buffers of cl_tiles each
+    }
+    cl_tiles *= 2;
     mq::StackParams& p = P->p;
     p.n_layers = n_layers;
     p.B = B;
@@ -647,7 +660,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     p.cl_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
     p.cluster = pair ? 1 : 0;
     p.cl_tiles = cl_tiles;
-    const size_t cl_bytes = cl_tiles ? ((size_t)12 * cl_tiles + 15 & ~(size_t)15) + (size_t)cl_tiles * 32 * nt * 16 : 0;
+    // [full mbarriers, uses | free mbarriers, free uses] (32 B per tile) + the partial slots
+    const size_t cl_bytes = cl_tiles ? (size_t)32 * cl_tiles + (size_t)cl_tiles * 32 * nt * 16 : 0;
     p.xs_bytes = (int)((p.cl_off + cl_bytes + 15) & ~(size_t)15);
     const size_t fixed = (size_t)p.xs_bytes + mq::kStackWarps * 8 * 16;  // full + empty barriers
     const int d = (int)((kSmemFullSm - std::min(fixed, kSmemFullSm)) / (mq::kStackWarps * stage_max));
@@ -662,7 +676,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     P->grid = sm_count();
     size_t od, ol, op;
     P->ll_bytes = ll_bytes;
-    P->ws_bytes = stack_ws_layout(n_layers, ll_bytes, partials, &od, &ol, &op);
+    P->tk_bytes = (size_t)n_tickets * sizeof(int);
+    P->ws_bytes = stack_ws_layout(n_layers, ll_bytes, partials, &od, &ol, &op, P->tk_bytes);
     *workspace_bytes = P->ws_bytes;
     return MQ_OK;
 }
@@ -695,7 +710,7 @@ int mq_stack_run(const void* plan_host, const void* table_dev, void* workspace, 
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
     mq::StackParams p = P->p;
     size_t od, ol, op;
-    stack_ws_layout(p.n_layers, P->ll_bytes, 0, &od, &ol, &op);
+    stack_ws_layout(p.n_layers, P->ll_bytes, 0, &od, &ol, &op, P->tk_bytes);
     char* w = reinterpret_cast<char*>(workspace);
     p.layers = reinterpret_cast<const mq::StackLayer*>(table_dev);
     p.tickets = reinterpret_cast<int*>(w);
@@ -734,7 +749,7 @@ int mq_stack_epoch(const void* plan_host, void* workspace, size_t workspace_byte
     if (workspace_bytes < P->ws_bytes)
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, P->ws_bytes);
     size_t od, ol, op;
-    stack_ws_layout(P->p.n_layers, P->ll_bytes, 0, &od, &ol, &op);
+    stack_ws_layout(P->p.n_layers, P->ll_bytes, 0, &od, &ol, &op, P->tk_bytes);
     unsigned long long* ctr = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(workspace) + od);
     const int n = P->p.n_layers + 1;
     cudaStream_t s = (cudaStream_t)stream;

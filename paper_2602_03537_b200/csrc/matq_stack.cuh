@@ -46,6 +46,11 @@ struct __align__(8) StackLayer {
     int ext_pub;      // X comes from outside the step and a later layer overwrites it: count the
                       // CTAs that finished staging it (done[l])
     int war_wait;     // this layer overwrites layer war_wait's external X: wait until every CTA staged it, or -1
+    int cl_base;      // pair layers (S == 2, CTA pairs): first slot of this layer's buffer -- pair
+                      // layers alternate between two, so a partner one layer ahead never waits
+    int tk_off;       // S > 1 through the workspace: this layer's own tickets (StackParams::tickets + tk_off)
+    long long ws_off;  // and its own partials (StackParams::ws + ws_off): no layer reuses another's, since
+                       // without grid barriers a fast CTA may already be a layer ahead
 };
 
 struct StackParams {
@@ -63,8 +68,8 @@ struct StackParams {
     int cluster;       // 1: CTA pairs (cluster of 2); S == 2 layers reduce through DSMEM
     int cl_off;        // byte offset of the pair-reduction area: [cl_tiles mbarriers][cl_tiles use counters][slots]
     int cl_tiles;      // most row tiles a CTA holds in an S == 2 layer
-    float* ws;         // split-K partials (max over layers)
-    int* tickets;      // split-K tickets, self-resetting
+    float* ws;         // split-K partials (per layer: StackLayer::ws_off)
+    int* tickets;      // split-K tickets, self-resetting (per layer: StackLayer::tk_off)
     unsigned long long* done;  // [n_layers] monotone external-staging counters (64-bit: never wrap)
     unsigned long long* launch_ctr;
     unsigned long long* ll;      // LL activation words of every producing layer (workspace)
@@ -202,6 +207,21 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
     unsigned long long v;
     asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+// pair-slot credits: chunk 0 releases a consumed slot to chunk 1 across the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t raddr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAITC_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAITC_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
 }
 // the consumer warps only (the producer warp runs ahead across layers): named
 // barrier 0 with the consumer thread count (1..15 are the tile hand-off barriers)
@@ -687,11 +707,21 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     };
     auto emit = [&](int rt, const float (&v)[NT][4]) {
         if (pair) {
-            const int li = rt - wp.ta;
+            const int li = L.cl_base + rt - wp.ta;  // this pair layer's slot buffer
             const uint32_t cl = smem_addr(smem + p.cl_off);
             const uint32_t bar = cl + 8 * li;
-            const uint32_t slot = cl + ((12u * p.cl_tiles + 15u) & ~15u) + (uint32_t)((li * 32 + lane) * NT * 16);
+            const uint32_t slot = cl + 32u * p.cl_tiles + (uint32_t)((li * 32 + lane) * NT * 16);
             if (wp.kc == 1) {  // chunk 1: ship the scaled partial to chunk 0
+                // credit: chunk 0 has consumed this slot's previous partial (no grid
+                // barrier orders the two CTAs' layers any more)
+                unsigned* fuses = reinterpret_cast<unsigned*>(smem + p.cl_off + 24 * p.cl_tiles);
+                uint32_t fu = 0;
+                if (lane == 0) {
+                    fu = fuses[li];
+                    fuses[li] = fu + 1u;
+                }
+                fu = __shfl_sync(0xffffffffu, fu, 0);
+                if (fu > 0) mbar_wait_cluster(cl + 16 * p.cl_tiles + 8 * li, (fu - 1u) & 1u);
                 const uint32_t rbar = mapa_rank(bar, 0), rslot = mapa_rank(slot, 0);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
@@ -719,6 +749,11 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 fin[nt][3] = v[nt][3] * out_scale_l + __uint_as_float(q.w);
             }
             store_final(rt, fin);
+            // slot free: every lane's slot loads fed its Y stores, which are issued (in
+            // order) before this point, so a relaxed arrive cannot overtake the reads --
+            // a release would also wait for the global stores to complete (~1 us)
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(mapa_rank(cl + 16 * p.cl_tiles + 8 * li, 1));
             return;
         }
         if (L.S == 1) {
@@ -739,12 +774,12 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 for (int c = 0; c < 2; ++c) {
                     const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
                     if (b < p.B && row < L.N)
-                        st_global_f32(p.ws + ((long long)wp.kc * p.B + b) * L.Np + row, v[nt][2 * h + c] * out_scale_l);
+                        st_global_f32(p.ws + L.ws_off + ((long long)wp.kc * p.B + b) * L.Np + row, v[nt][2 * h + c] * out_scale_l);
                 }
         __syncwarp();
         int last = 0;
         // lane 1: lane 0's in-flight bulk copies would delay an acq_rel RMW
-        if (lane == 1) last = (atom_add_acq_rel(p.tickets + rt, 1) == L.S - 1);
+        if (lane == 1) last = (atom_add_acq_rel(p.tickets + L.tk_off + rt, 1) == L.S - 1);
         last = __shfl_sync(0xffffffffu, last, 1);
         if (!last) return;
         float fin[NT][4];
@@ -757,7 +792,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                     const int row = r0 + 8 * h, b = nt * 8 + 2 * t + c;
                     float sum = 0.0f;
                     if (b < p.B && row < L.N) {
-                        const float* wq = p.ws + (long long)b * L.Np + row;
+                        const float* wq = p.ws + L.ws_off + (long long)b * L.Np + row;
                         const long long cstride = (long long)p.B * L.Np;
                         int q = 0;
                         for (; q + 4 <= L.S; q += 4) {
@@ -771,7 +806,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 }
         store_final(rt, fin);
         __syncwarp();
-        if (lane == 0) p.tickets[rt] = 0;
+        if (lane == 0) p.tickets[L.tk_off + rt] = 0;
     };
     // A tile cut by warp boundaries (warps wa < ... < wb) is emitted by wa, the
     // warp holding its first step: that is wa's LAST segment, so wa finishes it
@@ -907,11 +942,15 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         fence_mbar_init();
     }
     if (p.cluster && threadIdx.x == kSyncThread) {
+        // [full mbarriers][uses] (chunk 0 side), [free mbarriers][free uses] (chunk 1 side)
         const uint32_t cl = smem_addr(smem + p.cl_off);
         unsigned* uses = reinterpret_cast<unsigned*>(smem + p.cl_off + 8 * p.cl_tiles);
+        unsigned* fuses = reinterpret_cast<unsigned*>(smem + p.cl_off + 24 * p.cl_tiles);
         for (int i = 0; i < p.cl_tiles; ++i) {
             mbar_init(cl + 8 * i, 1);
+            mbar_init(cl + 16 * p.cl_tiles + 8 * i, 1);
             uses[i] = 0u;
+            fuses[i] = 0u;
         }
         fence_mbar_init();
     }
@@ -922,6 +961,7 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         // the same slot stride the consumer uses: the stage size in uniform kernels
         constexpr uint32_t kFix = RFIX ? 128u + 512u * PlaneCount<RFIX ? RFIX : 2, CHILD>::value : 0u;
         stack_producer<kFix>(rc);
+        if (p.cluster) cluster_sync_all();  // see the end of the consumer path
         return;
     }
     const unsigned long long target = (sh.gen + 1ull) * gridDim.x;
@@ -941,6 +981,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
             }
         }
     }
+    // a CTA pair touches each other's shared memory (partials, slot credits) until
+    // the last pair layer: neither exits before both are done
+    if (p.cluster) cluster_sync_all();
 }
 
 template <int R>
