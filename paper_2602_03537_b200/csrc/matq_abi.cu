@@ -462,7 +462,9 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
         if (xs > kXsMaxStack && cs > 1) continue;
         const int cpc = std::min(sms / S, n_rt);
         if (cpc < 1) break;
-        const int work = mq::cdiv(n_rt, cpc) * cs;          // busiest CTA
+        // busiest CTA: S = 1 splits the layer's (tile, step) pairs stream-K style
+        // (every CTA within one step of the mean); S > 1 deals whole tiles per chunk
+        const int work = S == 1 ? mq::cdiv((long long)n_rt * nsteps, sms) : mq::cdiv(n_rt, cpc) * cs;
         const double per_warp = (double)mq::cdiv(work, mq::kStackWarps);
         const double fix = S == 1 ? 0.0 : (pair && S == 2 ? 0.5 : (pair ? 6.0 : 3.0));
         const double cost = 4.0 * per_warp + fix + (work % mq::kStackWarps ? 0.5 : 0.0);
@@ -630,6 +632,14 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
                 }
         }
         cs_max = std::max(cs_max, c.cs);
+        if (c.S == 1) {  // stream-K: pairs [c fq + min(c, fr), ...), boundary parts through LL words
+            const long long P = (long long)L.n_rt * L.nsteps;
+            t.flat = 1;
+            t.fq = (int)(P / sm_count());
+            t.fr = (int)(P % sm_count());
+            t.fl_off = (long long)(ll_bytes / 8);
+            ll_bytes += (size_t)sm_count() * 32 * nt * 4 * 8;
+        }
         if (pair && c.S == 2) {
             cl_tiles = std::max(cl_tiles, mq::cdiv(L.n_rt, c.cpc));
             t.cl_base = n_pair_layers++ & 1;  // buffer index; scaled to slots below

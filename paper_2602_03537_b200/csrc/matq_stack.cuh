@@ -48,6 +48,11 @@ struct __align__(8) StackLayer {
     int war_wait;     // this layer overwrites layer war_wait's external X: wait until every CTA staged it, or -1
     int cl_base;      // pair layers (S == 2, CTA pairs): first slot of this layer's buffer -- pair
                       // layers alternate between two, so a partner one layer ahead never waits
+    int flat;         // S == 1, stream-K split: CTA c takes pairs [c fq + min(c, fr), ...) of the layer's
+    int fq, fr;       // n_rt * nsteps (tile, step) pairs (tile-major) -- every CTA within one step
+                      // of the mean; a tile cut by a CTA boundary is summed through fl_off
+    long long fl_off;  // word offset in StackParams::ll of [grid][32 lanes][NT * 4] LL words: slot c
+                       // holds CTA c + 1's part of CTA c's last tile
     int tk_off;       // S > 1 through the workspace: this layer's own tickets (StackParams::tickets + tk_off)
     long long ws_off;  // and its own partials (StackParams::ws + ws_off): no layer reuses another's, since
                        // without grid barriers a fast CTA may already be a layer ahead
@@ -124,6 +129,7 @@ constexpr int kSplitUnits = 3 * kStackWarps + (MQ_SMSP3_UNITS - 3) * (kStackWarp
 __device__ __forceinline__ int warp_units(int w) { return 3 * w + (MQ_SMSP3_UNITS - 3) * (w >> 2); }
 struct WarpPlan {
     int ta, ntiles, ns, chunk0, kc, f0, f1;
+    int fo, P;  // the CTA's pairs are [fo, fo + P) (flat index over tiles ta.. x ns steps); f0, f1 too
 };
 // a / b for 0 <= a < 2^22, 0 < b: float reciprocal + one-step correction
 // (~10 instructions; the compiler's 32/64-bit division sequences cost 20-60,
@@ -136,26 +142,33 @@ __device__ __forceinline__ int udiv_small(int a, int b) {
 }
 __device__ __forceinline__ WarpPlan warp_plan(const StackLayer& L, int cta, int warp) {
     WarpPlan w{};
-    if (cta >= L.cpc * L.S) return w;
-    const int j = udiv_small(cta, L.S);
-    w.kc = cta - j * L.S;
-    w.ta = udiv_small(j * L.n_rt, L.cpc);
-    w.ntiles = udiv_small((j + 1) * L.n_rt, L.cpc) - w.ta;
-    w.chunk0 = w.kc * L.cs;
-    w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
-    const int P = w.ntiles * w.ns;
-    w.f0 = warp_units(warp) * P / kSplitUnits;
-    w.f1 = warp_units(warp + 1) * P / kSplitUnits;
+    if (L.flat) {  // stream-K over the whole layer (K in one chunk)
+        w.ns = L.nsteps;
+        w.fo = cta * L.fq + min(cta, L.fr);
+        w.P = L.fq + (cta < L.fr ? 1 : 0);
+    } else {
+        if (cta >= L.cpc * L.S) return w;
+        const int j = udiv_small(cta, L.S);
+        w.kc = cta - j * L.S;
+        w.ta = udiv_small(j * L.n_rt, L.cpc);
+        w.ntiles = udiv_small((j + 1) * L.n_rt, L.cpc) - w.ta;
+        w.chunk0 = w.kc * L.cs;
+        w.ns = max(0, min(w.chunk0 + L.cs, L.nsteps) - w.chunk0);
+        w.P = w.ntiles * w.ns;
+    }
+    w.f0 = w.fo + warp_units(warp) * w.P / kSplitUnits;
+    w.f1 = w.fo + warp_units(warp + 1) * w.P / kSplitUnits;
     return w;
 }
+// local (CTA-relative) start of warp v's range
 __device__ __forceinline__ int plan_f0(const WarpPlan& w, int warp) {
-    return warp_units(warp) * (w.ntiles * w.ns) / kSplitUnits;
+    return warp_units(warp) * w.P / kSplitUnits;
 }
-// The last warp whose range starts at or before step x: the largest v with
+// The last warp whose range starts at or before local step x: the largest v with
 // floor(U(v) P / kSplitUnits) <= x, i.e. U(v) <= umax = ceil(kSplitUnits (x + 1) / P) - 1
 // (never an empty warp); the estimate 4 umax / (9 + U3) is off by at most one.
 __device__ __forceinline__ int last_warp_at(const WarpPlan& w, int x) {
-    const int P = w.ntiles * w.ns;
+    const int P = w.P;
     const int umax = udiv_small(kSplitUnits * (x + 1) + P - 1, P) - 1;
     int v = min(kStackWarps - 1, 4 * umax / (9 + MQ_SMSP3_UNITS));
     while (v > 0 && warp_units(v) > umax) --v;
@@ -169,7 +182,7 @@ __device__ __forceinline__ int tile_parts(const WarpPlan& w, int wa, int f_last)
     const int vmax = last_warp_at(w, f_last);
     constexpr int kMinUnits = MQ_SMSP3_UNITS < 3 ? MQ_SMSP3_UNITS : 3;
     // every warp has >= floor(P kMinUnits / kSplitUnits) >= 1 steps
-    if (w.ntiles * w.ns * kMinUnits >= kSplitUnits) return vmax - wa;
+    if (w.P * kMinUnits >= kSplitUnits) return vmax - wa;
     int n = 0;
     for (int v = wa + 1; v <= vmax; ++v) n += plan_f0(w, v) < plan_f0(w, v + 1);
     return n;
@@ -816,11 +829,18 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     auto slot_ptr = [&](int w) { return slots + (w * 32 + lane) * (NT * 4); };
     const int first_lt = wp.ns > 0 ? udiv_small(wp.f0, wp.ns) : 0;
     int lt = first_lt, si = wp.ns > 0 ? wp.f0 - first_lt * wp.ns : 0;
+    const int f_end = wp.fo + wp.P;  // this CTA's range: [fo, f_end)
+    // stream-K boundary parts (flat layers): LL words {float, tag} per lane
+    auto remote_slot = [&](int cta) {
+        return p.ll + L.fl_off + ((long long)cta * 32 + lane) * (NT * 4);
+    };
     // segment by segment: the steps of one row tile inside [f0, f1)
 #pragma unroll 1
     for (int f = wp.f0; f < wp.f1;) {
         const int seg = min(wp.ns - si, wp.f1 - f);
-        const bool starts_tile = si == 0;  // this segment holds the tile's first step
+        const int tstart = lt * wp.ns, tlast = tstart + wp.ns - 1;
+        const int lfirst = max(tstart, wp.fo);  // the tile's first step inside this CTA
+        const bool head = f == lfirst;           // this segment holds it
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -850,34 +870,63 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
         si += seg;
         if (f == wp.f1) MQ_STS_WMAX(l, 5);  // this warp's last step decoded
         const bool tile_end = si == wp.ns;
-        if (starts_tile && tile_end) {
-            emit(wp.ta + lt, tot);
-        } else if (!starts_tile) {
+        const bool lend = tile_end || f == f_end;  // this segment reaches the tile's last step in this CTA
+        const int llast = min(tlast, f_end - 1) - wp.fo;  // CTA-local index of that step
+        if (head && lend && tstart >= wp.fo && tlast < f_end) {
+            emit(wp.ta + lt, tot);  // the whole tile in this warp
+        } else if (!head) {
             float* sp = slot_ptr(warp);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) sp[nt * 4 + i] = tot[nt][i];
-            // hand the part to the emitter wa (holder of the tile's first step)
+            // hand the part to the tile's head wa (holder of its first step here)
             // through named barrier wa + 1: bar.arrive orders the slot stores and
             // does not wait
-            const int wa = last_warp_at(wp, lt * wp.ns);
-            named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, (lt + 1) * wp.ns - 1)));
+            const int wa = last_warp_at(wp, lfirst - wp.fo);
+            named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, llast)));
         } else {
-            // emitter (its range ends inside the tile): own part, then the later
-            // warps' parts in warp order
-            const int f_last = (lt + 1) * wp.ns - 1;
-            named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, f_last)));
-            const int vmax = last_warp_at(wp, f_last);
-            for (int w2 = warp + 1; w2 <= vmax; ++w2) {
-                if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
-                const float* sp = slot_ptr(w2);
+            // head: own part, the later warps' parts in warp order, then the next
+            // CTA's part (a tile running past this CTA's range), in that order
+            if (!lend) {
+                named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, llast)));
+                const int vmax = last_warp_at(wp, llast);
+                for (int w2 = warp + 1; w2 <= vmax; ++w2) {
+                    if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
+                    const float* sp = slot_ptr(w2);
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
+                }
+            }
+            if (tlast >= f_end) {  // the next CTA's part of this tile
+                const unsigned long long* src = remote_slot(rc.cta);
+                unsigned long long v[NT * 4];
+                for (;;) {
+                    bool ok = true;
+#pragma unroll
+                    for (int i = 0; i < NT * 4; i += 2) {
+                        ld_ll2(src + i, v[i], v[i + 1]);
+                        ok = ok && (uint32_t)(v[i] >> 32) == sh.tag && (uint32_t)(v[i + 1] >> 32) == sh.tag;
+                    }
+                    if (ok) break;
+                }
+                __syncwarp();
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) tot[nt][i] += sp[nt * 4 + i];
+                    for (int i = 0; i < 4; ++i) tot[nt][i] += __uint_as_float((uint32_t)v[nt * 4 + i]);
             }
-            emit(wp.ta + lt, tot);
+            if (tstart < wp.fo) {  // the tile started in the previous CTA: ship this part there
+                unsigned long long* dst = remote_slot(rc.cta - 1);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) st_ll(dst + nt * 4 + i, __float_as_uint(tot[nt][i]), sh.tag);
+            } else {
+                emit(wp.ta + lt, tot);
+            }
         }
         if (tile_end) {
             si = 0;
