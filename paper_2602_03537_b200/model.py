@@ -162,9 +162,8 @@ class LinearStack:
     def stack_kernel_ok(self, config) -> bool:
         """Where the persistent K3S path is the default (single GPU, B <= 16,
         G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix*.txt):
-        * uniform r: at B <= 4 always (1.12-1.19x the per-layer K3 graph at
-          B = 1, fused or unfused); at B = 8-16 for r <= 4 (up to 1.7x) -- for
-          r >= 6 the graph wins there (r = 8: 0.87x at B = 8, 0.67x at B = 16);
+        * uniform r: at B <= 4 always; at B = 8-16 for r <= 3 (1.3x at r = 3)
+          -- for r >= 4 the graph wins there;
         * heterogeneous (per-layer r, parents): fused stacks at B <= 4 (1.10x at
           B = 1).  Unfused ones (224 linears, the k/v ones only 1024 rows)
           measure at par at B = 1 and the graph wins at larger B.
@@ -172,7 +171,9 @@ class LinearStack:
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
         if len(rs) == 1:
-            ok = self.B <= 4 or max(rs) <= 4
+            # round 2 (LL hand-off, stream-K): B = 8 / 16 at r = 4 measure 2.71 / 4.08 ms
+            # on K3S against 2.41 / 3.12 on the graph; r <= 3 still win there (1.68 vs 2.26)
+            ok = self.B <= 4 or max(rs) <= 3
         else:
             ok = self.fused and parents and self.B <= 4
         return (ok and self.tp == 1 and self.B <= 16 and self.G == 128)
