@@ -363,50 +363,66 @@ def sweep_leg(torch, stack, clocks, peak, batches, configs, steps=10, warmup=3):
     return out
 
 
+def graph_seconds(torch, fns, reps, clocks=None):
+    """Device seconds per call of ``fns`` (each fn(stream)): the calls are
+    captured once into a CUDA graph (no host launch cost in the timed region),
+    replayed ``reps`` times between CUDA events on the capture stream."""
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for fn in fns:
+            fn(s)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for fn in fns:
+            fn(s)
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            g.replay()
+    s.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.active(True)
+    e0.record(s)
+    with torch.cuda.stream(s):
+        for _ in range(reps):
+            g.replay()
+    e1.record(s)
+    e1.synchronize()
+    if clocks:
+        clocks.active(False)
+    del g
+    return e0.elapsed_time(e1) / 1e3 / (reps * len(fns))
+
+
 def prefill_leg(torch, mq, clocks, batches=(64, 256, 1024), bits=(4, 8), reps=10):
     """Qwen3-14B linears through K4 (tcgen05) at prefill batches: TFLOP/s per
     layer and for the 4-layer block, vs the measured bf16 peak and a dense
-    bf16 cuBLAS GEMM of the same shape (3 weight copies rotated: L2-cold)."""
+    bf16 cuBLAS GEMM of the same shape.  Both sides rotate 3 weight copies
+    (L2-cold) inside one CUDA graph (device time, no host launch cost)."""
     from paper_2602_03537_b200.model import QWEN3_14B, KINDS, full_layer_dims
 
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
         pk = json.load(f)
     tf_peak = float(pk.get("bf16_tflops", 1631.2))
 
-    def timed(fn):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        clocks.active(True)
-        e0.record()
-        for _ in range(reps):
-            fn()
-        e1.record()
-        e1.synchronize()
-        clocks.active(False)
-        return e0.elapsed_time(e1) / 1e3 / reps
-
     res = {}
     for kind in KINDS:
         N, K = full_layer_dims(QWEN3_14B, kind)
         pts = [mq.PlaneTensor.random_parent(N, K, seed=i) for i in range(3)]
-        Wd = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+        Wd = [torch.randn(N, K, device="cuda").to(torch.bfloat16) for _ in range(3)]
         for B in batches:
             X = torch.randn(B, K, device="cuda").to(torch.bfloat16)
             Y = torch.empty(B, N, device="cuda", dtype=torch.bfloat16)
-            dense = timed(lambda: torch.matmul(X, Wd.t(), out=Y))
+            dense = graph_seconds(torch, [lambda s, w=w: torch.matmul(X, w.t(), out=Y) for w in Wd], reps, clocks)
             for r in bits:
-                it = [0]
-
-                def run():
-                    pts[it[0] % 3].gemm(X, r, out=Y)
-                    it[0] += 1
-                t = timed(run)
+                t = graph_seconds(torch, [lambda s, pt=pt: pt.gemm(X, r, out=Y, pdl=True, stream=s)
+                                          for pt in pts], reps, clocks)
                 res[(kind, B, r)] = (t, dense, 2.0 * B * N * K)
         del pts, Wd
         torch.cuda.empty_cache()
     out = {"model": "Qwen3-14B", "peak_tflops": tf_peak, "peak_kind": "measured bf16 (burst)",
+           "timing": "CUDA graph of 3 rotated weight copies per side (L2-cold), device time",
            "per_layer": {}, "block": {}}
     for (kind, B, r), (t, dense, fl) in res.items():
         out["per_layer"]["%s_B%d_r%d" % (kind, B, r)] = {

@@ -222,6 +222,11 @@ MQ_API int mq_debug_timestamps(unsigned long long* out, int n) {
     if (cudaMemcpy(out, dbg_buffer(), bytes, cudaMemcpyDeviceToHost) != cudaSuccess) return MQ_ERR_CUDA;
     return MQ_OK;
 }
+MQ_API int mq_debug_gemm_timestamps(unsigned long long* out, int n) {
+    if (n < 64 * 160 * 6) return MQ_ERR_INVALID;
+    return cudaMemcpy(out, mq::gemm_dbg_buffer(), sizeof(unsigned long long) * 64 * 160 * 6,
+                      cudaMemcpyDeviceToHost) == cudaSuccess ? MQ_OK : MQ_ERR_CUDA;
+}
 MQ_API int mq_debug_reset(void) {
     const size_t bytes = sizeof(unsigned long long) * (size_t)mq::kTsSlots * mq::kTsCtas * mq::kTsEvents;
     return cudaMemset(dbg_buffer(), 0, bytes) == cudaSuccess ? MQ_OK : MQ_ERR_CUDA;

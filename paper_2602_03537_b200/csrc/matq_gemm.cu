@@ -61,6 +61,15 @@ cudaError_t launch_rc(int bn, const CUtensorMap& map, const GemmParams& p, int g
 
 }  // namespace
 
+#ifdef MQ_GEMV_TIMING
+unsigned long long* gemm_dbg_buffer() {
+    static unsigned long long* buf = nullptr;
+    if (!buf && cudaMalloc(&buf, sizeof(unsigned long long) * 64 * 160 * 6) == cudaSuccess)
+        cudaMemset(buf, 0, sizeof(unsigned long long) * 64 * 160 * 6);
+    return buf;
+}
+#endif
+
 GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
     GemmConfig c{};
     c.bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
@@ -74,7 +83,11 @@ GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
         const int cs = cdiv(nsteps, S);
         if (cdiv(nsteps, cs) != S) continue;
         const int units = c.n_tiles * S;
-        const double cost = (double)cdiv(units, sms) * (cs + (S > 1 ? 4.0 : 0.0));
+        // a split tile costs its partial round trip: ~1.5 steps when every unit is
+        // resident (the S splits reduce 1/S of the columns each), ~4 when the last
+        // split to arrive reduces the whole tile
+        const double fix = S == 1 ? 0.0 : (units <= sms ? 1.5 : 4.0);
+        const double cost = (double)cdiv(units, sms) * (cs + fix);
         if (cost < best - 1e-9) {
             best = cost;
             c.S = S;
@@ -132,6 +145,12 @@ cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, in
     }
     p.out_scale = out_scale;
     p.y_f32 = y_f32 ? 1 : 0;
+    p.coop = (c.S > 1 && c.n_tiles * c.S <= c.grid) ? 1 : 0;
+#ifdef MQ_GEMV_TIMING
+    static int dbg_ctr = 0;
+    p.dbg_slot = dbg_ctr++ % 64;
+    p.dbg_ts = gemm_dbg_buffer();
+#endif
     const bool ch = child && r < 8;
     const int bn = c.bn, grid = c.grid;
     switch (r) {

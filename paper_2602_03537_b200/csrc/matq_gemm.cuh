@@ -47,7 +47,22 @@ struct GemmParams {
     int* tickets;       // [n_tiles], zero, self-resetting
     float out_scale;
     int y_f32;
+    int coop;  // S > 1 and every unit resident at once (n_tiles * S <= grid)
+#ifdef MQ_GEMV_TIMING
+    unsigned long long* dbg_ts;
+    int dbg_slot;
+#endif
 };
+#ifdef MQ_GEMV_TIMING
+#define MQ_GTS(ev) do { if (blockIdx.x < 160) p.dbg_ts[((size_t)p.dbg_slot * 160 + blockIdx.x) * 6 + (ev)] = gtimer_gemm(); } while (0)
+__device__ __forceinline__ unsigned long long gtimer_gemm() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#else
+#define MQ_GTS(ev) do { } while (0)
+#endif
 
 constexpr int kGemmThreads = 23 * 32;
 constexpr int kGemmBM = 128;
@@ -126,6 +141,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
     pdl_launch_dependents();
+    if (threadIdx.x == 0) MQ_GTS(0);
 
     const int n_units = p.n_tiles * p.S;
     const int my_units = (int)blockIdx.x < n_units ? (n_units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
@@ -165,6 +181,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
+        __syncwarp();  // lane 0's role loop rejoins its warp before the final barrier
     } else if (warp == kWarpW) {
         // ---------------- producer: raw weight blocks (independent of X: no PDL wait) --
         if (lane == 0) {
@@ -188,6 +205,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
             }
         }
+        __syncwarp();  // lane 0's role loop rejoins its warp before the final barrier
     } else if (warp == kWarpMma) {
         // ---------------- MMA issuer ----------------------------------------
         if (lane == 0) {
@@ -203,6 +221,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int kk = 0; kk < 4 * nst; ++kk, ++ks) {
                     const int s = ks % NS;
                     mbar_wait(op_full(s), (ks / NS) & 1);
+                    if (ks == 0) MQ_GTS(2);
                     tc_fence_after();
 #pragma unroll
                     for (int k16 = 0; k16 < kGemmBK / 16; ++k16) {
@@ -214,7 +233,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 }
                 umma_commit(tfull(buf));
             }
+            MQ_GTS(3);
         }
+        __syncwarp();  // lane 0's role loop rejoins its warp before the final barrier
     } else if (warp >= kEpiWarp0) {
         // ---------------- epilogue: TMEM -> Y / split-K partials ---------------------
         auto epilogue = [&](int ui) {
@@ -225,6 +246,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             const int mt = tile / p.n_bt, bt = tile % p.n_bt;
             const int buf = ui & 1;
             mbar_wait(tfull(buf), (ui >> 1) & 1);
+            if (warp == kEpiWarp0 && lane == 0 && ui == my_units - 1) MQ_GTS(4);
             tc_fence_after();
             const int row = mt * kGemmBM + et;
             const int b_lim = min(BN, p.B - bt * BN);
@@ -233,7 +255,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 if (p.y_f32) reinterpret_cast<float*>(p.Y)[o] = v;
                 else reinterpret_cast<uint16_t*>(p.Y)[o] = f32_to_bf16_rn(v);
             };
-            float* part = p.ws + ((long long)tile * p.S + split) * (BN * kGemmBM);
+            // split-K partial of this unit: [BN / 4][128 rows][4] floats (float4 per row and
+            // 4 columns: the TMEM lane's 32 columns go out as 8 vector stores)
+            float4* part4 = reinterpret_cast<float4*>(p.ws + ((long long)tile * p.S + split) * (BN * kGemmBM));
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
@@ -247,7 +271,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) part[(32 * c + j) * kGemmBM + et] = __uint_as_float(v[j]);
+                    for (int i = 0; i < 8; ++i)
+                        part4[(8 * c + i) * kGemmBM + et] =
+                            make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                        __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
                 }
             }
             // TMEM buffer can be refilled as soon as it is read
@@ -255,35 +282,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty(buf));
             if (p.S > 1) {
-                // publish partials; the last split of the tile reduces in split order
+                // publish the partial.  coop (every unit resident at once): each split waits
+                // for all S partials and reduces a 1/S share of the columns; otherwise the
+                // last split to arrive reduces the tile.  Split order either way
+                // (deterministic).
                 __threadfence();
                 named_bar_sync(1, 128);
-                if (et == 0) *flag_ptr = (atom_add_acq_rel(p.tickets + tile, 1) == p.S - 1);
+                if (et == 0) *flag_ptr = atom_add_acq_rel(p.tickets + tile, 1);
                 named_bar_sync(1, 128);
-                const int last = *flag_ptr;
-                if (last) {
-                    __threadfence();
-                    const float* t0 = p.ws + (long long)tile * p.S * (BN * kGemmBM);
-                    if (row < p.N) {
+                const int arrived = *flag_ptr;
+                int q_lo = 0, q_hi = 0;  // column quads [q_lo, q_hi) reduced here
+                const int nq = (b_lim + 3) >> 2;
+                if (p.coop) {
+                    if (et == 0)
+                        while (ld_acquire_s32(p.tickets + tile) < p.S) {
+                        }
+                    named_bar_sync(1, 128);
+                    q_lo = split * nq / p.S;
+                    q_hi = (split + 1) * nq / p.S;
+                } else if (arrived == p.S - 1) {
+                    q_hi = nq;
+                }
+                __threadfence();
+                const float4* t0 = reinterpret_cast<const float4*>(p.ws + (long long)tile * p.S * (BN * kGemmBM));
+                const long long sstride = (long long)(BN / 4) * kGemmBM;  // float4s per split
+                if (row < p.N) {
 #pragma unroll 1
-                        for (int j0 = 0; j0 < b_lim; j0 += 8) {
-                            float acc[8];
+                    for (int q0 = q_lo; q0 < q_hi; q0 += 4) {
+                        float4 acc[4];
 #pragma unroll
-                            for (int u = 0; u < 8; ++u) acc[u] = 0.0f;
-                            for (int sp = 0; sp < p.S; ++sp) {  // split order: deterministic
-                                const float* src = t0 + (long long)sp * (BN * kGemmBM) + j0 * kGemmBM + et;
-                                float v[8];
+                        for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int sp = 0; sp < p.S; ++sp) {  // split order: deterministic
+                            float4 v[4];
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) v[u] = j0 + u < BN ? __ldcg(src + u * kGemmBM) : 0.0f;
+                            for (int u = 0; u < 4; ++u)
+                                v[u] = q0 + u < q_hi ? __ldcg(t0 + sp * sstride + (long long)(q0 + u) * kGemmBM + et)
+                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-                                for (int u = 0; u < 8; ++u) acc[u] += v[u];
+                            for (int u = 0; u < 4; ++u) {
+                                acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
                             }
+                        }
 #pragma unroll
-                            for (int u = 0; u < 8; ++u)
-                                if (j0 + u < b_lim) store_y(j0 + u, acc[u]);
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = 4 * (q0 + u);
+                            if (q0 + u < q_hi) {
+                                if (j < b_lim) store_y(j, acc[u].x);
+                                if (j + 1 < b_lim) store_y(j + 1, acc[u].y);
+                                if (j + 2 < b_lim) store_y(j + 2, acc[u].z);
+                                if (j + 3 < b_lim) store_y(j + 3, acc[u].w);
+                            }
                         }
                     }
-                    if (et == 0) p.tickets[tile] = 0;
+                }
+                named_bar_sync(1, 128);
+                if (et == 0) {
+                    if (p.coop) {  // the last split through resets the ticket (2 S arrivals)
+                        if (atom_add_acq_rel(p.tickets + tile, 1) == 2 * p.S - 1) p.tickets[tile] = 0;
+                    } else if (arrived == p.S - 1) {
+                        p.tickets[tile] = 0;
+                    }
                 }
                 named_bar_sync(1, 128);  // flag slot reuse
             }
@@ -308,6 +366,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int f = 0; f < nst; ++f, ++fglob) {
                     const int rsl = fglob % RS;
                     mbar_wait(raw_full(rsl), (fglob / RS) & 1);
+                    if (fglob == 0 && dw == 0 && lane == 0) MQ_GTS(1);
                     uint2 raw[NPL];  // the two words (of four) of this decoder's word pair
                     float sc[2];
                     const uint32_t blk = raw_st(rsl) + (uint32_t)rtl * kBlk;
@@ -359,6 +418,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (warp == kWarpMma) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
+        if (lane == 0) MQ_GTS(5);  // every warp (incl. the split-K reduction) is done
     }
 }
 

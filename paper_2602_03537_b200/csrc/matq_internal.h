@@ -6,6 +6,9 @@
 #include "matq_common.cuh"
 
 namespace mq {
+#ifdef MQ_GEMV_TIMING
+unsigned long long* gemm_dbg_buffer();  // K4 phase stamps [64 launches][160 CTAs][6]
+#endif
 
 cudaError_t launch_pack_planes(const uint8_t* codes, long long ldc, const Layout& L, int nbits,
                                uint32_t* blob, cudaStream_t s);
