@@ -53,7 +53,7 @@ def _gain_matched_scales(K: int):
 class LinearStack:
     def __init__(self, shape: DecoderShape = LLAMA31_8B, batch: int = 1, group_size: int = 128,
                  tp: int = 1, rank: int = 0, process_group=None, seed: int = 0,
-                 n_layers: int | None = None, fused: bool = True):
+                 n_layers: int | None = None, fused: bool = True, shard_from_full: bool = False):
         _lib.require_cuda()
         if batch < 1 or batch > 32:
             raise ValueError("decode batch must lie in [1, 32]")
@@ -71,9 +71,25 @@ class LinearStack:
         for i in range(self.n_layers):
             for kind in kinds:
                 N, K = tp_layer_dims(shape, kind, tp, rank)
-                sd = seed * 1000003 + (i * 8 + kinds.index(kind)) * 8 + rank
                 sr = _gain_matched_scales(K * tp if kind in ("o", "down") else K)
-                pt = PlaneTensor.random_parent(N, K, group_size, seed=sd, scale_range=sr, signed_rows=True)
+                if shard_from_full and tp > 1:
+                    # this rank's shard (tp.decoder_plan) of the parent a tp = 1 stack with the
+                    # same seed holds: the TP step must reproduce the single-GPU step
+                    from .tp import decoder_plan
+
+                    sd = seed * 1000003 + (i * 8 + kinds.index(kind)) * 8
+                    fN, fK = full_layer_dims(shape, kind)
+                    codes, scales = PlaneTensor.random_parent_codes(fN, fK, group_size, sd,
+                                                                    _gain_matched_scales(fK), True)
+                    plan = decoder_plan(shape, kind, tp, rank, group_size)
+                    rows = torch.cat([torch.arange(a, b, device=codes.device) for a, b in plan.segments])
+                    (k0, k1), (g0, g1) = plan.cols, plan.groups
+                    pt = PlaneTensor.from_codes(codes[rows, k0:k1].contiguous(), 8,
+                                                scales[rows, g0:g1].contiguous(), group_size)
+                    del codes, scales
+                else:
+                    sd = seed * 1000003 + (i * 8 + kinds.index(kind)) * 8 + rank
+                    pt = PlaneTensor.random_parent(N, K, group_size, seed=sd, scale_range=sr, signed_rows=True)
                 self.layers.append(("layers.%d.%s" % (i, kind), kind, pt))
                 self.parent_seeds.append((sd, sr, True))
         self.stream = torch.cuda.Stream()
@@ -93,6 +109,7 @@ class LinearStack:
         dev = torch.device("cuda", torch.cuda.current_device())
         self.graph = None
         self.program = None
+        self.programs = []
         self.x = torch.zeros((batch, h), dtype=torch.bfloat16, device=dev)
         self.bufs = {}
         for name, kind, pt in self.layers[:len(kinds)]:
@@ -176,15 +193,16 @@ class LinearStack:
             ok = self.B <= 4 or max(rs) <= 3
         else:
             ok = self.fused and parents and self.B <= 4
-        return (ok and self.tp == 1 and self.B <= 16 and self.G == 128)
+        return ok and self.B <= 16 and self.G == 128  # tp > 1: one K3S launch per all-reduce segment
 
-    def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None) -> None:
+    def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None, graph: bool = True) -> None:
         """(Re)capture the decode step for a per-layer bit-width config.
 
         Single-GPU stacks with B <= 16 run as ONE persistent K3S launch per step
         (weights keep streaming across layer boundaries; a heterogeneous config
-        dispatches per layer inside the kernel); TP and B > 16 run as a CUDA
-        graph of per-layer K3 launches with PDL."""
+        dispatches per layer inside the kernel); under TP one K3S launch per
+        segment between all-reduces; otherwise a CUDA graph of per-layer K3
+        launches with PDL."""
         if isinstance(config, int):
             config = {n: config for n in self.names}
         missing = [n for n in self.names if n not in config]
@@ -196,7 +214,28 @@ class LinearStack:
         self.config = dict(config)
         use_stack = self.stack_kernel_ok(self.config) if stack_kernel is None else stack_kernel
         self.program = None
-        if use_stack:
+        self.programs = []
+        if use_stack and self.tp > 1:
+            # TP: one persistent K3S launch per segment between all-reduces
+            # (x -> qkv -> o | all-reduce | -> gate_up -> down | all-reduce), the
+            # segment's last layer being the row-parallel one whose partial is summed
+            from .device import StackProgram
+
+            sl = self._stack_layers()
+            seg = []
+            for (name, kind, _), lay in zip(self.layers, sl):
+                seg.append((name, lay))
+                if kind in ("o", "down"):
+                    rs = [self.config[n] for n, _ in seg]
+                    self.programs.append((StackProgram([l for _, l in seg], rs[0] if len(set(rs)) == 1 else rs,
+                                                       self.B), lay[2]))
+                    seg = []
+
+            def run():
+                for prog, out in self.programs:
+                    prog.run(self.stream)
+                    self._all_reduce(out)
+        elif use_stack:
             from .device import StackProgram
 
             rs = [self.config[n] for n, _, _ in self.layers]
@@ -207,18 +246,28 @@ class LinearStack:
         with torch.cuda.stream(self.stream):
             run()  # warm the launch path outside capture
         self.stream.synchronize()
+        self._eager = run
+        if not graph:  # e.g. a gloo process group: its collectives cannot be graph-captured
+            self.graph = None
+            return
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=self.stream):
             run()
         self.graph = g
 
     def launches_per_step(self) -> int:
+        """libmatq kernel launches per step (NCCL's all-reduce kernels not counted)."""
+        if getattr(self, "programs", None):
+            return len(self.programs)
         return 1 if getattr(self, "program", None) is not None else len(self.layers)
 
     def step(self) -> None:
         """Replay one captured decode step (device-resident activations)."""
         with torch.cuda.stream(self.stream):
-            self.graph.replay()
+            if self.graph is None:
+                self._eager()
+            else:
+                self.graph.replay()
 
     def decode(self, x_host: torch.Tensor | None = None) -> torch.Tensor:
         """End-to-end step through the public API: pinned host x -> device,
