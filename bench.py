@@ -770,42 +770,52 @@ def main():
         del hs
         torch.cuda.empty_cache()
 
-    # Full-model decode: the same sliced linears inside a
-    # Llama-3.1-8B-shaped decoder (bf16 attention over a 256-token KV cache,
-    # RMSNorm, RoPE, SiLU, bf16 lm_head), one CUDA graph per token; set beside
-    # the paper's own full-model numbers (RTX A6000)
+    # Full-model decode (BASELINE C5): the same sliced
+    # linears inside Llama-3.1-8B / Qwen3-14B / Phi-3-Medium-shaped decoders
+    # (bf16 attention over a 256-token KV cache, RMSNorm, RoPE, SiLU, bf16
+    # lm_head), one CUDA graph per token, tensor-parallel over the N ranks
+    # (tp.decoder_plan, NCCL all-reduces in the graph); set beside the paper's
+    # own full-model numbers (RTX A6000)
     full = None
-    if not args.no_full and world == 1 and args.model == "Llama-3.1-8B":
+    if not args.no_full:
         from paper_2602_03537_b200.llama import LlamaDecoder
+        from paper_2602_03537_b200.shapes import SHAPES as DSHAPES
 
         stack.graph = None
         torch.cuda.empty_cache()
         paper = {2: 138.0, 3: 124.4, 4: 109.3}
-        dec = LlamaDecoder(batch=args.batch, context=256, bits=args.bits, n_layers=args.layers)
-        full = {"context": 256, "lm_head": "bf16 128256x4096", "attention": "torch SDPA (GQA), bf16",
-                "per_bits": {}}
-        for rb in (2, 3, 4, 8):
-            dec.set_bits(rb)
-            dec.capture()
-            for _ in range(args.warmup):
-                dec.step()
-            barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            clocks.active(True)
-            e0.record(dec.stream)
-            for _ in range(args.steps):
-                dec.step()
-            e1.record(dec.stream)
-            barrier()
-            clocks.active(False)
-            fsec = e0.elapsed_time(e1) / 1e3 / args.steps
-            rec = {"tok_s": args.batch / fsec, "ms_per_step": fsec * 1e3}
-            if rb in paper and args.batch == 1:
-                rec["paper_a6000_tok_s"] = paper[rb]
-                rec["vs_paper"] = (args.batch / fsec) / paper[rb]
-            full["per_bits"][str(rb)] = rec
-        del dec
-        torch.cuda.empty_cache()
+        vocab = {"Llama-3.1-8B": 128256, "Qwen3-14B": 151936, "Phi-3-Medium": 32064}
+        full = {"context": 256, "lm_head": "bf16, replicated", "attention": "torch SDPA (GQA), bf16",
+                "tp": world, "models": {}}
+        for mname in ("Llama-3.1-8B", "Qwen3-14B", "Phi-3-Medium"):
+            dec = LlamaDecoder(DSHAPES[mname], batch=args.batch, context=256, bits=args.bits,
+                               vocab=vocab[mname], n_layers=args.layers, tp=world, rank=rank, process_group=pg)
+            rec_m = {"per_bits": {}}
+            for rb in ((2, 3, 4, 8) if mname == "Llama-3.1-8B" else (args.bits,)):
+                dec.set_bits(rb)
+                dec.capture()
+                for _ in range(args.warmup):
+                    dec.step()
+                barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                clocks.active(True)
+                e0.record(dec.stream)
+                for _ in range(args.steps):
+                    dec.step()
+                e1.record(dec.stream)
+                barrier()
+                clocks.active(False)
+                fsec = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.steps)
+                rec = {"tok_s": args.batch / fsec, "ms_per_step": fsec * 1e3}
+                if mname == "Llama-3.1-8B" and rb in paper and args.batch == 1:
+                    rec["paper_a6000_tok_s"] = paper[rb]
+                    rec["vs_paper"] = (args.batch / fsec) / paper[rb]
+                rec_m["per_bits"][str(rb)] = rec
+            dec.set_bits(args.bits)
+            rec_m["components_ms_r%d" % args.bits] = dec.component_ms()
+            full["models"][mname] = rec_m
+            del dec
+            torch.cuda.empty_cache()
 
     # C1: one 4096x4096 linear (the reference bench's case), L2-cold
     c1 = None

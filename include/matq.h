@@ -244,6 +244,11 @@ MQ_API int mq_add_rmsnorm(void* x, const void* delta, const float* w, void* y, i
                           void* stream);
 MQ_API int mq_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache, void* vcache,
                       int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos, void* stream);
+/* mq_qknorm_rope_kv: mq_rope_kv with a per-head RMSNorm of q and k first
+ *   (Qwen3's q_norm / k_norm weights, fp32 of head_dim; eps 1e-6). */
+MQ_API int mq_qknorm_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache,
+                             void* vcache, int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos,
+                             const float* q_norm, const float* k_norm, float eps, void* stream);
 MQ_API int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream);
 
 #ifdef __cplusplus

@@ -73,6 +73,7 @@ _SIGS = {
     "mq_fit_grid": ([_vp, _ll, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp, _vp], _i),
     "mq_add_rmsnorm": ([_vp, _vp, _vp, _vp, _i, _i, _f, _vp], _i),
     "mq_rope_kv": ([_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp], _i),
+    "mq_qknorm_rope_kv": ([_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _f, _vp], _i),
     "mq_silu_mul": ([_vp, _vp, _i, _i, _vp], _i),
     "mq_gptq_block": ([_vp, _ll, _i, _i, _i, _i, _vp, _i, _i, _vp, _ll, _vp, _vp, _i, _vp, _ll, _vp, _ll, _vp,
                        _ll, _vp], _i),

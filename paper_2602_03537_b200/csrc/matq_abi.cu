@@ -963,12 +963,20 @@ int mq_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, i
 
 int mq_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache, void* vcache, int B,
                int n_heads, int n_kv_heads, int head_dim, int T, int pos, void* stream) {
+    return mq_qknorm_rope_kv(qkv, cosv, sinv, q, kcache, vcache, B, n_heads, n_kv_heads, head_dim, T, pos, nullptr,
+                             nullptr, 0.0f, stream);
+}
+
+int mq_qknorm_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kcache, void* vcache,
+                      int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos, const float* q_norm,
+                      const float* k_norm, float eps, void* stream) {
     if (!qkv || !cosv || !sinv || !q || !kcache || !vcache) return fail(MQ_ERR_INVALID, "null pointer");
-    if (B < 1 || n_heads < 1 || n_kv_heads < 1 || head_dim < 2 || (head_dim & 1) || pos < 0 || pos >= T)
+    if (B < 1 || n_heads < 1 || n_kv_heads < 1 || head_dim % 64 || head_dim > 256 || pos < 0 || pos >= T)
         return fail(MQ_ERR_INVALID, "bad shape");
+    if ((q_norm == nullptr) != (k_norm == nullptr)) return fail(MQ_ERR_INVALID, "q_norm and k_norm go together");
     return cuda_status(mq::launch_rope_kv(qkv, cosv, sinv, q, kcache, vcache, B, n_heads, n_kv_heads, head_dim, T,
-                                          pos, (cudaStream_t)stream),
-                       "mq_rope_kv");
+                                          pos, q_norm, k_norm, eps, (cudaStream_t)stream),
+                       "mq_qknorm_rope_kv");
 }
 
 int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream) {

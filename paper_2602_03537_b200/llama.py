@@ -1,8 +1,10 @@
-"""Full-model decode harness: a Llama-3.1-8B-shaped decoder
-whose linears are sliced ``MatLinear`` layers, so the decode number can be set
-beside the paper's full-model measurement (Llama-3.1-8B-Instruct single-token
-forward: 138.0 / 124.4 / 109.3 tok/s at 2 / 3 / 4 bits on an
-RTX A6000).
+"""Full-model decode harness (BASELINE C5): a Llama /
+Qwen3 / Phi-3-shaped decoder whose linears are sliced ``MatLinear`` layers, so
+the decode number can be set beside the paper's full-model measurement
+(Llama-3.1-8B-Instruct single-token forward: 138.0 / 124.4 /
+109.3 tok/s at 2 / 3 / 4 bits on an RTX A6000), on one GPU or tensor-parallel
+(``tp``: tp.decoder_plan shards of the single-GPU parents, attention over the
+rank's own heads, one all-reduce after o and after down).
 
 Everything around the hot path is NOT part of the deliverable: embedding
 lookup, RMSNorm, rotary embedding, a KV cache with grouped-query attention
@@ -45,32 +47,66 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
 
 class LlamaDecoder:
     def __init__(self, shape: DecoderShape = LLAMA31_8B, batch: int = 1, context: int = 256,
-                 bits=4, vocab: int = 128256, seed: int = 0, n_layers: int | None = None, glue: str = "cuda"):
+                 bits=4, vocab: int = 128256, seed: int = 0, n_layers: int | None = None, glue: str = "cuda",
+                 tp: int = 1, rank: int = 0, process_group=None):
         if glue not in ("cuda", "torch"):
             raise ValueError("glue must be 'cuda' or 'torch'")
         self.shape, self.B, self.T, self.glue = shape, batch, context, glue
+        self.tp, self.rank, self.pg = tp, rank, process_group
         self.n_layers = n_layers or shape.n_layers
-        dev = torch.device("cuda")
+        dev = torch.device("cuda", torch.cuda.current_device())
         g = torch.Generator(device="cuda").manual_seed(seed)
         h, hd = shape.hidden, shape.head_dim
         self.embed = (torch.randn(vocab, h, device=dev, generator=g) * 0.02).to(torch.bfloat16)
         self.lm_head = (torch.randn(vocab, h, device=dev, generator=g) / math.sqrt(h)).to(torch.bfloat16)
         self.final_norm = torch.ones(h, device=dev)
+        # this rank's heads: q heads [q0, q1), kv heads [k0, k1) (tp.decoder_plan)
+        if tp > 1:
+            from .tp import decoder_plan
+
+            (qa, qb), (ka, kb), _ = decoder_plan(shape, "qkv", tp, rank).segments
+            q0, q1, k0, k1 = qa // hd, qb // hd, (ka - shape.q_out) // hd, (kb - shape.q_out) // hd
+        else:
+            q0, q1, k0, k1 = 0, shape.n_heads, 0, shape.n_kv_heads
+        self.nh, self.nkv = q1 - q0, k1 - k0
+        grp = shape.n_heads // shape.n_kv_heads
+        # local kv head of each local q head (GQA; replicated kv heads when tp does not divide them)
+        self.kv_of_q = torch.tensor([(q0 + i) // grp - k0 for i in range(self.nh)], device=dev)
+        self.uniform_gqa = self.nh % max(1, self.nkv) == 0 and all(
+            (q0 + i) // grp - k0 == i // (self.nh // self.nkv) for i in range(self.nh))
         self.blocks = []
         for i in range(self.n_layers):
             blk = {}
             for kind in ("qkv", "o", "gate_up", "down"):
                 N, K = full_layer_dims(shape, kind)
-                pt = PlaneTensor.random_parent(N, K, seed=seed * 7919 + i * 4 + ("qkv", "o", "gate_up", "down").index(kind),
-                                               scale_range=_gain_matched_scales(K), signed_rows=True)
+                sd = seed * 7919 + i * 4 + ("qkv", "o", "gate_up", "down").index(kind)
+                if tp > 1:
+                    from .tp import decoder_plan
+
+                    codes, scales = PlaneTensor.random_parent_codes(N, K, 128, sd, _gain_matched_scales(K), True)
+                    plan = decoder_plan(shape, kind, tp, rank)
+                    rows = torch.cat([torch.arange(a, b_, device=dev) for a, b_ in plan.segments])
+                    (c0, c1), (g0, g1) = plan.cols, plan.groups
+                    pt = PlaneTensor.from_codes(codes[rows, c0:c1].contiguous(), 8,
+                                                scales[rows, g0:g1].contiguous(), 128)
+                    del codes, scales
+                else:
+                    pt = PlaneTensor.random_parent(N, K, seed=sd, scale_range=_gain_matched_scales(K),
+                                                   signed_rows=True)
                 blk[kind] = MatLinear(pt, 4, name="layers.%d.%s" % (i, kind))
             blk["ln1"] = torch.ones(h, device=dev)
             blk["ln2"] = torch.ones(h, device=dev)
-            # KV cache: random history at positions 0..T-1, the decoded token's k/v at T
-            blk["kc"] = torch.zeros(batch, shape.n_kv_heads, context + 1, hd, device=dev, dtype=torch.bfloat16)
+            if shape.qk_norm:
+                blk["qn"] = 1.0 + 0.1 * torch.randn(hd, device=dev, generator=g)
+                blk["kn"] = 1.0 + 0.1 * torch.randn(hd, device=dev, generator=g)
+            # KV cache (the rank's kv heads): random history at positions 0..T-1, the decoded
+            # token's k/v at T
+            blk["kc"] = torch.zeros(batch, self.nkv, context + 1, hd, device=dev, dtype=torch.bfloat16)
             blk["vc"] = torch.zeros_like(blk["kc"])
-            blk["kc"][:, :, :context] = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
-            blk["vc"][:, :, :context] = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
+            hk = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
+            hv = torch.randn(batch, shape.n_kv_heads, context, hd, device=dev, generator=g)
+            blk["kc"][:, :, :context] = hk[:, k0:k1]
+            blk["vc"][:, :, :context] = hv[:, k0:k1]
             blk["k"], blk["v"] = blk["kc"][:, :, :context], blk["vc"][:, :, :context]
             self.blocks.append(blk)
         self.set_bits(bits)
@@ -80,13 +116,35 @@ class LlamaDecoder:
         self.sin = ang.sin().to(torch.bfloat16)
         self.tokens = torch.zeros(batch, dtype=torch.long, device=dev)
         self.logits = torch.empty(batch, vocab, device=dev, dtype=torch.bfloat16)
-        nq = shape.n_heads * hd
+        nq = self.nh * hd
+        inter = self.blocks[0]["down"].planes.K
+        self.inter = inter
         e = lambda *sz: torch.empty(*sz, device=dev, dtype=torch.bfloat16)  # noqa: E731
-        self.buf = {"x": e(batch, h), "hn": e(batch, h), "qkv": e(batch, nq + 2 * shape.n_kv_heads * hd),
-                    "q": e(batch, shape.n_heads, 1, hd), "o": e(batch, h), "gu": e(batch, 2 * shape.intermediate),
-                    "act": e(batch, shape.intermediate), "d": e(batch, h)}
+        self.buf = {"x": e(batch, h), "hn": e(batch, h), "qkv": e(batch, nq + 2 * self.nkv * hd),
+                    "q": e(batch, self.nh, 1, hd), "o": e(batch, h), "gu": e(batch, 2 * inter),
+                    "act": e(batch, inter), "d": e(batch, h)}
         self.stream = torch.cuda.Stream()
         self.graph = None
+
+    def _all_reduce(self, t: torch.Tensor) -> None:
+        if self.tp > 1:
+            torch.distributed.all_reduce(t, group=self.pg)
+
+    def _qk_norm(self, blk) -> None:
+        """Qwen3: per-head RMSNorm of q and k (in the fused qkv row) before the rotary step."""
+        if not self.shape.qk_norm:
+            return
+        B, hd = self.B, self.shape.head_dim
+        qk = self.buf["qkv"][:, : (self.nh + self.nkv) * hd].view(B, self.nh + self.nkv, hd)
+        w = torch.cat((blk["qn"].expand(self.nh, hd), blk["kn"].expand(self.nkv, hd)))
+        qk.copy_(_rms_norm(qk, w, 1e-6))
+
+    def _attend(self, q, kc, vc):
+        """Single-query attention over the cache with the rank's GQA head map."""
+        if self.uniform_gqa:
+            return F.scaled_dot_product_attention(q, kc, vc, enable_gqa=True)
+        return F.scaled_dot_product_attention(q, kc.index_select(1, self.kv_of_q),
+                                              vc.index_select(1, self.kv_of_q))
 
     def set_bits(self, bits) -> None:
         """Uniform int, or {name: r} over the fused linears' names."""
@@ -112,44 +170,104 @@ class LlamaDecoder:
         else:
             self._forward_torch()
 
-    def _forward_fused(self) -> None:
+    PARTS = ("linear", "attn", "glue", "comm", "head")
+
+    def _forward_fused(self, parts=PARTS) -> None:
         """One decode step: 4 sliced linears (PDL-chained K3) + 3 fused glue
-        kernels (norm, rotary/KV, gating) + SDPA per block."""
+        kernels (norm, rotary/KV, gating) + SDPA per block (+ 2 all-reduces
+        under tensor parallelism).  ``parts`` keeps only some component
+        classes (component_ms times each alone on the same buffers)."""
         from . import _lib
 
         s = self.shape
         B, hd, T = self.B, s.head_dim, self.T
-        nh, nkv, h = s.n_heads, s.n_kv_heads, s.hidden
+        nh, nkv, h = self.nh, self.nkv, s.hidden
         b = self.buf
         st = _lib.stream_ptr(None)
-        torch.index_select(self.embed, 0, self.tokens, out=b["x"])
+        lin, attn, glue, comm, head = (p in parts for p in self.PARTS)
+        if head:
+            torch.index_select(self.embed, 0, self.tokens, out=b["x"])
         delta = None
         for blk in self.blocks:
-            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta) if delta is not None else None,
-                      _lib.ptr(blk["ln1"]), _lib.ptr(b["hn"]), B, h, 1e-5, st)
-            blk["qkv"].planes.linear(b["hn"], blk["qkv"].bits, out=b["qkv"], pdl=True)
-            _lib.call("mq_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin), _lib.ptr(b["q"]),
-                      _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T, st)
-            att = F.scaled_dot_product_attention(b["q"], blk["kc"], blk["vc"], enable_gqa=True)
-            blk["o"].planes.linear(att.reshape(B, nh * hd), blk["o"].bits, out=b["o"], pdl=True)
-            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(b["o"]), _lib.ptr(blk["ln2"]),
-                      _lib.ptr(b["hn"]), B, h, 1e-5, st)
-            blk["gate_up"].planes.linear(b["hn"], blk["gate_up"].bits, out=b["gu"], pdl=True)
-            _lib.call("mq_silu_mul", _lib.ptr(b["gu"]), _lib.ptr(b["act"]), B, s.intermediate, st)
-            blk["down"].planes.linear(b["act"], blk["down"].bits, out=b["d"], pdl=True)
+            if glue:
+                _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta) if delta is not None else None,
+                          _lib.ptr(blk["ln1"]), _lib.ptr(b["hn"]), B, h, 1e-5, st)
+            if lin:
+                blk["qkv"].planes.linear(b["hn"], blk["qkv"].bits, out=b["qkv"], pdl=True)
+            if attn:
+                qn = _lib.ptr(blk["qn"]) if s.qk_norm else None
+                kn = _lib.ptr(blk["kn"]) if s.qk_norm else None
+                _lib.call("mq_qknorm_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin),
+                          _lib.ptr(b["q"]), _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T,
+                          qn, kn, 1e-6, st)
+                att = self._attend(b["q"], blk["kc"], blk["vc"])
+            else:
+                att = b["q"]
+            if lin:
+                blk["o"].planes.linear(att.reshape(B, nh * hd), blk["o"].bits, out=b["o"], pdl=True)
+            if comm:
+                self._all_reduce(b["o"])
+            if glue:
+                _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(b["o"]), _lib.ptr(blk["ln2"]),
+                          _lib.ptr(b["hn"]), B, h, 1e-5, st)
+            if lin:
+                blk["gate_up"].planes.linear(b["hn"], blk["gate_up"].bits, out=b["gu"], pdl=True)
+            if glue:
+                _lib.call("mq_silu_mul", _lib.ptr(b["gu"]), _lib.ptr(b["act"]), B, self.inter, st)
+            if lin:
+                blk["down"].planes.linear(b["act"], blk["down"].bits, out=b["d"], pdl=True)
+            if comm:
+                self._all_reduce(b["d"])
             delta = b["d"]
-        _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta), _lib.ptr(self.final_norm),
-                  _lib.ptr(b["hn"]), B, h, 1e-5, st)
-        torch.matmul(b["hn"], self.lm_head.t(), out=self.logits)
+        if glue:
+            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), _lib.ptr(delta), _lib.ptr(self.final_norm),
+                      _lib.ptr(b["hn"]), B, h, 1e-5, st)
+        if head:
+            torch.matmul(b["hn"], self.lm_head.t(), out=self.logits)
+
+    def component_ms(self, reps: int = 20) -> dict:
+        """Per-component device time of one step (ms): each component class
+        captured alone in its own CUDA graph (same shapes and buffers), plus
+        the whole step.  Under TP, "comm" is the all-reduces."""
+        def time_graph(fn):
+            with torch.cuda.stream(self.stream):
+                fn()
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                fn()
+            with torch.cuda.stream(self.stream):
+                g.replay()
+            self.stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
+            with torch.cuda.stream(self.stream):
+                for _ in range(reps):
+                    g.replay()
+            e1.record(self.stream)
+            e1.synchronize()
+            return e0.elapsed_time(e1) / reps
+
+        out = {"step": time_graph(lambda: self._forward_fused())}
+        for part in self.PARTS:
+            if part == "comm" and self.tp == 1:
+                continue
+            out[part] = time_graph(lambda p=part: self._forward_fused(parts=(p,)))
+        out["sum_of_parts"] = sum(v for k, v in out.items() if k != "step")
+        return out
 
     def _forward_torch(self) -> None:
         s = self.shape
         B, hd = self.B, s.head_dim
-        nh, nkv = s.n_heads, s.n_kv_heads
+        nh, nkv = self.nh, self.nkv
         x = self.embed[self.tokens]                                   # (B, h)
         for blk in self.blocks:
             hn = _rms_norm(x, blk["ln1"])
             qkv = blk["qkv"](hn)                                      # (B, (nh + 2 nkv) hd)
+            if s.qk_norm:
+                qk = qkv[:, : (nh + nkv) * hd].view(B, nh + nkv, hd)
+                w = torch.cat((blk["qn"].expand(nh, hd), blk["kn"].expand(nkv, hd)))
+                qkv = torch.cat((_rms_norm(qk, w, 1e-6).reshape(B, -1), qkv[:, (nh + nkv) * hd:]), dim=1)
             q = qkv[:, : nh * hd].view(B, nh, 1, hd)
             k = qkv[:, nh * hd:(nh + nkv) * hd].view(B, nkv, 1, hd)
             v = qkv[:, (nh + nkv) * hd:].view(B, nkv, 1, hd)
@@ -159,19 +277,26 @@ class LlamaDecoder:
             # a fixed-length step, so the graph replays identical work)
             kk = torch.cat((blk["k"], k), dim=2)
             vv = torch.cat((blk["v"], v), dim=2)
-            att = F.scaled_dot_product_attention(q, kk, vv, enable_gqa=True)   # (B, nh, 1, hd)
-            x = x + blk["o"](att.reshape(B, nh * hd))
+            att = self._attend(q, kk, vv)                             # (B, nh, 1, hd)
+            o = blk["o"](att.reshape(B, nh * hd))
+            self._all_reduce(o)
+            x = x + o
             hn = _rms_norm(x, blk["ln2"])
             gu = blk["gate_up"](hn)
-            inter = s.intermediate
-            x = x + blk["down"](F.silu(gu[:, :inter]) * gu[:, inter:])
+            inter = self.inter
+            d = blk["down"](F.silu(gu[:, :inter]) * gu[:, inter:])
+            self._all_reduce(d)
+            x = x + d
         x = _rms_norm(x, self.final_norm)
         torch.matmul(x, self.lm_head.t(), out=self.logits)
 
-    def capture(self) -> None:
+    def capture(self, graph: bool = True) -> None:
         with torch.cuda.stream(self.stream):
             self._forward()  # warm up the launch paths (workspaces, cuBLAS handles)
         self.stream.synchronize()
+        if not graph:  # e.g. gloo collectives, which cannot be graph-captured
+            self.graph = False
+            return
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=self.stream):
             self._forward()
@@ -181,7 +306,10 @@ class LlamaDecoder:
         if self.graph is None:
             self.capture()
         with torch.cuda.stream(self.stream):
-            self.graph.replay()
+            if self.graph is False:
+                self._forward()
+            else:
+                self.graph.replay()
 
     def decode(self, tokens_host: torch.Tensor) -> torch.Tensor:
         """One decode step through the public API: host token ids -> device ->
@@ -190,6 +318,9 @@ class LlamaDecoder:
             self.capture()
         with torch.cuda.stream(self.stream):
             self.tokens.copy_(tokens_host, non_blocking=True)
-            self.graph.replay()
+            if self.graph is False:
+                self._forward()
+            else:
+                self.graph.replay()
             nxt = self.logits.argmax(-1).to("cpu", non_blocking=True)
         return nxt

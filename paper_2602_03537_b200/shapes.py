@@ -20,6 +20,7 @@ class DecoderShape:
     n_kv_heads: int
     head_dim: int
     n_layers: int
+    qk_norm: bool = False  # per-head RMSNorm of q and k before the rotary embedding (Qwen3)
 
     @property
     def qkv_out(self) -> int:
@@ -35,7 +36,7 @@ class DecoderShape:
 
 
 LLAMA31_8B = DecoderShape("Llama-3.1-8B", 4096, 14336, 32, 8, 128, 32)
-QWEN3_14B = DecoderShape("Qwen3-14B", 5120, 17408, 40, 8, 128, 40)
+QWEN3_14B = DecoderShape("Qwen3-14B", 5120, 17408, 40, 8, 128, 40, qk_norm=True)
 PHI3_MEDIUM = DecoderShape("Phi-3-Medium", 5120, 17920, 40, 10, 128, 40)
 SHAPES = {s.name: s for s in (LLAMA31_8B, QWEN3_14B, PHI3_MEDIUM)}
 
