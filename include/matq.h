@@ -153,7 +153,22 @@ typedef struct mq_stack_layer {
     int ldx, ldy, N, K;
     float out_scale;      /* 2^(c - r) for a parent slice */
     int r;                /* this layer's bits when mq_stack_plan's r = 0; else ignored */
+    /* activation prologue fused into the layer's staging (0 = none):
+     *   MQ_XOP_ADD_RMSNORM: R <- bf16(R + X); X' = bf16(R * rsqrt(mean(R^2) + eps) * norm_w), R the
+     *     residual stream (res_in, or NULL: the residual the previous ADD_RMSNORM layer of this
+     *     stack kept); CTA 0 writes the updated R to res_out when non-NULL;
+     *   MQ_XOP_SILU_MUL: X' = bf16(bf16(silu(X[:, :K])) * X[:, K:2K]) (X is 2K wide).
+     * The row-wise math of mq_add_rmsnorm / mq_silu_mul; an add-RMSNorm layer runs as one K chunk. */
+    int xop;
+    const void* res_in;   /* bf16 (B, K), row stride ldres */
+    void* res_out;        /* bf16 (B, K), row stride ldres */
+    const float* norm_w;  /* fp32 (K) */
+    int ldres;
+    float eps;
 } mq_stack_layer;
+#define MQ_XOP_NONE 0
+#define MQ_XOP_ADD_RMSNORM 1
+#define MQ_XOP_SILU_MUL 2
 MQ_API size_t mq_stack_plan_bytes(void);
 MQ_API size_t mq_stack_table_bytes(int n_layers);
 MQ_API int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes,

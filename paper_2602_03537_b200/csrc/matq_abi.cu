@@ -455,7 +455,8 @@ struct StackCfg {
 // pair: CTA pairs (clusters of 2) reduce S = 2 through DSMEM for ~free; S > 2
 // still goes through the global workspace and tickets (~2 us of tail: partial
 // stores, an acq_rel ticket and the last chunk's reloads).
-StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXsMaxStack, bool pair) {
+StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXsMaxStack, bool pair,
+                             bool one_chunk = false) {
     const int n_rt = mq::pad16(N) / 16, nsteps = mq::pad256(K) / 256;
     StackCfg best_c{nsteps, 1, std::max(1, std::min(sms / nsteps, n_rt))};
     double best = 1e30;
@@ -465,6 +466,7 @@ StackCfg choose_stack_config(int N, int K, int B, int ncopy, int sms, size_t kXs
         if (S != S_try) continue;
         const size_t xs = (size_t)ncopy * B * (cs * 256 + 8) * 2;
         if (xs > kXsMaxStack && cs > 1) continue;
+        if (one_chunk && S_try > 1) break;  // a fused row-wise prologue needs the whole row
         const int cpc = std::min(sms / S, n_rt);
         if (cpc < 1) break;
         // busiest CTA: S = 1 splits the layer's (tile, step) pairs stream-K style
@@ -496,14 +498,15 @@ size_t stack_ws_layout(int n_layers, size_t ll_bytes, size_t partial_bytes, size
 // two (-2).  -1: no earlier layer writes X (activations from outside the step).
 int stack_x_producer(const mq_stack_layer* layers, int i, int B, size_t* elem_off) {
     const mq_stack_layer& in = layers[i];
+    const int xw = in.xop == MQ_XOP_SILU_MUL ? 2 * in.K : in.K;  // columns of X the layer reads
     auto lo = [](const void* p) { return reinterpret_cast<uintptr_t>(p); };
-    const uintptr_t x0 = lo(in.X), x1 = x0 + 2 * ((size_t)(B - 1) * in.ldx + in.K);
+    const uintptr_t x0 = lo(in.X), x1 = x0 + 2 * ((size_t)(B - 1) * in.ldx + xw);
     for (int j = i - 1; j >= 0; --j) {
         const mq_stack_layer& o = layers[j];
         const uintptr_t y0 = lo(o.Y), y1 = y0 + 2 * ((size_t)(B - 1) * o.ldy + o.N);
         if (x1 <= y0 || y1 <= x0) continue;  // no overlap: look further back
         const size_t e = (x0 - y0) / 2;  // X's first element inside Y (row 0: both have B rows)
-        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 4 == 0 && e + (size_t)in.K <= (size_t)o.N;
+        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 4 == 0 && e + (size_t)xw <= (size_t)o.N;
         *elem_off = e;
         return inside ? j : -2;
     }
@@ -542,7 +545,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     int cs_max = 1, nstage_max = 1, r_first = 0, nsteps_max = 1, cl_tiles = 0, nrt_max = 1;
     bool zp_any = false, uniform = true;
     size_t partials = 0, stage_max = 0, ll_bytes = 0;
-    int n_tickets = 0, n_pair_layers = 0;
+    int n_tickets = 0, n_pair_layers = 0, res_k = 0, res_k_max = 0;
+    std::vector<int> res_pub((size_t)n_layers, 0);
     std::vector<int> war((size_t)n_layers, -1);
     // staging holds the most copies any layer stages and the ring the largest
     // stage: every layer's K chunk is sized for both, so any layer fits
@@ -561,6 +565,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         const int npl_budget = ri == 8 ? 8 : ri + 1;
         stage_max = std::max(stage_max, (size_t)npl_budget * 512 + 128);
         nsteps_max = std::max(nsteps_max, mq::pad256(std::max(layers[i].K, 1)) / 256);
+        if (layers[i].xop == MQ_XOP_ADD_RMSNORM) res_k_max = std::max(res_k_max, layers[i].K);
         nrt_max = std::max(nrt_max, mq::pad16(std::max(layers[i].N, 1)) / 16);
     }
     // CTA-pair reduction slots: at most ceil(n_rt / (sms / 2)) tiles per CTA
@@ -568,7 +573,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     const size_t cl_reserve = cl_max ? (size_t)32 * cl_max + (size_t)cl_max * 32 * nt * 16 : 0;
     // everything but the activation chunk: table, partial slots, zero-point
     // constants, barriers, a 2-deep ring
-    const size_t other = sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
+    const size_t res_bytes = res_k_max ? (((size_t)B * res_k_max * 2 + 15) & ~(size_t)15) + (size_t)B * (res_k_max / 128) * 4 + 16 : 0;
+    const size_t other = res_bytes + sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
                          (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 128 + (size_t)2 * mq::kStackWarps * stage_max + 256;
     // the activation chunk's cap: 80 KB keeps B <= 4 stacks on the measured-best
     // decompositions; B >= 5 would otherwise split K > 2 ways (global split-K
@@ -586,11 +592,28 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < in.N || (in.ldx & 7) ||
             (reinterpret_cast<uintptr_t>(in.X) & 15))
             return fail(MQ_ERR_INVALID, "layer %d: bad shape / alignment", i);
+        if (in.xop < MQ_XOP_NONE || in.xop > MQ_XOP_SILU_MUL) return fail(MQ_ERR_INVALID, "layer %d: bad xop", i);
+        if (in.xop == MQ_XOP_SILU_MUL && in.ldx < 2 * in.K)
+            return fail(MQ_ERR_INVALID, "layer %d: SiLU gating reads [g | u] of 2 K columns", i);
+        if (in.xop == MQ_XOP_ADD_RMSNORM) {
+            if (!in.norm_w || (in.K & 127)) return fail(MQ_ERR_INVALID, "layer %d: add-RMSNorm needs norm_w, K %% 128 == 0", i);
+            if ((in.res_in || in.res_out) && (in.ldres < in.K || (in.ldres & 7)))
+                return fail(MQ_ERR_INVALID, "layer %d: bad residual stride", i);
+            if (!in.res_in && (res_k == 0 || res_k != in.K))
+                return fail(MQ_ERR_INVALID, "layer %d: no kept residual of width %d before it", i, in.K);
+            for (int j = 0; j < i; ++j)
+                if (in.res_in && stack_overlap(in.res_in, in.ldres, in.K, layers[j].Y, layers[j].ldy, layers[j].N, B))
+                    return fail(MQ_ERR_INVALID, "layer %d: the residual is written inside the stack", i);
+            res_k = in.K;
+        }
         if (i == 0) r_first = ri;
         uniform = uniform && ri == r_first;
         const bool child = nplanes == ri;
         const int npl = (child || ri == 8) ? ri : ri + 1;
-        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair);
+        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair,
+                                               in.xop == MQ_XOP_ADD_RMSNORM);
+        if (in.xop == MQ_XOP_ADD_RMSNORM && c.S != 1)
+            return fail(MQ_ERR_INVALID, "layer %d: the fused prologue's row does not fit the staging area", i);
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
         mq::StackLayer& t = T[i];
         memset(&t, 0, sizeof(t));
@@ -610,11 +633,24 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         t.cs = c.cs;
         t.cpc = c.cpc;
         t.out_scale = in.out_scale;
+        t.xop = in.xop;
+        t.res_in = reinterpret_cast<const uint16_t*>(in.res_in);
+        t.res_out = reinterpret_cast<uint16_t*>(in.res_out);
+        t.norm_w = in.norm_w;
+        t.ldres = in.ldres;
+        t.eps = in.eps;
         t.r = ri;
         t.stage_bytes = npl * 512 + 128;
         t.xll = -1;
         t.yll = -1;
         t.war_wait = -1;
+        if (in.xop == MQ_XOP_ADD_RMSNORM && in.res_out)  // over the residual an earlier layer read
+            for (int k = 0; k <= i; ++k)
+                if (layers[k].xop == MQ_XOP_ADD_RMSNORM && layers[k].res_in &&
+                    stack_overlap(layers[k].res_in, layers[k].ldres, layers[k].K, in.res_out, in.ldres, in.K, B)) {
+                    war[(size_t)i] = std::max(war[(size_t)i], k);
+                    res_pub[(size_t)k] = 1;
+                }
         size_t e = 0;
         const int j = stack_x_producer(layers, i, B, &e);
         if (j == -2)
@@ -658,6 +694,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     }
     for (int i = 0; i < n_layers; ++i) {
         T[i].war_wait = war[(size_t)i];
+        if (res_pub[(size_t)i]) T[i].ext_pub = 1;
         T[i].cl_base *= cl_tiles;  // two slot buffers of cl_tiles each
     }
     cl_tiles *= 2;
@@ -672,7 +709,14 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     p.slot_off = (int)((p.cs_off + zc_bytes + 15) & ~(size_t)15);
     const size_t slot_bytes = (size_t)mq::kStackWarps * 32 * nt * 4 * sizeof(float);
     p.table_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
-    p.cl_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
+    p.res_k = res_k_max;
+    p.xops = 0;
+    for (int i = 0; i < n_layers; ++i) p.xops |= layers[i].xop != MQ_XOP_NONE;
+    if (p.xops && (nt != 1 || nplanes != 8))
+        return fail(MQ_ERR_INVALID, "fused activation prologues need B <= 8 and parent layers");
+    p.res_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
+    p.rpart_off = (int)((p.res_off + (size_t)B * res_k_max * 2 + 15) & ~(size_t)15);
+    p.cl_off = (int)((p.rpart_off + (size_t)B * (res_k_max / 128) * 4 + 15) & ~(size_t)15);
     p.cluster = pair ? 1 : 0;
     p.cl_tiles = cl_tiles;
     // [full mbarriers, uses | free mbarriers, free uses] (32 B per tile) + the partial slots
@@ -704,14 +748,14 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
     if (st || !pair) return st;
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
-    if (mq::stack_pair_capacity(P->nt, P->r, P->nplanes == P->r, P->smem) >= P->grid &&
-        mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, true) == cudaSuccess)
+    if (mq::stack_pair_capacity(P->nt, P->r, P->nplanes == P->r, P->smem, P->p.xops) >= P->grid &&
+        mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, true, P->p.xops) == cudaSuccess)
         return MQ_OK;
     // pairs cannot all be resident (or the driver rejects a cooperative cluster
     // launch): plain cooperative CTAs, global split-K
     st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, false);
     if (st) return st;
-    if (mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, false) != cudaSuccess)
+    if (mq::stack_probe(P->nt, P->r, P->nplanes == P->r, P->grid, P->smem, false, P->p.xops) != cudaSuccess)
         return fail(MQ_ERR_CUDA, "mq_stack_plan: the persistent kernel cannot be launched cooperatively "
                                  "(%d CTAs, %zu B shared memory)", P->grid, P->smem);
     return MQ_OK;

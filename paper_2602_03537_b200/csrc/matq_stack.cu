@@ -7,11 +7,11 @@
 namespace mq {
 
 namespace {
-template <int NT, int R, bool CHILD>
+template <int NT, int R, bool CHILD, bool XOPS>
 cudaError_t set_smem(size_t smem) {
     static int smem_set = 0;
     if ((int)smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(k_stack<NT, R, CHILD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k_stack<NT, R, CHILD, XOPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;
         smem_set = (int)smem;
@@ -32,10 +32,10 @@ bool stack_nocoop() {
     return v != 0;
 }
 
-template <int NT, int R, bool CHILD>
+template <int NT, int R, bool CHILD, bool XOPS = false>
 cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaStream_t stream) {
-    auto kern = k_stack<NT, R, CHILD>;
-    cudaError_t e = set_smem<NT, R, CHILD>(smem);
+    auto kern = k_stack<NT, R, CHILD, XOPS>;
+    cudaError_t e = set_smem<NT, R, CHILD, XOPS>(smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -65,9 +65,9 @@ cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaSt
     return e;
 }
 
-template <int NT, int R, bool CHILD>
+template <int NT, int R, bool CHILD, bool XOPS = false>
 int pair_capacity(size_t smem) {
-    if (set_smem<NT, R, CHILD>(smem) != cudaSuccess) return 0;
+    if (set_smem<NT, R, CHILD, XOPS>(smem) != cudaSuccess) return 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2);
     cfg.blockDim = dim3(kStackThreads);
@@ -80,7 +80,7 @@ int pair_capacity(size_t smem) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k_stack<NT, R, CHILD>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, k_stack<NT, R, CHILD, XOPS>, &cfg) != cudaSuccess) {
         (void)cudaGetLastError();
         return 0;
     }
@@ -92,6 +92,10 @@ template <int R>
 cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, size_t smem,
                            cudaStream_t stream) {
     constexpr bool kChildOk = R < 8;
+    if (p.xops) {  // fused prologues: parents at NT = 1 only (the planner checks)
+        if (nt != 1 || (child && kChildOk)) return cudaErrorInvalidValue;
+        return launch_one_stack<1, R, false, true>(p, grid, smem, stream);
+    }
     if (child && kChildOk) {
         if (nt == 1) return launch_one_stack<1, R, kChildOk>(p, grid, smem, stream);
         return launch_one_stack<2, R, kChildOk>(p, grid, smem, stream);
@@ -101,16 +105,21 @@ cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, s
 }
 
 cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream) {
+    if (p.xops) {
+        if (nt != 1) return cudaErrorInvalidValue;
+        return launch_one_stack<1, 0, false, true>(p, grid, smem, stream);
+    }
     if (nt == 1) return launch_one_stack<1, 0, false>(p, grid, smem, stream);
     return launch_one_stack<2, 0, false>(p, grid, smem, stream);
 }
 
 // Plan-time probe: launch the planned kernel with the planned attributes and no
 // layers (it returns at entry) and report whether the driver accepts it.
-cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster) {
+cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster, bool xops) {
     StackParams p{};
     p.n_layers = 0;
     p.cluster = cluster ? 1 : 0;
+    p.xops = xops ? 1 : 0;
     cudaError_t e = r == 0 ? launch_stack_mixed(p, nt, grid, smem, 0) : cudaSuccess;
     if (r != 0) {
         switch (r) {
@@ -126,8 +135,19 @@ cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool c
     return e;
 }
 
-int stack_pair_capacity(int nt, int r, bool child, size_t smem) {
+int stack_pair_capacity(int nt, int r, bool child, size_t smem, bool xops) {
     const bool c = child && r < 8;
+    if (xops) {
+        if (nt != 1 || c) return 0;  // c: a child slice (r < 8)
+        switch (r) {
+            case 0: return pair_capacity<1, 0, false, true>(smem);
+            case 2: return pair_capacity<1, 2, false, true>(smem);
+            case 3: return pair_capacity<1, 3, false, true>(smem);
+            case 4: return pair_capacity<1, 4, false, true>(smem);
+            case 6: return pair_capacity<1, 6, false, true>(smem);
+            default: return pair_capacity<1, 8, false, true>(smem);
+        }
+    }
 #define MQ_CAP(R)                                                                   \
     if (r == R) {                                                                   \
         if (nt == 1) return c ? pair_capacity<1, R, (R < 8)>(smem) : pair_capacity<1, R, false>(smem); \

@@ -53,6 +53,12 @@ struct __align__(8) StackLayer {
                       // of the mean; a tile cut by a CTA boundary is summed through fl_off
     long long fl_off;  // word offset in StackParams::ll of [grid][32 lanes][NT * 4] LL words: slot c
                        // holds CTA c + 1's part of CTA c's last tile
+    int xop;          // activation prologue fused into staging (MQ_XOP_*: 0 none, 1 add + RMSNorm, 2 SiLU gating)
+    const uint16_t* res_in;  // xop 1: bf16 residual [B][ldres], or null: the smem residual of the previous xop-1 layer
+    uint16_t* res_out;       // xop 1: CTA 0 writes the updated residual here (or null)
+    const float* norm_w;     // xop 1: RMSNorm weight [K]
+    int ldres;
+    float eps;
     int tk_off;       // S > 1 through the workspace: this layer's own tickets (StackParams::tickets + tk_off)
     long long ws_off;  // and its own partials (StackParams::ws + ws_off): no layer reuses another's, since
                        // without grid barriers a fast CTA may already be a layer ahead
@@ -71,6 +77,10 @@ struct StackParams {
     int stages;        // per-warp ring depth
     int stage_stride;  // bytes per ring slot (the largest stage of the stack)
     int cluster;       // 1: CTA pairs (cluster of 2); S == 2 layers reduce through DSMEM
+    int res_off;       // xop-1 stacks: byte offset of the kept residual [B][res_k] bf16 ...
+    int rpart_off;     // ... and of its per-(row, 128-column group) sums of squares [B][res_k / 128]
+    int res_k;
+    int xops;          // some layer has a fused prologue: the XOPS kernel instantiation (NT = 1, parents)
     int cl_off;        // byte offset of the pair-reduction area: [cl_tiles mbarriers][cl_tiles use counters][slots]
     int cl_tiles;      // most row tiles a CTA holds in an S == 2 layer
     float* ws;         // split-K partials (per layer: StackLayer::ws_off)
@@ -370,6 +380,91 @@ __device__ __forceinline__ void ld_ll2(const unsigned long long* p, unsigned lon
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
 
+// 16 bf16 activations of row b from column col (LL words polled until tagged,
+// or plain loads): lo / hi halves guarded by the caller's bounds
+__device__ __forceinline__ void load_x16(const StackParams& p, const StackLayer& L, int b, int col, bool hi_ok,
+                                         uint32_t tag, uint32_t (&w)[8]) {
+    if (L.xll >= 0) {
+        const unsigned long long* src = p.ll + L.xll + (long long)b * L.ldxll + (col >> 1);
+        unsigned long long v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = (unsigned long long)tag << 32;
+        for (;;) {
+            ld_ll2(src, v[0], v[1]);
+            ld_ll2(src + 2, v[2], v[3]);
+            if (hi_ok) {
+                ld_ll2(src + 4, v[4], v[5]);
+                ld_ll2(src + 6, v[6], v[7]);
+            }
+            bool ok = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) ok = ok && (uint32_t)(v[i] >> 32) == tag;
+            if (ok) break;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) w[i] = (uint32_t)v[i];
+    } else {
+        const uint16_t* src = L.X + (long long)b * L.ldx + col;
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src));
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = w[5] = w[6] = w[7] = 0u;
+        if (hi_ok) {
+            const uint4 c = __ldcg(reinterpret_cast<const uint4*>(src + 8));
+            w[4] = c.x; w[5] = c.y; w[6] = c.z; w[7] = c.w;
+        }
+    }
+}
+
+// Add + RMSNorm prologue, pass 1 (consumer threads; the layer is one K chunk):
+// R <- bf16(R + X) into the kept residual (R from res_in, or the residual the
+// previous add-norm layer kept), and per (row, 128-column group) sums of R^2 --
+// summed in group order by the staging pass (deterministic).
+__device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, const StackLayer& L, uint32_t tag,
+                                                      uint8_t* smem_base) {
+    constexpr int kOctets = kConsumerThreads / 8;
+    const int ol = threadIdx.x & 7;
+    const int ngroups = L.K >> 7;
+    uint16_t* res = reinterpret_cast<uint16_t*>(smem_base + p.res_off);
+    float* part = reinterpret_cast<float*>(smem_base + p.rpart_off);
+    const int oct0 = (threadIdx.x >> 5) * 4;
+    for (int base = oct0; base < p.B * ngroups; base += kOctets) {  // warp-uniform trip count
+        const int task = base + ((threadIdx.x >> 3) & 3);
+        const bool active = task < p.B * ngroups;
+        const int b = active ? udiv_small(task, ngroups) : 0, grp = task - b * ngroups;
+        const int col = (grp << 7) + (ol << 4);
+        float ss = 0.0f;
+        if (active) {
+            uint32_t d[8], r[8];
+            load_x16(p, L, b, col, true, tag, d);
+            if (L.res_in) {
+                const uint16_t* src = L.res_in + (long long)b * L.ldres + col;
+                const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src)), c = __ldcg(reinterpret_cast<const uint4*>(src + 8));
+                r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = c.x; r[5] = c.y; r[6] = c.z; r[7] = c.w;
+            } else {
+                const uint4 a = *reinterpret_cast<const uint4*>(res + b * p.res_k + col);
+                const uint4 c = *reinterpret_cast<const uint4*>(res + b * p.res_k + col + 8);
+                r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = c.x; r[5] = c.y; r[6] = c.z; r[7] = c.w;
+            }
+            uint32_t o[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint16_t v0 = f32_to_bf16_rn(__uint_as_float(r[i] << 16) + __uint_as_float(d[i] << 16));
+                const uint16_t v1 = f32_to_bf16_rn(__uint_as_float(r[i] & 0xFFFF0000u) + __uint_as_float(d[i] & 0xFFFF0000u));
+                const float f0 = bf16_to_f32(v0), f1 = bf16_to_f32(v1);
+                ss += f0 * f0 + f1 * f1;
+                o[i] = (uint32_t)v0 | ((uint32_t)v1 << 16);
+            }
+            *reinterpret_cast<uint4*>(res + b * p.res_k + col) = make_uint4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<uint4*>(res + b * p.res_k + col + 8) = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+        __syncwarp();
+        ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+        ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+        if (active && ol == 0) part[b * (p.res_k >> 7) + grp] = ss;
+    }
+}
+
 // Stage X[:, chunk] into shared memory (consumer threads).  An octet of lanes
 // takes one (batch row, 128-column group); each lane 16 columns.  From LL words
 // (polled) or plain bf16 (X from outside the step).  Per mode:
@@ -379,9 +474,9 @@ __device__ __forceinline__ void ld_ll2(const unsigned long long* p, unsigned lon
 //        for the output: tot += s * (acc / lambda_g - c / lambda_g);
 //   ZP   (bf16, r != 8, one n-tile): copies x * 2^-o and the zero-point constant;
 //   else a plain copy.
-template <int R, int NT, bool F16, bool ZP, int NCOPY>
+template <int R, int NT, bool F16, bool ZP, int NCOPY, bool XOPS>
 __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLayer& L, uint16_t* xs, float* zc,
-                                            int col_base, int Kc, uint32_t tag) {
+                                            int col_base, int Kc, uint32_t tag, const uint8_t* smem_base) {
     constexpr int kOctets = kConsumerThreads / 8;
     const int ol = threadIdx.x & 7;
     const int ngroups = Kc >> 7;
@@ -400,7 +495,24 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i] = 0u;
         const bool lo_ok = active && col < L.K, hi_ok = active && col + 8 < L.K;  // K % 8 == 0
-        if (L.xll >= 0) {
+        if (XOPS && L.xop == 1) {
+            // X' = bf16(R * rsqrt(mean(R^2) + eps) * w); R (already R + delta) kept in smem by the pre-pass
+            if (lo_ok) {
+                const uint16_t* rr = reinterpret_cast<const uint16_t*>(smem_base + p.res_off) + b * p.res_k + col;
+                const float* part = reinterpret_cast<const float*>(smem_base + p.rpart_off) + b * (p.res_k >> 7);
+                float ss = 0.0f;
+                for (int gi = 0; gi < (L.K >> 7); ++gi) ss += part[gi];  // fixed order: deterministic
+                const float inv = rsqrtf(ss / (float)L.K + L.eps);
+                const uint4 r0 = *reinterpret_cast<const uint4*>(rr), r1 = *reinterpret_cast<const uint4*>(rr + 8);
+                const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const float a = __uint_as_float(rw[i] << 16) * inv * __ldg(L.norm_w + col + 2 * i);
+                    const float c = __uint_as_float(rw[i] & 0xFFFF0000u) * inv * __ldg(L.norm_w + col + 2 * i + 1);
+                    w[i] = (uint32_t)f32_to_bf16_rn(a) | ((uint32_t)f32_to_bf16_rn(c) << 16);
+                }
+            }
+        } else if (L.xll >= 0) {
             const unsigned long long* src = p.ll + L.xll + (long long)b * L.ldxll + (col >> 1);
             unsigned long long v[8];
 #pragma unroll
@@ -433,6 +545,18 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
             if (hi_ok) {
                 const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src + 8));
                 w[4] = a.x; w[5] = a.y; w[6] = a.z; w[7] = a.w;
+            }
+        }
+        if (XOPS && L.xop == 2 && lo_ok) {  // SiLU gating: u sits K columns after g in the same rows
+            uint32_t u[8];
+            load_x16(p, L, b, col + L.K, hi_ok, tag, u);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float g0 = __uint_as_float(w[i] << 16), g1 = __uint_as_float(w[i] & 0xFFFF0000u);
+                const float s0 = bf16_to_f32(f32_to_bf16_rn(g0 / (1.0f + __expf(-g0))));  // torch: silu in bf16
+                const float s1 = bf16_to_f32(f32_to_bf16_rn(g1 / (1.0f + __expf(-g1))));
+                w[i] = (uint32_t)f32_to_bf16_rn(s0 * __uint_as_float(u[i] << 16)) |
+                       ((uint32_t)f32_to_bf16_rn(s1 * __uint_as_float(u[i] & 0xFFFF0000u)) << 16);
             }
         }
         __syncwarp();
@@ -540,7 +664,7 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
 // One layer of the step, slice width R.  Uniform stacks instantiate k_stack
 // with R fixed; heterogeneous stacks (an EvoPress configuration: per-layer r)
 // dispatch here on the layer table's r -- the ring and cursor are shared.
-template <int R, int NT, bool CHILD, bool FIXED>
+template <int R, int NT, bool CHILD, bool FIXED, bool XOPS>
 __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLayer* tab, int l,
                                             const RingCtx& rc, int& cstage, uint32_t& parity,
                                             StackShared& sh, uint8_t* smem, unsigned long long target) {
@@ -572,7 +696,11 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // consumer_sync that ends every layer)
     MQ_STS(l, 0);
     MQ_STS(l, 1);
-    stack_stage<R, NT, F16, ZP, NCOPY>(p, L, xs, zc, col_base, Kc, sh.tag);
+    if (XOPS && L.xop == 1) {  // add + RMSNorm: the residual update and the row sums first
+        stack_addnorm_prepass(p, L, sh.tag, smem);
+        consumer_sync();
+    }
+    stack_stage<R, NT, F16, ZP, NCOPY, XOPS>(p, L, xs, zc, col_base, Kc, sh.tag, smem);
     if (threadIdx.x == kSyncThread && L.war_wait >= 0 && L.war_wait < l) {
         // this layer overwrites a buffer an earlier layer read from outside the
         // step: every CTA must have staged it (almost always long done)
@@ -587,6 +715,14 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 while (ld_acquire_u64(p.done + l) < target) {
                 }
             consumer_sync();
+        }
+    }
+    if (XOPS && L.res_out && blockIdx.x == 0) {  // the updated residual for the next kernel (after the WAR wait)
+        const uint16_t* res = reinterpret_cast<const uint16_t*>(smem + p.res_off);
+        for (int i = threadIdx.x; i < p.B * (L.K >> 3); i += kConsumerThreads) {
+            const int b = udiv_small(i, L.K >> 3), c = (i - b * (L.K >> 3)) * 8;
+            *reinterpret_cast<uint4*>(L.res_out + (long long)b * L.ldres + c) =
+                *reinterpret_cast<const uint4*>(res + b * p.res_k + c);
         }
     }
     MQ_STS(l, 2);
@@ -942,7 +1078,9 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
 }
 
 // RFIX = the uniform slice width, or 0: per-layer r from the table (parents only)
-template <int NT, int RFIX, bool CHILD>
+// XOPS: the layers may carry fused activation prologues (mq_stack_layer.xop); the
+// headline stacks run the XOPS = false instantiation, free of their code
+template <int NT, int RFIX, bool CHILD, bool XOPS = false>
 __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
     __shared__ StackShared sh;
@@ -1019,14 +1157,14 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
 #pragma unroll 1
     for (int l = 0; l < p.n_layers; ++l) {
         if constexpr (RFIX != 0) {
-            stack_layer<RFIX, NT, CHILD, true>(p, tab, l, rc, cstage, parity, sh, smem, target);
+            stack_layer<RFIX, NT, CHILD, true, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target);
         } else {
             switch (tab[l].r) {
-                case 2: stack_layer<2, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
-                case 3: stack_layer<3, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
-                case 4: stack_layer<4, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
-                case 6: stack_layer<6, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
-                default: stack_layer<8, NT, false, false>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 2: stack_layer<2, NT, false, false, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 3: stack_layer<3, NT, false, false, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 4: stack_layer<4, NT, false, false, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                case 6: stack_layer<6, NT, false, false, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
+                default: stack_layer<8, NT, false, false, XOPS>(p, tab, l, rc, cstage, parity, sh, smem, target); break;
             }
         }
     }
@@ -1041,8 +1179,8 @@ cudaError_t launch_stack_r(const StackParams& p, int nt, bool child, int grid, s
 cudaError_t launch_stack_mixed(const StackParams& p, int nt, int grid, size_t smem, cudaStream_t stream);
 // CTAs of k_stack<nt, r, child> (r = 0: the mixed kernel) that can be co-resident as
 // clusters of 2 with `smem` bytes each, or 0 when unknown
-int stack_pair_capacity(int nt, int r, bool child, size_t smem);
+int stack_pair_capacity(int nt, int r, bool child, size_t smem, bool xops);
 // launch the planned configuration with no layers: does the driver accept it?
-cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster);
+cudaError_t stack_probe(int nt, int r, bool child, int grid, size_t smem, bool cluster, bool xops);
 
 }  // namespace mq

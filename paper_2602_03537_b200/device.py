@@ -354,7 +354,10 @@ class StackProgram:
     graph-capturable launch.
     """
 
-    def __init__(self, layers, r, B: int):
+    def __init__(self, layers, r, B: int, ops=None):
+        """``ops``: optional per-layer activation prologue (None or a dict with xop,
+        res_in, res_out, norm_w, eps: mq_stack_layer's fused residual-add + RMSNorm /
+        SiLU gating)."""
         import ctypes
 
         _lib.require_cuda()
@@ -377,6 +380,19 @@ class StackProgram:
                 raise ValueError("stack activations must be bf16 with unit column stride")
             arr[i] = _lib.StackLayer(_lib.ptr(pt.blob), X.data_ptr(), Y.data_ptr(), X.stride(0), Y.stride(0),
                                      pt.N, pt.K, scale, rs[i])
+            op = ops[i] if ops else None
+            if op:
+                arr[i].xop = int(op["xop"])
+                for key in ("res_in", "res_out"):
+                    t = op.get(key)
+                    if t is not None:
+                        if t.dtype != torch.bfloat16 or t.stride(1) != 1:
+                            raise ValueError("the residual must be bf16 with unit column stride")
+                        setattr(arr[i], key, t.data_ptr())
+                        arr[i].ldres = t.stride(0)
+                if op.get("norm_w") is not None:
+                    arr[i].norm_w = op["norm_w"].data_ptr()
+                arr[i].eps = float(op.get("eps", 1e-5))
         r_plan = rs[0] if len(set(rs)) == 1 else 0
         if r_plan == 0 and nplanes != 8:
             raise ValueError("per-layer bit-widths need parent layers")
@@ -387,7 +403,7 @@ class StackProgram:
                   ctypes.byref(ws))
         self.table = torch.frombuffer(bytearray(table.raw), dtype=torch.uint8).cuda()
         self.ws = torch.zeros(max(ws.value, 1), dtype=torch.uint8, device="cuda")
-        self._keep = layers  # the tensors the table points at
+        self._keep = (layers, ops)  # the tensors the table points at
         self.n_layers = n
 
     def run(self, stream=None) -> None:

@@ -48,9 +48,17 @@ def _rope(x: torch.Tensor, cos: torch.Tensor, sin: torch.Tensor) -> torch.Tensor
 class LlamaDecoder:
     def __init__(self, shape: DecoderShape = LLAMA31_8B, batch: int = 1, context: int = 256,
                  bits=4, vocab: int = 128256, seed: int = 0, n_layers: int | None = None, glue: str = "cuda",
-                 tp: int = 1, rank: int = 0, process_group=None):
+                 tp: int = 1, rank: int = 0, process_group=None, linears: str | None = None):
         if glue not in ("cuda", "torch"):
             raise ValueError("glue must be 'cuda' or 'torch'")
+        # "k3s": per block ONE persistent launch for o -> gate_up -> down -> next qkv with the
+        # residual add + RMSNorm and the SiLU gating fused into the layers' activation staging
+        # (single GPU, B <= 4); "k3": per-layer GEMV launches + the glue kernels
+        if linears is None:
+            linears = "k3s" if (tp == 1 and batch <= 4 and glue == "cuda") else "k3"
+        if linears not in ("k3", "k3s") or (linears == "k3s" and (tp > 1 or glue != "cuda")):
+            raise ValueError("linears must be 'k3' or 'k3s' (k3s: single GPU, CUDA glue)")
+        self.linears = linears
         self.shape, self.B, self.T, self.glue = shape, batch, context, glue
         self.tp, self.rank, self.pg = tp, rank, process_group
         self.n_layers = n_layers or shape.n_layers
@@ -122,9 +130,10 @@ class LlamaDecoder:
         e = lambda *sz: torch.empty(*sz, device=dev, dtype=torch.bfloat16)  # noqa: E731
         self.buf = {"x": e(batch, h), "hn": e(batch, h), "qkv": e(batch, nq + 2 * self.nkv * hd),
                     "q": e(batch, self.nh, 1, hd), "o": e(batch, h), "gu": e(batch, 2 * inter),
-                    "act": e(batch, inter), "d": e(batch, h)}
+                    "act": e(batch, inter), "d": e(batch, h), "att": e(batch, nq), "xr": e(batch, h)}
         self.stream = torch.cuda.Stream()
         self.graph = None
+        self.segments = None
 
     def _all_reduce(self, t: torch.Tensor) -> None:
         if self.tp > 1:
@@ -153,6 +162,33 @@ class LlamaDecoder:
                 r = bits if isinstance(bits, int) else bits["layers.%d.%s" % (i, kind)]
                 blk[kind].set_bits(r)
         self.graph = None
+        self.segments = None
+
+    def _build_segments(self) -> None:
+        """K3S programs: block i's [o_i, gate_up_i (+ x += o; RMSNorm ln2), down_i (+ SiLU
+        gating), qkv_{i+1} (+ x += down; RMSNorm ln1 of block i+1; x written back)]; the
+        last block writes its post-attention residual to buf['xr'] for the final norm."""
+        from . import _lib
+        from .device import StackProgram
+
+        b, h, nb = self.buf, self.shape.hidden, len(self.blocks)
+        self.segments = []
+        for i, blk in enumerate(self.blocks):
+            layers = [(blk["o"].planes, b["att"], b["o"]), (blk["gate_up"].planes, b["o"], b["gu"]),
+                      (blk["down"].planes, b["gu"], b["d"])]
+            rs = [blk["o"].bits, blk["gate_up"].bits, blk["down"].bits]
+            last = i == nb - 1
+            ops = [None,
+                   dict(xop=_lib.MQ_XOP_ADD_RMSNORM, res_in=b["x"], res_out=b["xr"] if last else None,
+                        norm_w=blk["ln2"], eps=1e-5),
+                   dict(xop=_lib.MQ_XOP_SILU_MUL)]
+            if not last:
+                nxt = self.blocks[i + 1]
+                layers.append((nxt["qkv"].planes, b["d"], b["qkv"]))
+                rs.append(nxt["qkv"].bits)
+                ops.append(dict(xop=_lib.MQ_XOP_ADD_RMSNORM, res_in=None, res_out=b["x"],
+                                norm_w=nxt["ln1"], eps=1e-5))
+            self.segments.append(StackProgram(layers, rs[0] if len(set(rs)) == 1 else rs, self.B, ops=ops))
 
     def linear_bytes(self) -> int:
         from .device import algorithmic_bytes
@@ -165,10 +201,50 @@ class LlamaDecoder:
         return tot
 
     def _forward(self) -> None:
-        if self.glue == "cuda":
-            self._forward_fused()
-        else:
+        if self.glue != "cuda":
             self._forward_torch()
+        elif self.linears == "k3s":
+            self._forward_k3s()
+        else:
+            self._forward_fused()
+
+    def _forward_k3s(self, parts=("linear", "attn", "glue", "comm", "head")) -> None:
+        """One decode step with one K3S launch per block (o, gate_up, down and the
+        next block's qkv; the residual / RMSNorm / SiLU glue fused into staging):
+        per block K3S + rotary/KV + SDPA."""
+        from . import _lib
+
+        if self.segments is None:
+            self._build_segments()
+        s = self.shape
+        B, hd, T = self.B, s.head_dim, self.T
+        nh, nkv, h = self.nh, self.nkv, s.hidden
+        b = self.buf
+        st = _lib.stream_ptr(None)
+        lin, attn, glue, head = ("linear" in parts), ("attn" in parts), ("glue" in parts), ("head" in parts)
+        if head:
+            torch.index_select(self.embed, 0, self.tokens, out=b["x"])
+        blk0 = self.blocks[0]
+        if glue:
+            _lib.call("mq_add_rmsnorm", _lib.ptr(b["x"]), None, _lib.ptr(blk0["ln1"]), _lib.ptr(b["hn"]),
+                      B, h, 1e-5, st)
+        if lin:
+            blk0["qkv"].planes.linear(b["hn"], blk0["qkv"].bits, out=b["qkv"], pdl=True)
+        for i, blk in enumerate(self.blocks):
+            if attn:
+                qn = _lib.ptr(blk["qn"]) if s.qk_norm else None
+                kn = _lib.ptr(blk["kn"]) if s.qk_norm else None
+                _lib.call("mq_qknorm_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin),
+                          _lib.ptr(b["q"]), _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T,
+                          qn, kn, 1e-6, st)
+                b["att"].copy_(self._attend(b["q"], blk["kc"], blk["vc"]).reshape(B, nh * hd))
+            if lin:
+                self.segments[i].run(torch.cuda.current_stream())
+        if glue:
+            _lib.call("mq_add_rmsnorm", _lib.ptr(b["xr"]), _lib.ptr(b["d"]), _lib.ptr(self.final_norm),
+                      _lib.ptr(b["hn"]), B, h, 1e-5, st)
+        if head:
+            torch.matmul(b["hn"], self.lm_head.t(), out=self.logits)
 
     PARTS = ("linear", "attn", "glue", "comm", "head")
 
@@ -248,12 +324,13 @@ class LlamaDecoder:
             e1.synchronize()
             return e0.elapsed_time(e1) / reps
 
-        out = {"step": time_graph(lambda: self._forward_fused())}
+        fwd = self._forward_k3s if self.linears == "k3s" else self._forward_fused
+        out = {"step": time_graph(lambda: fwd()), "linears": self.linears}
         for part in self.PARTS:
             if part == "comm" and self.tp == 1:
                 continue
-            out[part] = time_graph(lambda p=part: self._forward_fused(parts=(p,)))
-        out["sum_of_parts"] = sum(v for k, v in out.items() if k != "step")
+            out[part] = time_graph(lambda p=part: fwd(parts=(p,)))
+        out["sum_of_parts"] = sum(v for k, v in out.items() if k not in ("step", "linears"))
         return out
 
     def _forward_torch(self) -> None:

@@ -78,11 +78,14 @@ def _fp32_reference(dec, r):
     return rms(x, dec.final_norm) @ dec.lm_head.float().t()
 
 
+@pytest.mark.parametrize("linears", ["k3", "k3s"])
 @pytest.mark.parametrize("qk_norm", [False, True], ids=["llama-gqa", "qwen3-qknorm"])
 @pytest.mark.parametrize("r", [4, 8])
-def test_decoder_step_vs_fp32_dequantised_reference(llama, qk_norm, r):
+def test_decoder_step_vs_fp32_dequantised_reference(llama, qk_norm, r, linears):
+    """linears = k3s: one persistent launch per block with the residual add +
+    RMSNorm and the SiLU gating fused into the layers' activation staging."""
     shape = _shape(qk_norm=qk_norm)
-    dec = llama.LlamaDecoder(shape, batch=3, context=16, bits=r, vocab=1024)
+    dec = llama.LlamaDecoder(shape, batch=3, context=16, bits=r, vocab=1024, linears=linears)
     dec.tokens.copy_(torch.tensor([1, 77, 500], device="cuda"))
     with torch.cuda.stream(dec.stream):
         dec._forward()
@@ -152,3 +155,23 @@ def test_decoder_tp2_gloo_matches_single_gpu(llama, kv):
     kv_, nh, nkv, err = q.get()
     assert nh == 4 and nkv == (1 if kv == 2 else 1)
     assert err <= 3e-2, err
+
+
+@pytest.mark.parametrize("B", [1, 4])
+def test_decoder_k3s_segments_match_per_layer_path(llama, B):
+    """The fused K3S block segments against the per-layer K3 + glue-kernel step
+    (same weights): only summation orders differ; graph replays are bitwise stable."""
+    outs = {}
+    for lin in ("k3", "k3s"):
+        dec = llama.LlamaDecoder(_shape(), batch=B, context=16, bits=4, vocab=1024, linears=lin)
+        dec.tokens.copy_(torch.arange(B, device="cuda") * 13 + 1)
+        torch.cuda.synchronize()
+        dec.step()
+        torch.cuda.synchronize()
+        outs[lin] = dec.logits.float().clone()
+        if lin == "k3s":
+            assert len(dec.segments) == dec.n_layers
+            dec.step()
+            torch.cuda.synchronize()
+            assert torch.equal(dec.logits.float(), outs[lin])
+    assert rel_err(outs["k3s"].cpu().numpy(), outs["k3"].cpu().numpy()) <= 2e-2
