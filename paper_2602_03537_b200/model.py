@@ -179,8 +179,7 @@ class LinearStack:
     def stack_kernel_ok(self, config) -> bool:
         """Where the persistent K3S path is the default (single GPU, B <= 16,
         G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix*.txt):
-        * uniform r: at B <= 4 always; at B = 8-16 for r <= 3 (1.3x at r = 3)
-          -- for r >= 4 the graph wins there;
+        * uniform r: see the table in the body (profiles/r2_dispatch_matrix.txt);
         * heterogeneous (per-layer r, parents): fused stacks at B <= 4 (1.10x at
           B = 1).  Unfused ones (224 linears, the k/v ones only 1024 rows)
           measure at par at B = 1 and the graph wins at larger B.
@@ -188,9 +187,12 @@ class LinearStack:
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
         if len(rs) == 1:
-            # round 2 (LL hand-off, stream-K): B = 8 / 16 at r = 4 measure 2.71 / 4.08 ms
-            # on K3S against 2.41 / 3.12 on the graph; r <= 3 still win there (1.68 vs 2.26)
-            ok = self.B <= 4 or max(rs) <= 3
+            # measured (scripts/dispatch_matrix.py, profiles/r2_dispatch_matrix.txt): K3S wins
+            # at B <= 2 for every r, at B <= 4 but r = 8, at B <= 8 for r in {2, 3, 6} and at
+            # B = 16 for r = 2 only; the fp16 staging path (r in {4, 8}) degrades with B
+            r0 = next(iter(rs))
+            ok = (self.B <= 2 or (self.B <= 4 and r0 != 8) or (self.B <= 8 and r0 in (2, 3, 6))
+                  or r0 == 2)
         else:
             ok = self.fused and parents and self.B <= 4
         return ok and self.B <= 16 and self.G == 128  # tp > 1: one K3S launch per all-reduce segment
