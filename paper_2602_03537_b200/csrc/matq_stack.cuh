@@ -695,12 +695,12 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // (the previous layer's readers of the staging area are done: the
     // consumer_sync that ends every layer)
     MQ_STS(l, 0);
-    MQ_STS(l, 1);
     if (XOPS && L.xop == 1) {  // add + RMSNorm: the residual update and the row sums first
         stack_addnorm_prepass(p, L, sh.tag, smem);
         consumer_sync();
     }
     stack_stage<R, NT, F16, ZP, NCOPY, XOPS>(p, L, xs, zc, col_base, Kc, sh.tag, smem);
+    MQ_STS_WMAX(l, 1);  // this warp's staging tasks done (max over warps)
     if (threadIdx.x == kSyncThread && L.war_wait >= 0 && L.war_wait < l) {
         // this layer overwrites a buffer an earlier layer read from outside the
         // step: every CTA must have staged it (almost always long done)
@@ -745,7 +745,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             xrow_addr[nt][s2] = xs_saddr + (uint32_t)(cp * p.xcopy_stride + n * p.xs_stride + 8 * mi) * 2u;
         }
     }
-    MQ_STS(l, 3);
+
 
     // ---- this warp's units of layer l --------------------------------------
     float tot[NT][4], acc[NT][4];
@@ -1026,6 +1026,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             // CTA's part (a tile running past this CTA's range), in that order
             if (!lend) {
                 named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, llast)));
+                if (f == wp.f1) MQ_STS_WMAX(l, 3);  // the parts of this warp's last tile arrived
                 const int vmax = last_warp_at(wp, llast);
                 for (int w2 = warp + 1; w2 <= vmax; ++w2) {
                     if (plan_f0(wp, w2) == plan_f0(wp, w2 + 1)) continue;  // no steps: no part
@@ -1053,6 +1054,7 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
                 for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
                     for (int i = 0; i < 4; ++i) tot[nt][i] += __uint_as_float((uint32_t)v[nt * 4 + i]);
+                MQ_STS_WMAX(l, 7);  // the next CTA's part arrived
             }
             if (tstart < wp.fo) {  // the tile started in the previous CTA: ship this part there
                 unsigned long long* dst = remote_slot(rc.cta - 1);
@@ -1069,12 +1071,11 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             ++lt;
         }
     }
-    MQ_STS(l, 4);
+    MQ_STS_WMAX(l, 4);  // this warp's tiles emitted (max over warps)
 
     // ---- end of layer l: the staging area and the partial slots are free again
     consumer_sync();
     MQ_STS(l, 6);
-    MQ_STS(l, 7);
 }
 
 // RFIX = the uniform slice width, or 0: per-layer r from the table (parents only)
