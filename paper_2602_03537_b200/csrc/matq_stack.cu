@@ -1,15 +1,20 @@
 // matq_stack.cu -- K3S instantiations and cooperative launcher.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
 
 #include "matq_stack.cuh"
 
 namespace mq {
 
 namespace {
+// the kernel's dynamic shared-memory limit only grows; serialised (plans and runs may
+// come from several host threads)
 template <int NT, int R, bool CHILD, bool XOPS>
 cudaError_t set_smem(size_t smem) {
+    static std::mutex mu;
     static int smem_set = 0;
+    std::lock_guard<std::mutex> lk(mu);
     if ((int)smem > smem_set) {
         cudaError_t e = cudaFuncSetAttribute(k_stack<NT, R, CHILD, XOPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
