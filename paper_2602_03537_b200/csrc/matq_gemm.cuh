@@ -282,33 +282,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty(buf));
             if (p.S > 1) {
-                // publish the partial.  coop (every unit resident at once): each split waits
-                // for all S partials and reduces a 1/S share of the columns; otherwise the
-                // last split to arrive reduces the tile.  Split order either way
-                // (deterministic).
+                // publish the partial.  coop (every unit resident at once): the whole CTA
+                // reduces a 1/S share of the tile's columns after the role loops (below);
+                // otherwise the last split to arrive reduces the tile here.  Split order
+                // either way (deterministic).
                 __threadfence();
                 named_bar_sync(1, 128);
                 if (et == 0) *flag_ptr = atom_add_acq_rel(p.tickets + tile, 1);
                 named_bar_sync(1, 128);
+                if (p.coop) return;
                 const int arrived = *flag_ptr;
-                int q_lo = 0, q_hi = 0;  // column quads [q_lo, q_hi) reduced here
-                const int nq = (b_lim + 3) >> 2;
-                if (p.coop) {
-                    if (et == 0)
-                        while (ld_acquire_s32(p.tickets + tile) < p.S) {
-                        }
-                    named_bar_sync(1, 128);
-                    q_lo = split * nq / p.S;
-                    q_hi = (split + 1) * nq / p.S;
-                } else if (arrived == p.S - 1) {
-                    q_hi = nq;
-                }
+                const int q_hi = arrived == p.S - 1 ? (b_lim + 3) >> 2 : 0;  // column quads reduced here
                 __threadfence();
                 const float4* t0 = reinterpret_cast<const float4*>(p.ws + (long long)tile * p.S * (BN * kGemmBM));
                 const long long sstride = (long long)(BN / 4) * kGemmBM;  // float4s per split
                 if (row < p.N) {
 #pragma unroll 1
-                    for (int q0 = q_lo; q0 < q_hi; q0 += 4) {
+                    for (int q0 = 0; q0 < q_hi; q0 += 4) {
                         float4 acc[4];
 #pragma unroll
                         for (int u = 0; u < 4; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -336,13 +326,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
                 }
                 named_bar_sync(1, 128);
-                if (et == 0) {
-                    if (p.coop) {  // the last split through resets the ticket (2 S arrivals)
-                        if (atom_add_acq_rel(p.tickets + tile, 1) == 2 * p.S - 1) p.tickets[tile] = 0;
-                    } else if (arrived == p.S - 1) {
-                        p.tickets[tile] = 0;
-                    }
-                }
+                if (et == 0 && arrived == p.S - 1) p.tickets[tile] = 0;
                 named_bar_sync(1, 128);  // flag slot reuse
             }
         };
@@ -415,6 +399,66 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (p.coop && my_units == 1) {
+        // coop split-K: once all S partials of this CTA's tile exist, all 23 warps reduce this
+        // split's 1/S share of the columns (flattened (column quad, row) tasks, rows fastest:
+        // coalesced loads and Y stores; four tasks in flight per thread)
+        int tile, split, st0, nst;
+        unit_of(0, tile, split, st0, nst);
+        const int mt = tile / p.n_bt, bt = tile % p.n_bt;
+        const int b_lim = min(BN, p.B - bt * BN);
+        const int nq = (b_lim + 3) >> 2;
+        const int q_lo = split * nq / p.S, q_hi = (split + 1) * nq / p.S;
+        if (threadIdx.x == 0)
+            while (ld_acquire_s32(p.tickets + tile) < p.S) {
+            }
+        __syncthreads();
+        __threadfence();
+        const float4* t0 = reinterpret_cast<const float4*>(p.ws + (long long)tile * p.S * (BN * kGemmBM));
+        const long long sstride = (long long)(BN / 4) * kGemmBM;
+        const int ntask = (q_hi - q_lo) * kGemmBM;
+        constexpr int kU = 4;
+#pragma unroll 1
+        for (int base = threadIdx.x; base < ntask; base += kU * kGemmThreads) {
+            float4 acc[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int sp = 0; sp < p.S; ++sp) {
+                float4 v[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int task = base + u * kGemmThreads;
+                    v[u] = task < ntask ? __ldcg(t0 + sp * sstride + (long long)(q_lo * kGemmBM + task))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    acc[u].x += v[u].x; acc[u].y += v[u].y; acc[u].z += v[u].z; acc[u].w += v[u].w;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int task = base + u * kGemmThreads;
+                if (task >= ntask) break;
+                const int q = q_lo + task / kGemmBM, et = task % kGemmBM;
+                const int row = mt * kGemmBM + et;
+                if (row >= p.N) continue;
+                const float vals[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int j = 4 * q + c;
+                    if (j < b_lim) {
+                        const long long o = (long long)(bt * BN + j) * p.ldy + row;
+                        if (p.y_f32) reinterpret_cast<float*>(p.Y)[o] = vals[c];
+                        else reinterpret_cast<uint16_t*>(p.Y)[o] = f32_to_bf16_rn(vals[c]);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && atom_add_acq_rel(p.tickets + tile, 1) == 2 * p.S - 1)
+            p.tickets[tile] = 0;  // the last split through resets the ticket (2 S arrivals)
+    }
     if (warp == kWarpMma) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem_base);
