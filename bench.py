@@ -733,9 +733,8 @@ def main():
         c2 = sweep_leg(torch, stack, clocks, peak, (1, 2, 4, 8, 16), [("r%d" % b, b) for b in LADDER])
 
     # C3: heterogeneous per-layer bit-widths (EvoPress-style budget-exact 3.5-bit
-    # config over the unfused linears, the reference's own moves), CUDA graph of
-    # the unfused stack: one launch per linear, each at its own r (faster here
-    # than the per-layer-dispatch K3S kernel, scripts/stack_matrix.py)
+    # config over the unfused linears, the reference's own moves): the default
+    # dispatch -- the per-layer-r K3S kernel at B <= 4, else the per-layer graph
     hetero = None
     if not args.no_hetero and args.model == "Llama-3.1-8B":
         from paper_2602_03537_b200.config import budget_config, level_histogram

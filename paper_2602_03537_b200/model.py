@@ -180,9 +180,7 @@ class LinearStack:
         """Where the persistent K3S path is the default (single GPU, B <= 16,
         G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix*.txt):
         * uniform r: see the table in the body (profiles/r2_dispatch_matrix.txt);
-        * heterogeneous (per-layer r, parents): fused stacks at B <= 4 (1.10x at
-          B = 1).  Unfused ones (224 linears, the k/v ones only 1024 rows)
-          measure at par at B = 1 and the graph wins at larger B.
+        * heterogeneous (per-layer r, parents): at B <= 4, fused or unfused.
         stack_kernel=True / False forces either path."""
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
@@ -194,7 +192,9 @@ class LinearStack:
             ok = (self.B <= 2 or (self.B <= 4 and r0 != 8) or (self.B <= 8 and r0 in (2, 3, 6))
                   or r0 == 2)
         else:
-            ok = self.fused and parents and self.B <= 4
+            # per-layer r (the dispatch kernel): 1.61 vs 1.96 ms fused, 1.99 vs 2.17 ms for the
+            # 224 unfused linears of C3 at B = 1 (scripts/stack_matrix.py)
+            ok = parents and self.B <= 4
         return ok and self.B <= 16 and self.G == 128  # tp > 1: one K3S launch per all-reduce segment
 
     def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None, graph: bool = True) -> None:
