@@ -265,6 +265,16 @@ MQ_API int mq_qknorm_rope_kv(const void* qkv, const void* cosv, const void* sinv
                              void* vcache, int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos,
                              const float* q_norm, const float* k_norm, float eps, void* stream);
 MQ_API int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream);
+/* mq_attn_decode: single-query decode attention for the decoder harness, with the
+ *   (optional q/k RMSNorm +) rotary step and the KV-cache write fused in: grid (n_heads, B);
+ *   q head h attends over cache rows [0, pos) of kv head kv_of_q[h] plus its new k / v
+ *   (written at pos by the first q head of each kv head); fp32 softmax (1/sqrt(head_dim));
+ *   att (B, n_heads * head_dim) bf16.  head_dim 64 or 128, pos < 51200 (the scores live in
+ *   shared memory). */
+MQ_API int mq_attn_decode(const void* qkv, const void* cosv, const void* sinv, const float* q_norm,
+                          const float* k_norm, float eps, void* kcache, void* vcache, const int* kv_of_q,
+                          void* att, int B, int n_heads, int n_kv_heads, int head_dim, int T, int pos,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -75,6 +75,7 @@ _SIGS = {
     "mq_rope_kv": ([_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp], _i),
     "mq_qknorm_rope_kv": ([_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _f, _vp], _i),
     "mq_silu_mul": ([_vp, _vp, _i, _i, _vp], _i),
+    "mq_attn_decode": ([_vp, _vp, _vp, _vp, _vp, _f, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp], _i),
     "mq_gptq_block": ([_vp, _ll, _i, _i, _i, _i, _vp, _i, _i, _vp, _ll, _vp, _vp, _i, _vp, _ll, _vp, _ll, _vp,
                        _ll, _vp], _i),
 }

@@ -1023,6 +1023,19 @@ int mq_qknorm_rope_kv(const void* qkv, const void* cosv, const void* sinv, void*
                        "mq_qknorm_rope_kv");
 }
 
+int mq_attn_decode(const void* qkv, const void* cosv, const void* sinv, const float* q_norm, const float* k_norm,
+                   float eps, void* kcache, void* vcache, const int* kv_of_q, void* att, int B, int n_heads,
+                   int n_kv_heads, int head_dim, int T, int pos, void* stream) {
+    if (!qkv || !cosv || !sinv || !kcache || !vcache || !kv_of_q || !att) return fail(MQ_ERR_INVALID, "null pointer");
+    if (B < 1 || n_heads < 1 || n_kv_heads < 1 || (head_dim != 64 && head_dim != 128) || pos < 0 || pos >= T ||
+        pos >= 50 * 1024)
+        return fail(MQ_ERR_INVALID, "bad shape (head_dim 64 / 128, 0 <= pos < min(T, 51200))");
+    if ((q_norm == nullptr) != (k_norm == nullptr)) return fail(MQ_ERR_INVALID, "q_norm and k_norm go together");
+    return cuda_status(mq::launch_attn_decode(qkv, cosv, sinv, q_norm, k_norm, eps, kcache, vcache, kv_of_q, att, B,
+                                              n_heads, n_kv_heads, head_dim, T, pos, (cudaStream_t)stream),
+                       "mq_attn_decode");
+}
+
 int mq_silu_mul(const void* gu, void* y, int B, int inter, void* stream) {
     if (!gu || !y) return fail(MQ_ERR_INVALID, "null pointer");
     if (B < 1 || inter < 1) return fail(MQ_ERR_INVALID, "bad shape");

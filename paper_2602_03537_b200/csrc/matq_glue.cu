@@ -143,6 +143,156 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const __nv_bflo
     }
 }
 
+// Single-query decode attention with the rotary step fused in: one CTA per (q head,
+// batch row), 256 threads.  The q head and its kv head's new k are RMS-normed (Qwen3,
+// optional) and rotated exactly as k_rope_kv does (bf16 per op); the first q head of each
+// kv head writes the new k / v into the caches at pos; every CTA scores its q against
+// cache rows [0, pos) plus the new k (kept in shared memory: no cross-CTA ordering), with an
+// fp32 softmax (scale 1/sqrt(hd)) and an fp32 weighted sum of V -> bf16 att row.  The work
+// of torch SDPA (GQA) + k_rope_kv in one launch per layer.  Latency-shaped: a thread owns
+// whole keys in the score pass (hd / 8 16-byte loads in flight), and in the V pass a
+// (key slice, 8-dim group) with eight keys in flight; slices are summed in shared memory.
+constexpr int kAttnThreads = 256;
+
+template <int HD>
+__global__ void __launch_bounds__(kAttnThreads)
+k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __restrict__ cosv,
+              const __nv_bfloat16* __restrict__ sinv, const float* __restrict__ qn, const float* __restrict__ kn,
+              float eps, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+              const int* __restrict__ kv_of_q, __nv_bfloat16* __restrict__ att, int nh, int nkv, int T, int pos) {
+    constexpr int HALF = HD / 2, DG = HD / 8, KS = kAttnThreads / DG;
+    __shared__ __align__(16) float qs[HD];
+    __shared__ float kns[HD], vns[HD];
+    __shared__ float red[32];
+    __shared__ __align__(16) float part[KS][HD + 4];
+    extern __shared__ float sc[];  // pos + 1 scores
+    glue_pdl_wait();
+    glue_pdl_launch();
+    const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+    const int j = kv_of_q[h];
+    const __nv_bfloat16* row = qkv + (long long)b * (nh + 2 * nkv) * HD;
+    // q head h and k head j: optional RMSNorm, then rotate (k_rope_kv's arithmetic)
+    for (int which = 0; which < 2; ++which) {
+        const __nv_bfloat16* src = row + (which == 0 ? h : nh + j) * HD;
+        const float* nw = which == 0 ? qn : kn;
+        float x = tid < HD ? bf(src[tid]) : 0.0f;
+        if (nw) {
+            const float inv = rsqrtf(block_sum(x * x, red) / (float)HD + eps);
+            x = bf(__float2bfloat16_rn(x * inv * (tid < HD ? nw[tid] : 0.0f)));
+        }
+        float* dst = which == 0 ? qs : kns;
+        if (tid < HD) dst[tid] = x;
+        __syncthreads();
+        float o = 0.0f;
+        if (tid < HD) {
+            const int jj = tid < HALF ? tid : tid - HALF;
+            const float c = bf(cosv[jj]), s = bf(sinv[jj]);
+            const float x1 = dst[jj], x2 = dst[jj + HALF];
+            o = tid < HALF ? bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(x1 * c)) - bf(__float2bfloat16_rn(x2 * s))))
+                           : bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(x2 * c)) + bf(__float2bfloat16_rn(x1 * s))));
+        }
+        __syncthreads();
+        if (tid < HD) dst[tid] = o;
+    }
+    if (tid < HD) vns[tid] = bf(row[(nh + nkv + j) * HD + tid]);
+    __syncthreads();
+    // the first q head of kv head j publishes the new k / v into the caches
+    const bool writer = h == 0 || kv_of_q[h - 1] != j;
+    __nv_bfloat16* kr = kc + ((long long)b * nkv + j) * T * HD;
+    __nv_bfloat16* vr = vc + ((long long)b * nkv + j) * T * HD;
+    if (writer && tid < HD) {
+        kr[(long long)pos * HD + tid] = __float2bfloat16_rn(kns[tid]);
+        vr[(long long)pos * HD + tid] = __float2bfloat16_rn(vns[tid]);
+    }
+    // scores: thread t owns keys t, t + 256, ...; the new key (index pos) from shared memory
+    const float scale = rsqrtf((float)HD);
+    float mx = -INFINITY;
+    for (int t = tid; t <= pos; t += kAttnThreads) {
+        float d = 0.0f;
+        if (t < pos) {
+            const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)t * HD);
+            uint4 u[DG];
+#pragma unroll
+            for (int i = 0; i < DG; ++i) u[i] = __ldg(kp + i);
+#pragma unroll
+            for (int i = 0; i < DG; ++i) {
+                const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * i);
+                const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * i + 4);
+                const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+                float2 f;
+                f = __bfloat1622float2(e[0]); d = fmaf(qa.x, f.x, d); d = fmaf(qa.y, f.y, d);
+                f = __bfloat1622float2(e[1]); d = fmaf(qa.z, f.x, d); d = fmaf(qa.w, f.y, d);
+                f = __bfloat1622float2(e[2]); d = fmaf(qb.x, f.x, d); d = fmaf(qb.y, f.y, d);
+                f = __bfloat1622float2(e[3]); d = fmaf(qb.z, f.x, d); d = fmaf(qb.w, f.y, d);
+            }
+        } else {
+#pragma unroll 8
+            for (int i = 0; i < HD; ++i) d = fmaf(qs[i], kns[i], d);
+        }
+        d *= scale;
+        sc[t] = d;
+        mx = fmaxf(mx, d);
+    }
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+#pragma unroll
+    for (int w = 1; w < kAttnThreads / 32; ++w) mx = fmaxf(mx, red[w]);
+    __syncthreads();
+    float sum = 0.0f;
+    for (int t = tid; t <= pos; t += kAttnThreads) {
+        const float e = __expf(sc[t] - mx);
+        sc[t] = e;
+        sum += e;
+    }
+    sum = block_sum(sum, red);  // ends with a barrier: every sc[] is visible
+    // V pass: thread (slice ks, dims 8 dg .. 8 dg + 7) sums keys ks, ks + KS, ...
+    const int dg = tid % DG, ks = tid / DG;
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+    const uint4* vp = reinterpret_cast<const uint4*>(vr) + dg;
+    int t = ks;
+    for (; t + 7 * KS < pos; t += 8 * KS) {
+        uint4 u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u[i] = __ldg(vp + (long long)(t + i * KS) * DG);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float p = sc[t + i * KS];
+            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = __bfloat1622float2(e[k]);
+                acc[2 * k] = fmaf(p, f.x, acc[2 * k]);
+                acc[2 * k + 1] = fmaf(p, f.y, acc[2 * k + 1]);
+            }
+        }
+    }
+    for (; t < pos; t += KS) {
+        const uint4 u = __ldg(vp + (long long)t * DG);
+        const float p = sc[t];
+        const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(e[k]);
+            acc[2 * k] = fmaf(p, f.x, acc[2 * k]);
+            acc[2 * k + 1] = fmaf(p, f.y, acc[2 * k + 1]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[ks][8 * dg + k] = acc[k];
+    __syncthreads();
+    if (tid < HD) {
+        float o = sc[pos] * vns[tid];
+#pragma unroll 8
+        for (int i = 0; i < KS; ++i) o += part[i][tid];
+        att[((long long)b * nh + h) * HD + tid] = __float2bfloat16_rn(o / sum);
+    }
+}
+
 // grid (rows, ceil(inter / (8 * 256))): 8 consecutive columns per thread (16-byte loads)
 __global__ void k_silu_mul(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ y, int inter) {
     glue_pdl_wait();
@@ -170,10 +320,12 @@ __global__ void k_silu_mul(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* 
 // programmatic dependent launch: the kernel's prologue overlaps the previous
 // kernel's tail; it waits (griddepcontrol.wait) before touching its inputs
 template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+static cudaError_t launch_pdl_smem(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                   Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -181,6 +333,11 @@ static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cud
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+    return launch_pdl_smem(kern, grid, block, 0, s, args...);
 }
 
 cudaError_t launch_add_rmsnorm(void* x, const void* delta, const float* w, void* y, int B, int h, float eps,
@@ -200,6 +357,26 @@ cudaError_t launch_rope_kv(const void* qkv, const void* cosv, const void* sinv, 
                       reinterpret_cast<const __nv_bfloat16*>(cosv), reinterpret_cast<const __nv_bfloat16*>(sinv),
                       reinterpret_cast<__nv_bfloat16*>(q), reinterpret_cast<__nv_bfloat16*>(kc),
                       reinterpret_cast<__nv_bfloat16*>(vc), nh, nkv, hd, T, pos, qn, kn, eps);
+}
+
+cudaError_t launch_attn_decode(const void* qkv, const void* cosv, const void* sinv, const float* qn, const float* kn,
+                               float eps, void* kc, void* vc, const int* kv_of_q, void* att, int B, int nh, int nkv,
+                               int hd, int T, int pos, cudaStream_t s) {
+    const size_t smem = sizeof(float) * (pos + 1);
+    if (pos < 0 || pos >= T || smem > 200 * 1024) return cudaErrorInvalidValue;
+    auto args = [&](auto kern) {
+        if (smem > 48 * 1024) {
+            const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        return launch_pdl_smem(kern, dim3(nh, B), dim3(kAttnThreads), smem, s, reinterpret_cast<const __nv_bfloat16*>(qkv),
+                          reinterpret_cast<const __nv_bfloat16*>(cosv), reinterpret_cast<const __nv_bfloat16*>(sinv),
+                          qn, kn, eps, reinterpret_cast<__nv_bfloat16*>(kc), reinterpret_cast<__nv_bfloat16*>(vc),
+                          kv_of_q, reinterpret_cast<__nv_bfloat16*>(att), nh, nkv, T, pos);
+    };
+    if (hd == 128) return args(k_attn_decode<128>);
+    if (hd == 64) return args(k_attn_decode<64>);
+    return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_silu_mul(const void* gu, void* y, int B, int inter, cudaStream_t s) {

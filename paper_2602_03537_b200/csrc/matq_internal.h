@@ -60,6 +60,9 @@ cudaError_t launch_add_rmsnorm(void* x, const void* delta, const float* w, void*
 cudaError_t launch_rope_kv(const void* qkv, const void* cosv, const void* sinv, void* q, void* kc, void* vc, int B,
                            int nh, int nkv, int hd, int T, int pos, const float* qn, const float* kn, float eps,
                            cudaStream_t s);
+cudaError_t launch_attn_decode(const void* qkv, const void* cosv, const void* sinv, const float* qn, const float* kn,
+                               float eps, void* kc, void* vc, const int* kv_of_q, void* att, int B, int nh, int nkv,
+                               int hd, int T, int pos, cudaStream_t s);
 cudaError_t launch_silu_mul(const void* gu, void* y, int B, int inter, cudaStream_t s);
 
 struct GemmConfig {

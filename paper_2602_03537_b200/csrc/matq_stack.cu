@@ -1,6 +1,7 @@
 // matq_stack.cu -- K3S instantiations and cooperative launcher.
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 
 #include "matq_stack.cuh"
@@ -37,6 +38,20 @@ bool stack_nocoop() {
     return v != 0;
 }
 
+// Programmatic dependent launch (the producer prefetches weights under the previous
+// kernel's tail).  On by default; MQ_STACK_PDL=0 turns it off, and a driver that rejects
+// it together with the cooperative / cluster attributes turns it off for the process.
+std::atomic<int> g_stack_pdl{-1};
+bool stack_pdl() {
+    int v = g_stack_pdl.load();
+    if (v < 0) {
+        const char* e = getenv("MQ_STACK_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_stack_pdl.store(v);
+    }
+    return v != 0;
+}
+
 template <int NT, int R, bool CHILD, bool XOPS = false>
 cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaStream_t stream) {
     auto kern = k_stack<NT, R, CHILD, XOPS>;
@@ -47,7 +62,7 @@ cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaSt
     cfg.blockDim = dim3(kStackThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     int n = 0;
     if (!(p.cluster && stack_nocoop())) {
         attr[n].id = cudaLaunchAttributeCooperative;
@@ -61,12 +76,24 @@ cudaError_t launch_one_stack(const StackParams& p, int grid, size_t smem, cudaSt
         attr[n].val.clusterDim.z = 1;
         ++n;
     }
+    const bool pdl = stack_pdl();
+    if (pdl) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = n;
     e = cudaLaunchKernelEx(&cfg, kern, p);
+    if (pdl && (e == cudaErrorInvalidValue || e == cudaErrorNotSupported)) {
+        (void)cudaGetLastError();
+        g_stack_pdl.store(0);
+        cfg.numAttrs = n - 1;
+        e = cudaLaunchKernelEx(&cfg, kern, p);
+    }
     if (getenv("MQ_STACK_LAUNCH_DEBUG"))
-        fprintf(stderr, "k_stack launch cluster=%d coop=%d grid=%d smem=%zu -> %s\n", p.cluster,
-                !(p.cluster && stack_nocoop()), grid, smem, cudaGetErrorString(e));
+        fprintf(stderr, "k_stack launch cluster=%d coop=%d pdl=%d grid=%d smem=%zu -> %s\n", p.cluster,
+                !(p.cluster && stack_nocoop()), (int)stack_pdl(), grid, smem, cudaGetErrorString(e));
     return e;
 }
 

@@ -415,12 +415,21 @@ __device__ __forceinline__ void load_x16(const StackParams& p, const StackLayer&
     }
 }
 
+// bf16x2 silu(g) * u, rounded like torch (silu to bf16, then the product to bf16)
+__device__ __forceinline__ uint32_t silu_mul_bf16x2(uint32_t g, uint32_t u) {
+    const float g0 = __uint_as_float(g << 16), g1 = __uint_as_float(g & 0xFFFF0000u);
+    const float s0 = bf16_to_f32(f32_to_bf16_rn(__fdividef(g0, 1.0f + __expf(-g0))));
+    const float s1 = bf16_to_f32(f32_to_bf16_rn(__fdividef(g1, 1.0f + __expf(-g1))));
+    return (uint32_t)f32_to_bf16_rn(s0 * __uint_as_float(u << 16)) |
+           ((uint32_t)f32_to_bf16_rn(s1 * __uint_as_float(u & 0xFFFF0000u)) << 16);
+}
+
 // Add + RMSNorm prologue, pass 1 (consumer threads; the layer is one K chunk):
 // R <- bf16(R + X) into the kept residual (R from res_in, or the residual the
 // previous add-norm layer kept), and per (row, 128-column group) sums of R^2 --
 // summed in group order by the staging pass (deterministic).
 __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, const StackLayer& L, uint32_t tag,
-                                                      uint8_t* smem_base) {
+                                                      uint8_t* smem_base, int l) {
     constexpr int kOctets = kConsumerThreads / 8;
     const int ol = threadIdx.x & 7;
     const int ngroups = L.K >> 7;
@@ -435,7 +444,10 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
         float ss = 0.0f;
         if (active) {
             uint32_t d[8], r[8];
-            load_x16(p, L, b, col, true, tag, d);
+            // everything that does not wait on the producing layer is issued before the
+            // LL polling (its loads are ordered after it): the residual, and the RMSNorm
+            // weights the staging pass reads (into L1)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(L.norm_w + col));
             if (L.res_in) {
                 const uint16_t* src = L.res_in + (long long)b * L.ldres + col;
                 const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src)), c = __ldcg(reinterpret_cast<const uint4*>(src + 8));
@@ -445,6 +457,8 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
                 const uint4 c = *reinterpret_cast<const uint4*>(res + b * p.res_k + col + 8);
                 r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = c.x; r[5] = c.y; r[6] = c.z; r[7] = c.w;
             }
+            load_x16(p, L, b, col, true, tag, d);
+            MQ_STS_WMAX(l + 128, 0);  // delta arrived (timing builds)
             uint32_t o[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -463,6 +477,7 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
         ss += __shfl_xor_sync(0xffffffffu, ss, 1);
         if (active && ol == 0) part[b * (p.res_k >> 7) + grp] = ss;
     }
+    MQ_STS_WMAX(l + 128, 1);
 }
 
 // Stage X[:, chunk] into shared memory (consumer threads).  An octet of lanes
@@ -476,7 +491,7 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
 //   else a plain copy.
 template <int R, int NT, bool F16, bool ZP, int NCOPY, bool XOPS>
 __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLayer& L, uint16_t* xs, float* zc,
-                                            int col_base, int Kc, uint32_t tag, const uint8_t* smem_base) {
+                                            int col_base, int Kc, uint32_t tag, const uint8_t* smem_base, int l) {
     constexpr int kOctets = kConsumerThreads / 8;
     const int ol = threadIdx.x & 7;
     const int ngroups = Kc >> 7;
@@ -500,9 +515,22 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
             if (lo_ok) {
                 const uint16_t* rr = reinterpret_cast<const uint16_t*>(smem_base + p.res_off) + b * p.res_k + col;
                 const float* part = reinterpret_cast<const float*>(smem_base + p.rpart_off) + b * (p.res_k >> 7);
+                // fixed order (deterministic, the same in every thread); K % 512 == 0 takes
+                // float4 loads (part is 16-byte aligned per row when res_k % 512 == 0)
                 float ss = 0.0f;
-                for (int gi = 0; gi < (L.K >> 7); ++gi) ss += part[gi];  // fixed order: deterministic
+                const int ng = L.K >> 7;
+                if ((ng & 3) == 0 && ((p.res_k >> 7) & 3) == 0) {
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int gi = 0; gi < ng; gi += 4) {
+                        const float4 v = *reinterpret_cast<const float4*>(part + gi);
+                        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+                    }
+                    ss = (acc.x + acc.y) + (acc.z + acc.w);
+                } else {
+                    for (int gi = 0; gi < ng; ++gi) ss += part[gi];
+                }
                 const float inv = rsqrtf(ss / (float)L.K + L.eps);
+                MQ_STS_WMAX(l + 128, 3);
                 const uint4 r0 = *reinterpret_cast<const uint4*>(rr), r1 = *reinterpret_cast<const uint4*>(rr + 8);
                 const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
 #pragma unroll
@@ -511,6 +539,43 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
                     const float c = __uint_as_float(rw[i] & 0xFFFF0000u) * inv * __ldg(L.norm_w + col + 2 * i + 1);
                     w[i] = (uint32_t)f32_to_bf16_rn(a) | ((uint32_t)f32_to_bf16_rn(c) << 16);
                 }
+                MQ_STS_WMAX(l + 128, 4);
+            }
+        } else if (XOPS && L.xop == 2 && L.xll >= 0) {
+            // SiLU gating from LL words: g (columns col..) and u (K columns further) in one poll
+            uint32_t u[8];
+            if (lo_ok) {
+                const unsigned long long* sg = p.ll + L.xll + (long long)b * L.ldxll + (col >> 1);
+                const unsigned long long* su = sg + (L.K >> 1);
+                unsigned long long v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = (unsigned long long)tag << 32;
+                for (;;) {
+                    ld_ll2(sg, v[0], v[1]);
+                    ld_ll2(sg + 2, v[2], v[3]);
+                    ld_ll2(su, v[8], v[9]);
+                    ld_ll2(su + 2, v[10], v[11]);
+                    if (hi_ok) {
+                        ld_ll2(sg + 4, v[4], v[5]);
+                        ld_ll2(sg + 6, v[6], v[7]);
+                        ld_ll2(su + 4, v[12], v[13]);
+                        ld_ll2(su + 6, v[14], v[15]);
+                    }
+                    bool ok = true;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) ok = ok && (uint32_t)(v[i] >> 32) == tag;
+                    if (ok) break;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    w[i] = (uint32_t)v[i];
+                    u[i] = (uint32_t)v[8 + i];
+                }
+#pragma unroll
+                MQ_STS_WMAX(l + 128, 4);  // g and u arrived
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = silu_mul_bf16x2(w[i], u[i]);
+                MQ_STS_WMAX(l + 128, 5);
             }
         } else if (L.xll >= 0) {
             const unsigned long long* src = p.ll + L.xll + (long long)b * L.ldxll + (col >> 1);
@@ -536,6 +601,7 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
             }
 #pragma unroll
             for (int i = 0; i < 8; ++i) w[i] = (uint32_t)v[i];
+            MQ_STS_WMAX(l + 128, 4);  // X arrived
         } else {
             const uint16_t* src = L.X + (long long)b * L.ldx + col;
             if (lo_ok) {
@@ -547,17 +613,11 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
                 w[4] = a.x; w[5] = a.y; w[6] = a.z; w[7] = a.w;
             }
         }
-        if (XOPS && L.xop == 2 && lo_ok) {  // SiLU gating: u sits K columns after g in the same rows
+        if (XOPS && L.xop == 2 && L.xll < 0 && lo_ok) {  // SiLU gating, X from outside the step
             uint32_t u[8];
             load_x16(p, L, b, col + L.K, hi_ok, tag, u);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float g0 = __uint_as_float(w[i] << 16), g1 = __uint_as_float(w[i] & 0xFFFF0000u);
-                const float s0 = bf16_to_f32(f32_to_bf16_rn(g0 / (1.0f + __expf(-g0))));  // torch: silu in bf16
-                const float s1 = bf16_to_f32(f32_to_bf16_rn(g1 / (1.0f + __expf(-g1))));
-                w[i] = (uint32_t)f32_to_bf16_rn(s0 * __uint_as_float(u[i] << 16)) |
-                       ((uint32_t)f32_to_bf16_rn(s1 * __uint_as_float(u[i] & 0xFFFF0000u)) << 16);
-            }
+            for (int i = 0; i < 8; ++i) w[i] = silu_mul_bf16x2(w[i], u[i]);
         }
         __syncwarp();
         uint16_t* dst = xs + b * p.xs_stride + c0;
@@ -696,10 +756,11 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // consumer_sync that ends every layer)
     MQ_STS(l, 0);
     if (XOPS && L.xop == 1) {  // add + RMSNorm: the residual update and the row sums first
-        stack_addnorm_prepass(p, L, sh.tag, smem);
+        stack_addnorm_prepass(p, L, sh.tag, smem, l);
         consumer_sync();
+        MQ_STS(l + 128, 2);
     }
-    stack_stage<R, NT, F16, ZP, NCOPY, XOPS>(p, L, xs, zc, col_base, Kc, sh.tag, smem);
+    stack_stage<R, NT, F16, ZP, NCOPY, XOPS>(p, L, xs, zc, col_base, Kc, sh.tag, smem, l);
     MQ_STS_WMAX(l, 1);  // this warp's staging tasks done (max over warps)
     if (threadIdx.x == kSyncThread && L.war_wait >= 0 && L.war_wait < l) {
         // this layer overwrites a buffer an earlier layer read from outside the
@@ -1152,6 +1213,9 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
         if (p.cluster) cluster_sync_all();  // see the end of the consumer path
         return;
     }
+    // programmatic dependent launch: the producer warp streams the (static) weights while
+    // the previous kernel drains; consumers touch activations / outputs only after it is done
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const unsigned long long target = (sh.gen + 1ull) * gridDim.x;
     int cstage = 0;
     uint32_t parity = 0;

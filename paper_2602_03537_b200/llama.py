@@ -80,6 +80,7 @@ class LlamaDecoder:
         grp = shape.n_heads // shape.n_kv_heads
         # local kv head of each local q head (GQA; replicated kv heads when tp does not divide them)
         self.kv_of_q = torch.tensor([(q0 + i) // grp - k0 for i in range(self.nh)], device=dev)
+        self.kv_of_q32 = self.kv_of_q.to(torch.int32)
         self.uniform_gqa = self.nh % max(1, self.nkv) == 0 and all(
             (q0 + i) // grp - k0 == i // (self.nh // self.nkv) for i in range(self.nh))
         self.blocks = []
@@ -155,6 +156,18 @@ class LlamaDecoder:
         return F.scaled_dot_product_attention(q, kc.index_select(1, self.kv_of_q),
                                               vc.index_select(1, self.kv_of_q))
 
+    def _attn_decode(self, blk, st) -> None:
+        """(q/k RMSNorm +) rotary step, KV-cache write at position T and single-query
+        attention for every q head in one kernel (mq_attn_decode) -> buf['att']."""
+        from . import _lib
+
+        s, b = self.shape, self.buf
+        qn = _lib.ptr(blk["qn"]) if s.qk_norm else None
+        kn = _lib.ptr(blk["kn"]) if s.qk_norm else None
+        _lib.call("mq_attn_decode", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin), qn, kn, 1e-6,
+                  _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), _lib.ptr(self.kv_of_q32), _lib.ptr(b["att"]),
+                  self.B, self.nh, self.nkv, s.head_dim, self.T + 1, self.T, st)
+
     def set_bits(self, bits) -> None:
         """Uniform int, or {name: r} over the fused linears' names."""
         for i, blk in enumerate(self.blocks):
@@ -211,7 +224,7 @@ class LlamaDecoder:
     def _forward_k3s(self, parts=("linear", "attn", "glue", "comm", "head")) -> None:
         """One decode step with one K3S launch per block (o, gate_up, down and the
         next block's qkv; the residual / RMSNorm / SiLU glue fused into staging):
-        per block K3S + rotary/KV + SDPA."""
+        per block K3S + one attention kernel (rotary, KV write, single-query attention)."""
         from . import _lib
 
         if self.segments is None:
@@ -232,12 +245,7 @@ class LlamaDecoder:
             blk0["qkv"].planes.linear(b["hn"], blk0["qkv"].bits, out=b["qkv"], pdl=True)
         for i, blk in enumerate(self.blocks):
             if attn:
-                qn = _lib.ptr(blk["qn"]) if s.qk_norm else None
-                kn = _lib.ptr(blk["kn"]) if s.qk_norm else None
-                _lib.call("mq_qknorm_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin),
-                          _lib.ptr(b["q"]), _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T,
-                          qn, kn, 1e-6, st)
-                b["att"].copy_(self._attend(b["q"], blk["kc"], blk["vc"]).reshape(B, nh * hd))
+                self._attn_decode(blk, st)
             if lin:
                 self.segments[i].run(torch.cuda.current_stream())
         if glue:
@@ -249,8 +257,8 @@ class LlamaDecoder:
     PARTS = ("linear", "attn", "glue", "comm", "head")
 
     def _forward_fused(self, parts=PARTS) -> None:
-        """One decode step: 4 sliced linears (PDL-chained K3) + 3 fused glue
-        kernels (norm, rotary/KV, gating) + SDPA per block (+ 2 all-reduces
+        """One decode step: 4 sliced linears (PDL-chained K3) + 2 glue kernels
+        (norm, gating) + one attention kernel (rotary, KV write, attention) per block (+ 2 all-reduces
         under tensor parallelism).  ``parts`` keeps only some component
         classes (component_ms times each alone on the same buffers)."""
         from . import _lib
@@ -271,16 +279,9 @@ class LlamaDecoder:
             if lin:
                 blk["qkv"].planes.linear(b["hn"], blk["qkv"].bits, out=b["qkv"], pdl=True)
             if attn:
-                qn = _lib.ptr(blk["qn"]) if s.qk_norm else None
-                kn = _lib.ptr(blk["kn"]) if s.qk_norm else None
-                _lib.call("mq_qknorm_rope_kv", _lib.ptr(b["qkv"]), _lib.ptr(self.cos), _lib.ptr(self.sin),
-                          _lib.ptr(b["q"]), _lib.ptr(blk["kc"]), _lib.ptr(blk["vc"]), B, nh, nkv, hd, T + 1, T,
-                          qn, kn, 1e-6, st)
-                att = self._attend(b["q"], blk["kc"], blk["vc"])
-            else:
-                att = b["q"]
+                self._attn_decode(blk, st)
             if lin:
-                blk["o"].planes.linear(att.reshape(B, nh * hd), blk["o"].bits, out=b["o"], pdl=True)
+                blk["o"].planes.linear(b["att"], blk["o"].bits, out=b["o"], pdl=True)
             if comm:
                 self._all_reduce(b["o"])
             if glue:

@@ -175,3 +175,63 @@ def test_decoder_k3s_segments_match_per_layer_path(llama, B):
             torch.cuda.synchronize()
             assert torch.equal(dec.logits.float(), outs[lin])
     assert rel_err(outs["k3s"].cpu().numpy(), outs["k3"].cpu().numpy()) <= 2e-2
+
+
+@pytest.mark.parametrize("hd", [64, 128])
+@pytest.mark.parametrize("qk_norm", [False, True], ids=["plain", "qknorm"])
+@pytest.mark.parametrize("heads", [(8, 2, None), (6, 3, [0, 0, 1, 1, 1, 2])], ids=["gqa", "ragged-map"])
+@pytest.mark.parametrize("B,T", [(1, 1), (3, 17), (2, 300), (1, 20001)])
+def test_attn_decode_kernel_vs_torch(llama, hd, qk_norm, heads, B, T):
+    """mq_attn_decode (rotary + optional q/k RMSNorm + KV write + single-query
+    attention, one launch) against the torch glue (_rms_norm, _rope in bf16) and an
+    fp32 softmax-attention; T = 20001 takes the > 48 KB dynamic shared-memory path."""
+    from paper_2602_03537_b200 import _lib
+
+    nh, nkv, kmap = heads
+    kmap = kmap or [i // (nh // nkv) for i in range(nh)]
+    pos = T - 1
+    g = torch.Generator(device="cuda").manual_seed(hd + T + nh)
+    qkv = torch.randn(B, (nh + 2 * nkv) * hd, device="cuda", generator=g).to(torch.bfloat16)
+    kc = torch.randn(B, nkv, T, hd, device="cuda", generator=g).to(torch.bfloat16)
+    vc = torch.randn(B, nkv, T, hd, device="cuda", generator=g).to(torch.bfloat16)
+    kc0, vc0 = kc.clone(), vc.clone()
+    ang = 37.0 / (10000.0 ** (torch.arange(0, hd, 2, device="cuda", dtype=torch.float32) / hd))
+    cos, sin = ang.cos().to(torch.bfloat16), ang.sin().to(torch.bfloat16)
+    qn = (1.0 + 0.1 * torch.randn(hd, device="cuda", generator=g)) if qk_norm else None
+    kn = (1.0 + 0.1 * torch.randn(hd, device="cuda", generator=g)) if qk_norm else None
+    kv_of_q = torch.tensor(kmap, device="cuda", dtype=torch.int32)
+    att = torch.full((B, nh * hd), float("nan"), device="cuda", dtype=torch.bfloat16)
+    _lib.call("mq_attn_decode", _lib.ptr(qkv), _lib.ptr(cos), _lib.ptr(sin),
+              _lib.ptr(qn) if qk_norm else None, _lib.ptr(kn) if qk_norm else None, 1e-6,
+              _lib.ptr(kc), _lib.ptr(vc), _lib.ptr(kv_of_q), _lib.ptr(att), B, nh, nkv, hd, T, pos,
+              _lib.stream_ptr(None))
+    torch.cuda.synchronize()
+    q = qkv[:, : nh * hd].view(B, nh, hd)
+    k = qkv[:, nh * hd:(nh + nkv) * hd].view(B, nkv, hd)
+    v = qkv[:, (nh + nkv) * hd:].view(B, nkv, hd)
+    if qk_norm:
+        q, k = llama._rms_norm(q, qn, 1e-6), llama._rms_norm(k, kn, 1e-6)
+    q, k = llama._rope(q, cos, sin), llama._rope(k, cos, sin)
+    # the new k / v land at pos (rounding of the fused norm may differ by one bf16 ulp)
+    assert torch.equal(vc[:, :, pos], v)
+    torch.testing.assert_close(kc[:, :, pos].float(), k.float(), rtol=1e-2, atol=1e-2)
+    assert torch.equal(kc[:, :, :pos], kc0[:, :, :pos]) and torch.equal(vc[:, :, :pos], vc0[:, :, :pos])
+    idx = kv_of_q.long()
+    kk = torch.cat((kc0[:, :, :pos].float(), k.float().unsqueeze(2)), dim=2).index_select(1, idx)
+    vv = torch.cat((vc0[:, :, :pos].float(), v.float().unsqueeze(2)), dim=2).index_select(1, idx)
+    p = torch.softmax((q.float().unsqueeze(2) @ kk.transpose(-1, -2)) / math.sqrt(hd), dim=-1)
+    want = (p @ vv).reshape(B, nh * hd)
+    got = att.float()
+    assert torch.isfinite(got).all()
+    assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 1e-2
+
+
+def test_attn_decode_rejects_bad_shapes(llama):
+    from paper_2602_03537_b200 import _lib
+
+    x = torch.zeros(64, device="cuda", dtype=torch.bfloat16)
+    m = torch.zeros(2, device="cuda", dtype=torch.int32)
+    for hd, T, pos in ((96, 4, 3), (64, 4, 4), (64, 4, -1)):
+        with pytest.raises(Exception):
+            _lib.call("mq_attn_decode", _lib.ptr(x), _lib.ptr(x), _lib.ptr(x), None, None, 1e-6, _lib.ptr(x),
+                      _lib.ptr(x), _lib.ptr(m), _lib.ptr(x), 1, 2, 1, hd, T, pos, _lib.stream_ptr(None))
