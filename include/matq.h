@@ -162,7 +162,7 @@ typedef struct mq_stack_layer {
     int xop;
     const void* res_in;   /* bf16 (B, K), row stride ldres */
     void* res_out;        /* bf16 (B, K), row stride ldres */
-    const float* norm_w;  /* fp32 (K) */
+    const float* norm_w;  /* fp32 (K), 16-byte aligned */
     int ldres;
     float eps;
 } mq_stack_layer;

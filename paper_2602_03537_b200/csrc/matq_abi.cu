@@ -573,9 +573,23 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     const size_t cl_reserve = cl_max ? (size_t)32 * cl_max + (size_t)cl_max * 32 * nt * 16 : 0;
     // everything but the activation chunk: table, partial slots, zero-point
     // constants, barriers, a 2-deep ring
-    const size_t res_bytes = res_k_max ? (((size_t)B * res_k_max * 2 + 15) & ~(size_t)15) + (size_t)B * (res_k_max / 128) * 4 + 16 : 0;
-    const size_t other = res_bytes + sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
-                         (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 128 + (size_t)2 * mq::kStackWarps * stage_max + 256;
+    // [kept residual B x K bf16][row-group sums B x K/128] (+ a K fp32 copy of the RMSNorm
+    // weight when the one-chunk staging still fits beside it: read at staging time without
+    // an L2 round trip)
+    size_t res_bytes = res_k_max ? (((size_t)B * res_k_max * 2 + 15) & ~(size_t)15) +
+                                       (((size_t)B * (res_k_max / 128) * 4 + 15) & ~(size_t)15) + 16
+                                 : 0;
+    size_t other = res_bytes + sizeof(mq::StackLayer) * (size_t)n_layers + (size_t)mq::kStackWarps * 32 * nt * 16 +
+                   (zp_any ? (size_t)2 * nsteps_max * nt * 32 : 0) + cl_reserve + mq::kStackWarps * 128 + (size_t)2 * mq::kStackWarps * stage_max + 256;
+    size_t nw_bytes = 0;
+    if (res_k_max) {
+        const size_t need_xs = (size_t)nstage_max * B * (mq::pad256(res_k_max) + 8) * 2;
+        const size_t nw = (size_t)res_k_max * 4 + 16;
+        if (other + need_xs + nw <= kSmemFullSm) {
+            nw_bytes = nw;
+            other += nw;
+        }
+    }
     // the activation chunk's cap: 80 KB keeps B <= 4 stacks on the measured-best
     // decompositions; B >= 5 would otherwise split K > 2 ways (global split-K
     // tails) -- the ring needs only 2 stages (scripts/sweep_stages.sh), so give
@@ -596,7 +610,8 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (in.xop == MQ_XOP_SILU_MUL && in.ldx < 2 * in.K)
             return fail(MQ_ERR_INVALID, "layer %d: SiLU gating reads [g | u] of 2 K columns", i);
         if (in.xop == MQ_XOP_ADD_RMSNORM) {
-            if (!in.norm_w || (in.K & 127)) return fail(MQ_ERR_INVALID, "layer %d: add-RMSNorm needs norm_w, K %% 128 == 0", i);
+            if (!in.norm_w || (in.K & 127) || (reinterpret_cast<uintptr_t>(in.norm_w) & 15))
+                return fail(MQ_ERR_INVALID, "layer %d: add-RMSNorm needs a 16-byte aligned norm_w, K %% 128 == 0", i);
             if ((in.res_in || in.res_out) && (in.ldres < in.K || (in.ldres & 7)))
                 return fail(MQ_ERR_INVALID, "layer %d: bad residual stride", i);
             if (!in.res_in && (res_k == 0 || res_k != in.K))
@@ -716,7 +731,9 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         return fail(MQ_ERR_INVALID, "fused activation prologues need B <= 8 and parent layers");
     p.res_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);
     p.rpart_off = (int)((p.res_off + (size_t)B * res_k_max * 2 + 15) & ~(size_t)15);
-    p.cl_off = (int)((p.rpart_off + (size_t)B * (res_k_max / 128) * 4 + 15) & ~(size_t)15);
+    const int nw_at = (int)((p.rpart_off + (size_t)B * (res_k_max / 128) * 4 + 15) & ~(size_t)15);
+    p.nw_off = nw_bytes ? nw_at : 0;
+    p.cl_off = (int)((nw_at + (nw_bytes ? (size_t)res_k_max * 4 : 0) + 15) & ~(size_t)15);
     p.cluster = pair ? 1 : 0;
     p.cl_tiles = cl_tiles;
     // [full mbarriers, uses | free mbarriers, free uses] (32 B per tile) + the partial slots

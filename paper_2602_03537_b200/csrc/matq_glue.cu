@@ -149,9 +149,10 @@ __global__ void k_rope_kv(const __nv_bfloat16* __restrict__ qkv, const __nv_bflo
 // kv head writes the new k / v into the caches at pos; every CTA scores its q against
 // cache rows [0, pos) plus the new k (kept in shared memory: no cross-CTA ordering), with an
 // fp32 softmax (scale 1/sqrt(hd)) and an fp32 weighted sum of V -> bf16 att row.  The work
-// of torch SDPA (GQA) + k_rope_kv in one launch per layer.  Latency-shaped: a thread owns
-// whole keys in the score pass (hd / 8 16-byte loads in flight), and in the V pass a
-// (key slice, 8-dim group) with eight keys in flight; slices are summed in shared memory.
+// of torch SDPA (GQA) + k_rope_kv in one launch per layer.  Latency-shaped: every global
+// load of the first 256 keys (K row of key tid; V of keys ks + i KS, i < 16, for the
+// thread's 8-dim group) is issued at entry together with the q / k / v rows, so the kernel
+// waits on memory about once; longer contexts loop over the rest.
 constexpr int kAttnThreads = 256;
 
 template <int HD>
@@ -160,7 +161,7 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
               const __nv_bfloat16* __restrict__ sinv, const float* __restrict__ qn, const float* __restrict__ kn,
               float eps, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
               const int* __restrict__ kv_of_q, __nv_bfloat16* __restrict__ att, int nh, int nkv, int T, int pos) {
-    constexpr int HALF = HD / 2, DG = HD / 8, KS = kAttnThreads / DG;
+    constexpr int HALF = HD / 2, DG = HD / 8, KS = kAttnThreads / DG, VPF = kAttnThreads / KS;  // VPF = DG
     __shared__ __align__(16) float qs[HD];
     __shared__ float kns[HD], vns[HD];
     __shared__ float red[32];
@@ -171,66 +172,110 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
     const int h = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
     const int j = kv_of_q[h];
     const __nv_bfloat16* row = qkv + (long long)b * (nh + 2 * nkv) * HD;
-    // q head h and k head j: optional RMSNorm, then rotate (k_rope_kv's arithmetic)
-    for (int which = 0; which < 2; ++which) {
-        const __nv_bfloat16* src = row + (which == 0 ? h : nh + j) * HD;
-        const float* nw = which == 0 ? qn : kn;
-        float x = tid < HD ? bf(src[tid]) : 0.0f;
-        if (nw) {
-            const float inv = rsqrtf(block_sum(x * x, red) / (float)HD + eps);
-            x = bf(__float2bfloat16_rn(x * inv * (tid < HD ? nw[tid] : 0.0f)));
+    const __nv_bfloat16* kr = kc + ((long long)b * nkv + j) * T * HD;
+    const __nv_bfloat16* vr = vc + ((long long)b * nkv + j) * T * HD;
+    const int dg = tid % DG, ks = tid / DG;
+    const uint4* vp = reinterpret_cast<const uint4*>(vr) + dg;
+    // ---- every load the first pass needs, issued up front ----
+    const int jj = tid < HALF ? tid : tid - HALF;
+    float qx = 0.f, kx = 0.f, vx = 0.f, cs = 0.f, sn = 0.f, qw = 0.f, kw = 0.f;
+    if (tid < HD) {
+        qx = bf(row[h * HD + tid]);
+        kx = bf(row[(nh + j) * HD + tid]);
+        vx = bf(row[(nh + nkv + j) * HD + tid]);
+        cs = bf(cosv[jj]);
+        sn = bf(sinv[jj]);
+        if (qn) {
+            qw = qn[tid];
+            kw = kn[tid];
         }
-        float* dst = which == 0 ? qs : kns;
-        if (tid < HD) dst[tid] = x;
-        __syncthreads();
-        float o = 0.0f;
-        if (tid < HD) {
-            const int jj = tid < HALF ? tid : tid - HALF;
-            const float c = bf(cosv[jj]), s = bf(sinv[jj]);
-            const float x1 = dst[jj], x2 = dst[jj + HALF];
-            o = tid < HALF ? bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(x1 * c)) - bf(__float2bfloat16_rn(x2 * s))))
-                           : bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(x2 * c)) + bf(__float2bfloat16_rn(x1 * s))));
-        }
-        __syncthreads();
-        if (tid < HD) dst[tid] = o;
     }
-    if (tid < HD) vns[tid] = bf(row[(nh + nkv + j) * HD + tid]);
+    uint4 kreg[DG];
+    const bool has_k = tid < pos;
+    if (has_k) {
+        const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)tid * HD);
+#pragma unroll
+        for (int i = 0; i < DG; ++i) kreg[i] = __ldg(kp + i);
+    }
+    uint4 vreg[VPF];
+#pragma unroll
+    for (int i = 0; i < VPF; ++i) {
+        const int t = ks + i * KS;
+        vreg[i] = t < pos ? __ldg(vp + (long long)t * DG) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    // ---- q head h and k head j: optional RMSNorm, then rotate (k_rope_kv's arithmetic) ----
+    if (qn) {
+        const float iq = rsqrtf(block_sum(qx * qx, red) / (float)HD + eps);
+        const float ik = rsqrtf(block_sum(kx * kx, red) / (float)HD + eps);
+        qx = bf(__float2bfloat16_rn(qx * iq * qw));
+        kx = bf(__float2bfloat16_rn(kx * ik * kw));
+    }
+    if (tid < HD) {
+        qs[tid] = qx;
+        kns[tid] = kx;
+        vns[tid] = vx;
+    }
     __syncthreads();
-    // the first q head of kv head j publishes the new k / v into the caches
-    const bool writer = h == 0 || kv_of_q[h - 1] != j;
-    __nv_bfloat16* kr = kc + ((long long)b * nkv + j) * T * HD;
-    __nv_bfloat16* vr = vc + ((long long)b * nkv + j) * T * HD;
-    if (writer && tid < HD) {
-        kr[(long long)pos * HD + tid] = __float2bfloat16_rn(kns[tid]);
-        vr[(long long)pos * HD + tid] = __float2bfloat16_rn(vns[tid]);
-    }
-    // scores: thread t owns keys t, t + 256, ...; the new key (index pos) from shared memory
-    const float scale = rsqrtf((float)HD);
-    float mx = -INFINITY;
-    for (int t = tid; t <= pos; t += kAttnThreads) {
-        float d = 0.0f;
-        if (t < pos) {
-            const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)t * HD);
-            uint4 u[DG];
-#pragma unroll
-            for (int i = 0; i < DG; ++i) u[i] = __ldg(kp + i);
-#pragma unroll
-            for (int i = 0; i < DG; ++i) {
-                const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * i);
-                const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * i + 4);
-                const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
-                float2 f;
-                f = __bfloat1622float2(e[0]); d = fmaf(qa.x, f.x, d); d = fmaf(qa.y, f.y, d);
-                f = __bfloat1622float2(e[1]); d = fmaf(qa.z, f.x, d); d = fmaf(qa.w, f.y, d);
-                f = __bfloat1622float2(e[2]); d = fmaf(qb.x, f.x, d); d = fmaf(qb.y, f.y, d);
-                f = __bfloat1622float2(e[3]); d = fmaf(qb.z, f.x, d); d = fmaf(qb.w, f.y, d);
-            }
+    float qo = 0.f, ko = 0.f;
+    if (tid < HD) {
+        const float q1 = qs[jj], q2 = qs[jj + HALF], k1 = kns[jj], k2 = kns[jj + HALF];
+        if (tid < HALF) {
+            qo = bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(q1 * cs)) - bf(__float2bfloat16_rn(q2 * sn))));
+            ko = bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(k1 * cs)) - bf(__float2bfloat16_rn(k2 * sn))));
         } else {
-#pragma unroll 8
-            for (int i = 0; i < HD; ++i) d = fmaf(qs[i], kns[i], d);
+            qo = bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(q2 * cs)) + bf(__float2bfloat16_rn(q1 * sn))));
+            ko = bf(__float2bfloat16_rn(bf(__float2bfloat16_rn(k2 * cs)) + bf(__float2bfloat16_rn(k1 * sn))));
         }
-        d *= scale;
+    }
+    __syncthreads();
+    if (tid < HD) {
+        qs[tid] = qo;
+        kns[tid] = ko;
+        // the first q head of kv head j publishes the new k / v into the caches
+        if (h == 0 || kv_of_q[h - 1] != j) {
+            kc[(((long long)b * nkv + j) * T + pos) * HD + tid] = __float2bfloat16_rn(ko);
+            vc[(((long long)b * nkv + j) * T + pos) * HD + tid] = __float2bfloat16_rn(vx);
+        }
+    }
+    __syncthreads();
+    // ---- scores: thread t owns keys t, t + 256, ...; the new key (index pos) from shared memory ----
+    const float scale = rsqrtf((float)HD);
+    auto dot = [&](const uint4 (&u)[DG]) {
+        float d = 0.0f;
+#pragma unroll
+        for (int i = 0; i < DG; ++i) {
+            const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * i);
+            const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * i + 4);
+            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+            float2 f;
+            f = __bfloat1622float2(e[0]); d = fmaf(qa.x, f.x, d); d = fmaf(qa.y, f.y, d);
+            f = __bfloat1622float2(e[1]); d = fmaf(qa.z, f.x, d); d = fmaf(qa.w, f.y, d);
+            f = __bfloat1622float2(e[2]); d = fmaf(qb.x, f.x, d); d = fmaf(qb.y, f.y, d);
+            f = __bfloat1622float2(e[3]); d = fmaf(qb.z, f.x, d); d = fmaf(qb.w, f.y, d);
+        }
+        return d;
+    };
+    float mx = -INFINITY;
+    if (has_k) {
+        const float d = dot(kreg) * scale;
+        sc[tid] = d;
+        mx = d;
+    }
+    for (int t = tid + kAttnThreads; t < pos; t += kAttnThreads) {
+        uint4 u[DG];
+        const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)t * HD);
+#pragma unroll
+        for (int i = 0; i < DG; ++i) u[i] = __ldg(kp + i);
+        const float d = dot(u) * scale;
         sc[t] = d;
+        mx = fmaxf(mx, d);
+    }
+    if (tid == 0) {
+        float d = 0.0f;
+#pragma unroll 8
+        for (int i = 0; i < HD; ++i) d = fmaf(qs[i], kns[i], d);
+        d *= scale;
+        sc[pos] = d;
         mx = fmaxf(mx, d);
     }
 #pragma unroll
@@ -248,32 +293,11 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
         sum += e;
     }
     sum = block_sum(sum, red);  // ends with a barrier: every sc[] is visible
-    // V pass: thread (slice ks, dims 8 dg .. 8 dg + 7) sums keys ks, ks + KS, ...
-    const int dg = tid % DG, ks = tid / DG;
+    // ---- V: thread (slice ks, dims 8 dg .. 8 dg + 7) sums keys ks, ks + KS, ... ----
     float acc[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
-    const uint4* vp = reinterpret_cast<const uint4*>(vr) + dg;
-    int t = ks;
-    for (; t + 7 * KS < pos; t += 8 * KS) {
-        uint4 u[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) u[i] = __ldg(vp + (long long)(t + i * KS) * DG);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float p = sc[t + i * KS];
-            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const float2 f = __bfloat1622float2(e[k]);
-                acc[2 * k] = fmaf(p, f.x, acc[2 * k]);
-                acc[2 * k + 1] = fmaf(p, f.y, acc[2 * k + 1]);
-            }
-        }
-    }
-    for (; t < pos; t += KS) {
-        const uint4 u = __ldg(vp + (long long)t * DG);
-        const float p = sc[t];
+    auto axpy = [&](const uint4& u, float p) {
         const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -281,6 +305,22 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
             acc[2 * k] = fmaf(p, f.x, acc[2 * k]);
             acc[2 * k + 1] = fmaf(p, f.y, acc[2 * k + 1]);
         }
+    };
+#pragma unroll
+    for (int i = 0; i < VPF; ++i) {
+        const int t = ks + i * KS;
+        if (t < pos) axpy(vreg[i], sc[t]);
+    }
+    for (int t = ks + VPF * KS; t < pos; t += 8 * KS) {
+        uint4 u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int tt = t + i * KS;
+            u[i] = tt < pos ? __ldg(vp + (long long)tt * DG) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (t + i * KS < pos) axpy(u[i], sc[t + i * KS]);
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) part[ks][8 * dg + k] = acc[k];

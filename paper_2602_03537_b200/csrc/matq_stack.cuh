@@ -79,6 +79,7 @@ struct StackParams {
     int cluster;       // 1: CTA pairs (cluster of 2); S == 2 layers reduce through DSMEM
     int res_off;       // xop-1 stacks: byte offset of the kept residual [B][res_k] bf16 ...
     int rpart_off;     // ... and of its per-(row, 128-column group) sums of squares [B][res_k / 128]
+    int nw_off;        // ... and of the layer's RMSNorm weight [res_k] fp32 (copied by the pre-pass), or 0
     int res_k;
     int xops;          // some layer has a fused prologue: the XOPS kernel instantiation (NT = 1, parents)
     int cl_off;        // byte offset of the pair-reduction area: [cl_tiles mbarriers][cl_tiles use counters][slots]
@@ -447,7 +448,11 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
             // everything that does not wait on the producing layer is issued before the
             // LL polling (its loads are ordered after it): the residual, and the RMSNorm
             // weights the staging pass reads (into L1)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(L.norm_w + col));
+            float4 nw4[4];
+            if (b == 0 && p.nw_off) {  // the staging pass reads the RMSNorm weight from shared memory
+#pragma unroll
+                for (int i = 0; i < 4; ++i) nw4[i] = __ldg(reinterpret_cast<const float4*>(L.norm_w + col) + i);
+            }
             if (L.res_in) {
                 const uint16_t* src = L.res_in + (long long)b * L.ldres + col;
                 const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src)), c = __ldcg(reinterpret_cast<const uint4*>(src + 8));
@@ -459,6 +464,11 @@ __device__ __forceinline__ void stack_addnorm_prepass(const StackParams& p, cons
             }
             load_x16(p, L, b, col, true, tag, d);
             MQ_STS_WMAX(l + 128, 0);  // delta arrived (timing builds)
+            if (b == 0 && p.nw_off) {
+                float4* nw = reinterpret_cast<float4*>(smem_base + p.nw_off) + (col >> 2);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) nw[i] = nw4[i];
+            }
             uint32_t o[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -533,10 +543,18 @@ __device__ __forceinline__ void stack_stage(const StackParams& p, const StackLay
                 MQ_STS_WMAX(l + 128, 3);
                 const uint4 r0 = *reinterpret_cast<const uint4*>(rr), r1 = *reinterpret_cast<const uint4*>(rr + 8);
                 const uint32_t rw[8] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+                const float4* nw4 = p.nw_off ? reinterpret_cast<const float4*>(smem_base + p.nw_off) + (col >> 2)
+                                             : reinterpret_cast<const float4*>(L.norm_w + col);
+                float nw[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float4 v = nw4[i];
+                    nw[4 * i] = v.x; nw[4 * i + 1] = v.y; nw[4 * i + 2] = v.z; nw[4 * i + 3] = v.w;
+                }
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    const float a = __uint_as_float(rw[i] << 16) * inv * __ldg(L.norm_w + col + 2 * i);
-                    const float c = __uint_as_float(rw[i] & 0xFFFF0000u) * inv * __ldg(L.norm_w + col + 2 * i + 1);
+                    const float a = __uint_as_float(rw[i] << 16) * inv * nw[2 * i];
+                    const float c = __uint_as_float(rw[i] & 0xFFFF0000u) * inv * nw[2 * i + 1];
                     w[i] = (uint32_t)f32_to_bf16_rn(a) | ((uint32_t)f32_to_bf16_rn(c) << 16);
                 }
                 MQ_STS_WMAX(l + 128, 4);

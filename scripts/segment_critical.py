@@ -32,15 +32,19 @@ for name, prog in (("no prologues", mq.StackProgram(layers, r, 1)), ("fused prol
     for _ in range(5):
         prog.run()
     torch.cuda.synchronize()
-    tot = []
+    tot, subs = [], []
     for _ in range(5):
         prog.run()
         torch.cuda.synchronize()
         buf = np.zeros(256 * 148 * 8 + 256 * 16 * 4, dtype=np.uint64)
         assert L.mq_debug_stack_timestamps(buf.ctypes.data, buf.size) == 0
-        ts = buf[: 256 * 148 * 8].reshape(256, 148, 8).astype(np.float64)[:4]
+        full = buf[: 256 * 148 * 8].reshape(256, 148, 8).astype(np.float64)
+        ts = full[:4]
         t0 = ts[0, :, 0].min()
         ts = (ts - t0) / 1e3
+        sub = np.where(full[128:132] > 0, (full[128:132] - t0) / 1e3, np.nan)
+        subs.append([[np.nanmax(sub[l, :, k]) - ts[l, :, 0].max() if np.isfinite(sub[l, :, k]).any() else np.nan
+                      for k in range(6)] + [ts[l, :, 1].max() - ts[l, :, 0].max()] for l in range(4)])
         rows, prev_end = [], 0.0
         for l in range(4):
             end = ts[l, :, 6]
@@ -56,3 +60,8 @@ for name, prog in (("no prologues", mq.StackProgram(layers, r, 1)), ("fused prol
                                                      "layer", "median"))
     for k in range(4):
         print("%-8s " % kinds[k] + " ".join("%6.2f" % v for v in m[k, :8]))
+    sm = np.nanmedian(np.array(subs), axis=0)
+    print("staging sub-phases (latest warp, us after the latest CTA's layer start): delta-arrived, prepass-done, "
+          "sync, inv, X-ready, silu-done, staged")
+    for k in range(4):
+        print("%-8s " % kinds[k] + " ".join("%6.2f" % v for v in sm[k]))
