@@ -94,13 +94,34 @@ GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
             c.cs = cs;
         }
     }
-    c.grid = std::min(c.n_tiles * c.S, sms);
+    c.t1 = 0;
+    // whole waves + a split tail: when the tiles overflow the grid by R < sms, the first
+    // floor(n_tiles / sms) waves run whole tiles and the R leftover tiles are split S2
+    // ways over the last wave (every split resident: the coop reduction), instead of a
+    // nearly empty extra wave of whole tiles (Qwen3-14B o / down at B = 1024: 160 tiles)
+    const int waves = c.n_tiles / sms, rem = c.n_tiles - waves * sms;
+    if (waves >= 1 && rem > 0) {
+        for (int S2 = std::min(8, nsteps); S2 >= 2; --S2) {
+            const int cs2 = cdiv(nsteps, S2);
+            if (cdiv(nsteps, cs2) != S2 || rem * S2 > sms) continue;
+            const double cost = (double)waves * nsteps + cs2 + 1.5;
+            if (cost < best - 1e-9) {
+                best = cost;
+                c.t1 = waves * sms;
+                c.S = S2;
+                c.cs = cs2;
+            }
+            break;  // the largest admissible split is the cheapest tail
+        }
+    }
+    const int units = c.t1 + (c.n_tiles - c.t1) * c.S;
+    c.grid = std::min(units, sms);
     return c;
 }
 
 size_t gemm_ws_bytes(const GemmConfig& c) {
     if (c.S <= 1) return 0;
-    return kGemmTicketBytes + (size_t)c.n_tiles * c.S * c.bn * kGemmBM * sizeof(float);
+    return kGemmTicketBytes + (size_t)(c.n_tiles - c.t1) * c.S * c.bn * kGemmBM * sizeof(float);
 }
 
 cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
@@ -139,13 +160,14 @@ cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, in
     p.n_tiles = c.n_tiles;
     p.S = c.S;
     p.cs = c.cs;
+    p.t1 = c.t1;
     if (c.S > 1) {
         p.tickets = reinterpret_cast<int*>(ws);
         p.ws = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + kGemmTicketBytes);
     }
     p.out_scale = out_scale;
     p.y_f32 = y_f32 ? 1 : 0;
-    p.coop = (c.S > 1 && c.n_tiles * c.S <= c.grid) ? 1 : 0;
+    p.coop = (c.S > 1 && (c.n_tiles - c.t1) * c.S <= c.grid) ? 1 : 0;
 #ifdef MQ_GEMV_TIMING
     static int dbg_ctr = 0;
     p.dbg_slot = dbg_ctr++ % 64;

@@ -42,7 +42,8 @@ struct GemmParams {
     int ldy;
     int B, N, K, nsteps, n_rt;
     int n_bt, n_tiles;  // token tiles, output tiles
-    int S, cs;          // K splits, steps per split
+    int S, cs;          // K splits, steps per split (of tiles t1 ..)
+    int t1;             // tiles [0, t1) are whole units (full waves before a split tail)
     float* ws;          // fp32 partials [n_tiles * S][BN][128] when S > 1
     int* tickets;       // [n_tiles], zero, self-resetting
     float out_scale;
@@ -143,16 +144,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     pdl_launch_dependents();
     if (threadIdx.x == 0) MQ_GTS(0);
 
-    const int n_units = p.n_tiles * p.S;
+    const int n_units = p.t1 + (p.n_tiles - p.t1) * p.S;
     const int my_units = (int)blockIdx.x < n_units ? (n_units - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-    // unit -> (tile, split, step range); consecutive units are splits of one tile
+    // unit -> (tile, split, step range); units [0, t1) are whole tiles, then consecutive
+    // units are the S splits of one tile
     auto unit_of = [&](int ui, int& tile, int& split, int& st0, int& nst) {
         const int u = (int)blockIdx.x + ui * (int)gridDim.x;
-        tile = u / p.S;
-        split = u - tile * p.S;
+        if (u < p.t1) {
+            tile = u;
+            split = 0;
+            st0 = 0;
+            nst = p.nsteps;
+            return;
+        }
+        const int v = u - p.t1;
+        tile = p.t1 + v / p.S;
+        split = v - (tile - p.t1) * p.S;
         st0 = split * p.cs;
         nst = max(0, min(p.nsteps, st0 + p.cs) - st0);
     };
+    auto is_split = [&](int tile) { return p.S > 1 && tile >= p.t1; };
+    // fp32 partials of the split tiles: [(tile - t1) * S + split][BN / 4][128][4]
+    auto part_base = [&](int tile) { return p.ws + (long long)(tile - p.t1) * p.S * (BN * kGemmBM); };
 
     // flattened (unit, step) sequence of this CTA
     int total_steps = 0;
@@ -257,13 +270,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             };
             // split-K partial of this unit: [BN / 4][128 rows][4] floats (float4 per row and
             // 4 columns: the TMEM lane's 32 columns go out as 8 vector stores)
-            float4* part4 = reinterpret_cast<float4*>(p.ws + ((long long)tile * p.S + split) * (BN * kGemmBM));
+            const bool split_tile = is_split(tile);
+            float4* part4 = split_tile ? reinterpret_cast<float4*>(part_base(tile) + (long long)split * (BN * kGemmBM))
+                                       : nullptr;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t v[32];
                 tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN + 32 * c), v);
                 tmem_ld_wait();
-                if (p.S == 1) {
+                if (!split_tile) {
                     if (row < p.N) {
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
@@ -281,7 +296,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty(buf));
-            if (p.S > 1) {
+            if (split_tile) {
                 // publish the partial.  coop (every unit resident at once): the whole CTA
                 // reduces a 1/S share of the tile's columns after the role loops (below);
                 // otherwise the last split to arrive reduces the tile here.  Split order
@@ -294,7 +309,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const int arrived = *flag_ptr;
                 const int q_hi = arrived == p.S - 1 ? (b_lim + 3) >> 2 : 0;  // column quads reduced here
                 __threadfence();
-                const float4* t0 = reinterpret_cast<const float4*>(p.ws + (long long)tile * p.S * (BN * kGemmBM));
+                const float4* t0 = reinterpret_cast<const float4*>(part_base(tile));
                 const long long sstride = (long long)(BN / 4) * kGemmBM;  // float4s per split
                 if (row < p.N) {
 #pragma unroll 1
@@ -399,12 +414,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
     tc_fence_before();
     __syncthreads();
-    if (p.coop && my_units == 1) {
-        // coop split-K: once all S partials of this CTA's tile exist, all 23 warps reduce this
-        // split's 1/S share of the columns (flattened (column quad, row) tasks, rows fastest:
-        // coalesced loads and Y stores; four tasks in flight per thread)
-        int tile, split, st0, nst;
-        unit_of(0, tile, split, st0, nst);
+    int l_tile = 0, l_split = 0, l_st0 = 0, l_nst = 0;
+    if (my_units > 0) unit_of(my_units - 1, l_tile, l_split, l_st0, l_nst);
+    if (p.coop && my_units > 0 && is_split(l_tile)) {
+        // coop split-K: once all S partials of this CTA's (last, split) tile exist, all 23
+        // warps reduce this split's 1/S share of the columns (flattened (column quad, row)
+        // tasks, rows fastest: coalesced loads and Y stores; four tasks in flight per thread)
+        const int tile = l_tile, split = l_split;
         const int mt = tile / p.n_bt, bt = tile % p.n_bt;
         const int b_lim = min(BN, p.B - bt * BN);
         const int nq = (b_lim + 3) >> 2;
@@ -414,7 +430,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
         __syncthreads();
         __threadfence();
-        const float4* t0 = reinterpret_cast<const float4*>(p.ws + (long long)tile * p.S * (BN * kGemmBM));
+        const float4* t0 = reinterpret_cast<const float4*>(part_base(tile));
         const long long sstride = (long long)(BN / 4) * kGemmBM;
         const int ntask = (q_hi - q_lo) * kGemmBM;
         constexpr int kU = 4;

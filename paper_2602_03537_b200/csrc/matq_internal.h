@@ -67,6 +67,7 @@ cudaError_t launch_silu_mul(const void* gu, void* y, int B, int inter, cudaStrea
 
 struct GemmConfig {
     int bn, n_tiles, S, cs, grid;
+    int t1;  // tiles [0, t1) run whole (one unit each); tiles [t1, n_tiles) split S ways
 };
 // Split-K tickets at the head of the K4 workspace (same convention as K3's).
 constexpr size_t kGemmTicketBytes = 64 * 1024;

@@ -425,9 +425,32 @@ def test_gemm_qwen_shapes_vs_fp32_torch(mq):
                 got = pt.gemm(X, r, out_dtype=torch.float32)
                 assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 5e-3, (n, k, B, r)
                 # batch rows are independent of the token tile they land in (a
-                # different B may pick another K split: fp32 rounding only)
+                # different B may pick another K split: fp32 rounding only, ~1e-5 of
+                # max |y| over K = 17408 when one side splits K 8 ways)
                 half = pt.gemm(X[: B // 2].contiguous(), r, out_dtype=torch.float32)
-                assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 1e-5
+                assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 5e-5
+
+
+def test_gemm_whole_waves_then_split_tail(mq):
+    """More tiles than SMs with a small remainder (19 row tiles x 8 token tiles = 152 on
+    148 SMs): one wave of whole tiles, then the 4 leftover tiles split over the last
+    wave.  Against fp32 torch on the exactly decoded weights, row-independent of the
+    path (the first half of the batch takes a whole-tile config), deterministic."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    n, k, B = 2432, 2048, 2048
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("the tile arithmetic assumes 148 SMs")
+    assert mq.device.gemm_workspace_bytes(n, k, B) > 0  # a split tail (whole tiles alone need none)
+    pt = mq.PlaneTensor.random_parent(n, k, seed=5)
+    g = torch.Generator(device="cuda").manual_seed(8)
+    X = torch.randn(B, k, device="cuda", generator=g).to(torch.bfloat16)
+    for r in (2, 4, 8):
+        want = X.float() @ pt.decode(r).T
+        got = pt.gemm(X, r, out_dtype=torch.float32)
+        assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 5e-3, r
+        assert torch.equal(got, pt.gemm(X, r, out_dtype=torch.float32))
+        half = pt.gemm(X[: B // 2].contiguous(), r, out_dtype=torch.float32)
+        assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 1e-5
 
 
 def test_linear_dispatch(mq):
