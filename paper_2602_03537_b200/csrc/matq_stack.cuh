@@ -1102,7 +1102,9 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
             named_bar_arrive(wa + 1, 32 * (1 + tile_parts(wp, wa, llast)));
         } else {
             // head: own part, the later warps' parts in warp order, then the next
-            // CTA's part (a tile running past this CTA's range), in that order
+            // CTA's part (a tile running past this CTA's range), in that order.  (Issuing
+            // the first poll of that part before the local-parts barrier measured no
+            // faster and cost the r = 4 kernel 2% through register allocation.)
             if (!lend) {
                 named_bar_sync(warp + 1, 32 * (1 + tile_parts(wp, warp, llast)));
                 if (f == wp.f1) MQ_STS_WMAX(l, 3);  // the parts of this warp's last tile arrived
@@ -1233,7 +1235,10 @@ __global__ void __launch_bounds__(kStackThreads, 1) k_stack(const StackParams p)
     }
     // programmatic dependent launch: the producer warp streams the (static) weights while
     // the previous kernel drains; consumers touch activations / outputs only after it is done
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifndef MQ_STACK_GDC
+#define MQ_STACK_GDC 1
+#endif
+    if (MQ_STACK_GDC) asm volatile("griddepcontrol.wait;" ::: "memory");
     const unsigned long long target = (sh.gen + 1ull) * gridDim.x;
     int cstage = 0;
     uint32_t parity = 0;
