@@ -7,13 +7,14 @@ the decode number can be set beside the paper's full-model measurement
 rank's own heads, one all-reduce after o and after down).
 
 Everything around the hot path is NOT part of the deliverable: embedding
-lookup, RMSNorm, rotary embedding, a KV cache with grouped-query attention
-(torch SDPA), SiLU gating, residuals, and a bf16 ``lm_head``.  ``glue="cuda"``
-(default) runs the row-wise steps as three fused kernels from libmatq
-(residual add + RMSNorm, rotary + KV-cache write, SiLU gating: 3 launches per
-block instead of ~25 torch kernels; attention stays torch SDPA, which beat a
-simple single-query kernel here); ``glue="torch"`` is the plain-torch
-statement of the same step, which the tests compare against.  The projections (q/k/v fused, o, gate/up fused, down) are int8
+lookup, RMSNorm, rotary embedding, a KV cache with grouped-query attention,
+SiLU gating, residuals, and a bf16 ``lm_head``.  ``glue="cuda"`` (default)
+runs them as libmatq kernels: with ``linears="k3s"`` the residual add +
+RMSNorm and the SiLU gating are fused into the K3S segments' activation
+staging, and one ``mq_attn_decode`` launch per layer does the rotary step,
+the KV-cache write and single-query GQA attention; ``glue="torch"`` is the
+plain-torch statement of the same step (torch SDPA), which the tests compare
+against.  The projections (q/k/v fused, o, gate/up fused, down) are int8
 parents sliced on the fly by K3 (decode) -- per layer a bit-width, uniform or
 from an EvoPress-style config.  One decode step = one token for every sequence
 in the batch at a fixed context length, replayed as one CUDA graph.
