@@ -379,6 +379,48 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     if (lane == 0) mbar_arrive(raw_empty(rsl));
                     const uint32_t s_lo = valid ? bf16x2_splat(sc[0] * p.out_scale) : 0u;
                     const uint32_t s_hi = valid ? bf16x2_splat(sc[1] * p.out_scale) : 0u;
+#ifndef MQ_GEMM_PREDECODE
+#define MQ_GEMM_PREDECODE 1
+#endif
+                    if (MQ_GEMM_PREDECODE) {
+                        // decode both words of the pair before waiting for their operand
+                        // stages: two independent dependency chains in flight, and the
+                        // decode overlaps the MMA still reading those stages
+                        uint32_t A2[2][16];
+                        if (valid) {
+#pragma unroll
+                            for (int wi = 0; wi < 2; ++wi) {
+                                uint32_t T[NPL];
+#pragma unroll
+                                for (int jj = 0; jj < NPL; ++jj) T[jj] = wi ? raw[jj].y : raw[jj].x;
+                                uint32_t Sl[R];
+                                slice_loaded<R, CHILD>(T, Sl);
+                                decode_word<R, false>(Sl, A2[wi]);
+#pragma unroll
+                                for (int qq = 0; qq < 16; ++qq)
+                                    A2[wi][qq] = hmul2_bf16(A2[wi][qq], (qq & 1) ? s_hi : s_lo);
+                            }
+                        }
+#pragma unroll
+                        for (int wi = 0; wi < 2; ++wi) {
+                            const int ks = 4 * fglob + 2 * half + wi;
+                            const int s = ks % NS;
+                            mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
+                            if (valid) {
+                                const uint32_t abase = a_st(s) + row_off;
+#pragma unroll
+                                for (int k16 = 0; k16 < 4; ++k16) {
+                                    const uint32_t chunk = (uint32_t)(2 * k16 + (jm >> 1));
+                                    stmatrix_x4(abase + ((chunk ^ swz) << 4), A2[wi][4 * k16], A2[wi][4 * k16 + 1],
+                                                A2[wi][4 * k16 + 2], A2[wi][4 * k16 + 3]);
+                                }
+                                fence_proxy_async_smem();
+                            }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(op_full(s));
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int wi = 0; wi < 2; ++wi) {
                         const int w = 2 * half + wi;
