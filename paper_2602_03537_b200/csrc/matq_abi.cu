@@ -555,11 +555,11 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (!valid_r(ri)) return fail(MQ_ERR_INVALID, "layer %d: unsupported bits %d", i, ri);
         // k_stack's staging rule: fp16 decode for r in {4, 8} at nt = 1 (copies at
         // offsets {0, 4} / {0} + the raw bf16 chunk), else the bf16 zero-point copies
-        const bool f16 = (ri == 4 || ri == 8) && nt == 1;
-        const int ncopy = f16 ? (ri == 4 ? 2 : 1) : ((ri != 8 && nt == 1) ? mq::zp_ncopies(ri) : 1);
+        const bool f16 = mq::stack_f16(ri, nt);
+        const int ncopy = f16 ? (ri == 4 ? 2 : 1) : (mq::stack_zp(ri, nt) ? mq::zp_ncopies(ri) : 1);
         nstage_max = std::max(nstage_max, f16 ? ncopy + 1 : ncopy);
         // k_stack's ZP rule (r = 6: one copy, constants still needed)
-        zp_any = zp_any || f16 || (ri != 8 && nt == 1);
+        zp_any = zp_any || mq::stack_zp(ri, nt);
         // budget the ring as if for a parent slice (r + 1 planes) even for children,
         // so a child stack gets its parent's decomposition (same summation order)
         const int npl_budget = ri == 8 ? 8 : ri + 1;

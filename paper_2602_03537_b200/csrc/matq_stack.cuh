@@ -29,6 +29,19 @@
 
 namespace mq {
 
+// Staging / decode mode of a stack layer (the planner mirrors it for the shared-memory
+// budget): fp16 decode for r in {4, 8}, else bf16 with the zero point folded into a
+// per-(group, row) constant (r != 8), both at one n-tile (B <= 8).  MQ_STACK_WIDE_ZP=1
+// extends them to B <= 16: correct (tests pass) but measured 3-9x slower -- the extra
+// activation copies for 16 rows crowd shared memory, so K splits many ways.
+#ifndef MQ_STACK_WIDE_ZP
+#define MQ_STACK_WIDE_ZP 0
+#endif
+__host__ __device__ constexpr bool stack_f16(int r, int nt) { return (r == 4 || r == 8) && (nt == 1 || MQ_STACK_WIDE_ZP); }
+__host__ __device__ constexpr bool stack_zp(int r, int nt) {
+    return stack_f16(r, nt) || (r != 8 && (nt == 1 || MQ_STACK_WIDE_ZP));
+}
+
 struct __align__(8) StackLayer {
     const uint32_t* blob;
     long long step_words;
@@ -754,8 +767,8 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // offsets 0 and 4 and a whole byte at 0, cutting the decode's ALU work by
     // 15-24% (scripts/micro/decode_rate.cu); activations are staged as fp16
     // scaled by a per-CTA power of two (exact; keeps them inside fp16's range)
-    constexpr bool F16 = (R == 4 || R == 8) && NT == 1;
-    constexpr bool ZP = F16 || ((R != 8) && (NT == 1));  // see k_gemv
+    constexpr bool F16 = stack_f16(R, NT);
+    constexpr bool ZP = stack_zp(R, NT);  // see k_gemv
     constexpr int NCOPY = F16 ? (R == 4 ? 2 : 1) : (ZP ? zp_ncopies(R) : 1);
     uint16_t* xs = reinterpret_cast<uint16_t*>(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

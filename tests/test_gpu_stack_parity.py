@@ -9,7 +9,8 @@ layer, at full model depth and on adversarial activations.
   <= 1e-2 (reference metric test_matmul.py:19-20).  Outputs
   must be finite -- no skipping.
 * Outlier activations (a few channels at 1e3 amid 1e-4 values, all-zero K
-  chunks, an all-zero row) through the fp16 staging (r in {4, 8}, B <= 8) and
+  chunks, an all-zero row) through the fp16 staging (r in {4, 8}, B <= 8), the bf16
+  two-n-tile path (B = 13, 16) and
   the bf16 zero-point staging (r in {2, 3, 6}).
 * The 64-bit step counter: seeded just below 2^32 launches and stepped across
   it (a 32-bit counter would mis-order the layer barriers there).
@@ -106,7 +107,7 @@ def _adversarial_x(B, K, kind, seed):
     return x.to(torch.bfloat16)
 
 
-@pytest.mark.parametrize("B", [1, 4, 8])
+@pytest.mark.parametrize("B", [1, 4, 8, 13, 16])
 @pytest.mark.parametrize("r", LADDER)
 @pytest.mark.parametrize("kind", ["outlier", "zeros", "both"])
 def test_adversarial_activations_vs_oracle(mq, r, B, kind):
