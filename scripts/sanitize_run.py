@@ -3,7 +3,9 @@
     compute-sanitizer --tool racecheck python scripts/sanitize_run.py k3s
 Paths: k3s (2-block stack, tiny shapes: stream-K, pair and global split-K
 layers, LL hand-off), k3s_llama (one Llama-3.1-8B block), mixed (per-layer r),
-k3 (single GEMV, B in {1, 5}), k4 (tcgen05 GEMM)."""
+k3 (single GEMV, B in {1, 5}), k4 (tcgen05 GEMM), k4tail (whole waves + split tail),
+decoder (a tiny Qwen3-style decoder step: K3S segments with fused add+RMSNorm / SiLU
+prologues, the decode-attention kernel, glue kernels)."""
 import os
 import sys
 
@@ -45,3 +47,20 @@ elif what == "k4":
         y = pt.gemm(X, r)
     torch.cuda.synchronize()
     print("k4 ok", float(y.float().abs().sum()))
+elif what == "k4tail":
+    pt = mq.PlaneTensor.random_parent(2432, 2048, 128, seed=3)
+    X = torch.randn(2048, 2048, device="cuda").to(torch.bfloat16)
+    y = pt.gemm(X, 4)
+    torch.cuda.synchronize()
+    print("k4tail ok", float(y.float().abs().sum()))
+elif what == "decoder":
+    from paper_2602_03537_b200.llama import LlamaDecoder
+
+    shape = DecoderShape("tiny", 512, 1024, 8, 2, 64, 2, qk_norm=True)
+    for B in (1, 3):
+        dec = LlamaDecoder(shape, batch=B, context=16, bits=4, vocab=1024, linears="k3s")
+        dec.tokens.copy_(torch.arange(B, device="cuda") + 1)
+        with torch.cuda.stream(dec.stream):
+            dec._forward()
+        dec.stream.synchronize()
+        print("decoder B", B, "ok", float(dec.logits.float().abs().sum()))
