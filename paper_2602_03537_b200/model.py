@@ -186,11 +186,10 @@ class LinearStack:
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
         if len(rs) == 1:
             # measured (scripts/dispatch_matrix.py, profiles/r2_dispatch_matrix.txt): K3S wins
-            # at B <= 2 for every r, at B <= 4 but r = 8, at B <= 8 for r in {2, 3, 6} and at
-            # B = 16 for r = 2 only; the fp16 staging path (r in {4, 8}) degrades with B
+            # at B <= 4 for every r, at B <= 8 but r = 8 and at B = 16 for r = 2 only (the
+            # two-n-tile bf16 path at B > 8 splits K many ways)
             r0 = next(iter(rs))
-            ok = (self.B <= 2 or (self.B <= 4 and r0 != 8) or (self.B <= 8 and r0 in (2, 3, 6))
-                  or r0 == 2)
+            ok = self.B <= 4 or (self.B <= 8 and r0 != 8) or r0 == 2
         else:
             # per-layer r (the dispatch kernel): 1.61 vs 1.96 ms fused, 1.99 vs 2.17 ms for the
             # 224 unfused linears of C3 at B = 1 (scripts/stack_matrix.py)
