@@ -165,10 +165,18 @@ typedef struct mq_stack_layer {
     const float* norm_w;  /* fp32 (K), 16-byte aligned */
     int ldres;
     float eps;
+    /* output epilogue (0 = none):
+     *   MQ_YOP_SILU_PAIRS: the layer's rows come in 16-row tiles of 8 gate rows followed by the
+     *     8 matching up rows (a fused gate/up weight stored interleaved); Y is (B, N / 2):
+     *     Y[:, 8t + i] = bf16(bf16(silu(bf16(g))) * bf16(u)), g / u = tile t's rows i / 8 + i --
+     *     mq_silu_mul's math, done where the rows are finished (N % 16 == 0). */
+    int yop;
 } mq_stack_layer;
 #define MQ_XOP_NONE 0
 #define MQ_XOP_ADD_RMSNORM 1
 #define MQ_XOP_SILU_MUL 2
+#define MQ_YOP_NONE 0
+#define MQ_YOP_SILU_PAIRS 1
 MQ_API size_t mq_stack_plan_bytes(void);
 MQ_API size_t mq_stack_table_bytes(int n_layers);
 MQ_API int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int nplanes,

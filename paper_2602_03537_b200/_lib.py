@@ -97,10 +97,12 @@ class StackLayer(ctypes.Structure):
                 ("ldx", ctypes.c_int), ("ldy", ctypes.c_int), ("N", ctypes.c_int), ("K", ctypes.c_int),
                 ("out_scale", ctypes.c_float), ("r", ctypes.c_int),
                 ("xop", ctypes.c_int), ("res_in", ctypes.c_void_p), ("res_out", ctypes.c_void_p),
-                ("norm_w", ctypes.c_void_p), ("ldres", ctypes.c_int), ("eps", ctypes.c_float)]
+                ("norm_w", ctypes.c_void_p), ("ldres", ctypes.c_int), ("eps", ctypes.c_float),
+                ("yop", ctypes.c_int)]
 
 
 MQ_XOP_NONE, MQ_XOP_ADD_RMSNORM, MQ_XOP_SILU_MUL = 0, 1, 2
+MQ_YOP_NONE, MQ_YOP_SILU_PAIRS = 0, 1
 
 
 class MatqError(RuntimeError):

@@ -496,6 +496,7 @@ size_t stack_ws_layout(int n_layers, size_t ll_bytes, size_t partial_bytes, size
 // X decides: X must lie entirely inside Y_j (same row stride, even element
 // offset) -- then layer i polls j's LL words -- else the stack cannot order the
 // two (-2).  -1: no earlier layer writes X (activations from outside the step).
+int stack_out_width(const mq_stack_layer& o) { return o.yop == MQ_YOP_SILU_PAIRS ? o.N / 2 : o.N; }
 int stack_x_producer(const mq_stack_layer* layers, int i, int B, size_t* elem_off) {
     const mq_stack_layer& in = layers[i];
     const int xw = in.xop == MQ_XOP_SILU_MUL ? 2 * in.K : in.K;  // columns of X the layer reads
@@ -503,10 +504,11 @@ int stack_x_producer(const mq_stack_layer* layers, int i, int B, size_t* elem_of
     const uintptr_t x0 = lo(in.X), x1 = x0 + 2 * ((size_t)(B - 1) * in.ldx + xw);
     for (int j = i - 1; j >= 0; --j) {
         const mq_stack_layer& o = layers[j];
-        const uintptr_t y0 = lo(o.Y), y1 = y0 + 2 * ((size_t)(B - 1) * o.ldy + o.N);
+        const int on = stack_out_width(o);
+        const uintptr_t y0 = lo(o.Y), y1 = y0 + 2 * ((size_t)(B - 1) * o.ldy + on);
         if (x1 <= y0 || y1 <= x0) continue;  // no overlap: look further back
         const size_t e = (x0 - y0) / 2;  // X's first element inside Y (row 0: both have B rows)
-        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 4 == 0 && e + (size_t)xw <= (size_t)o.N;
+        const bool inside = o.ldy == in.ldx && x0 >= y0 && (x0 - y0) % 4 == 0 && e + (size_t)xw <= (size_t)on;
         *elem_off = e;
         return inside ? j : -2;
     }
@@ -608,10 +610,13 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (nplanes < ri || nplanes > 8 || (nplanes != ri && nplanes < ri + 1))
             return fail(MQ_ERR_INVALID, "cannot slice %d bits out of %d planes", ri, nplanes);
         if (!in.blob || !in.X || !in.Y) return fail(MQ_ERR_INVALID, "layer %d: null pointer", i);
-        if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < in.N || (in.ldx & 7) ||
+        if (in.N < 1 || in.K < 1 || (in.K & 7) || in.ldx < in.K || in.ldy < (in.yop == MQ_YOP_SILU_PAIRS ? in.N / 2 : in.N) || (in.ldx & 7) ||
             (reinterpret_cast<uintptr_t>(in.X) & 15))
             return fail(MQ_ERR_INVALID, "layer %d: bad shape / alignment", i);
         if (in.xop < MQ_XOP_NONE || in.xop > MQ_XOP_SILU_MUL) return fail(MQ_ERR_INVALID, "layer %d: bad xop", i);
+        if (in.yop != MQ_YOP_NONE && in.yop != MQ_YOP_SILU_PAIRS) return fail(MQ_ERR_INVALID, "layer %d: bad yop", i);
+        if (in.yop == MQ_YOP_SILU_PAIRS && ((in.N & 15) || in.ldy < in.N / 2))
+            return fail(MQ_ERR_INVALID, "layer %d: gated output needs N %% 16 == 0 and ldy >= N / 2", i);
         if (in.xop == MQ_XOP_SILU_MUL && in.ldx < 2 * in.K)
             return fail(MQ_ERR_INVALID, "layer %d: SiLU gating reads [g | u] of 2 K columns", i);
         if (in.xop == MQ_XOP_ADD_RMSNORM) {
@@ -622,7 +627,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
             if (!in.res_in && (res_k == 0 || res_k != in.K))
                 return fail(MQ_ERR_INVALID, "layer %d: no kept residual of width %d before it", i, in.K);
             for (int j = 0; j < i; ++j)
-                if (in.res_in && stack_overlap(in.res_in, in.ldres, in.K, layers[j].Y, layers[j].ldy, layers[j].N, B))
+                if (in.res_in && stack_overlap(in.res_in, in.ldres, in.K, layers[j].Y, layers[j].ldy, stack_out_width(layers[j]), B))
                     return fail(MQ_ERR_INVALID, "layer %d: the residual is written inside the stack", i);
             res_k = in.K;
         }
@@ -659,6 +664,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         t.norm_w = in.norm_w;
         t.ldres = in.ldres;
         t.eps = in.eps;
+        t.yop = in.yop;
         t.r = ri;
         t.stage_bytes = npl * 512 + 128;
         t.xll = -1;
@@ -678,7 +684,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (j >= 0) {
             if (T[j].yll < 0) {  // j's output gets LL words: [B][pad16(N_j) / 2]
                 T[j].yll = (long long)(ll_bytes / 8);
-                T[j].ldyll = T[j].Np / 2;
+                T[j].ldyll = (T[j].yop == MQ_YOP_SILU_PAIRS ? T[j].Np / 2 : T[j].Np) / 2;
                 ll_bytes += (size_t)B * T[j].ldyll * 8;
             }
             t.xll = T[j].yll + (long long)(e / 2);
@@ -687,7 +693,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
             // activations from outside the step: a later layer overwriting them waits
             // until every CTA staged them
             for (int k = i; k < n_layers; ++k)
-                if (stack_overlap(in.X, in.ldx, in.K, layers[k].Y, layers[k].ldy, layers[k].N, B)) {
+                if (stack_overlap(in.X, in.ldx, in.K, layers[k].Y, layers[k].ldy, stack_out_width(layers[k]), B)) {
                     t.ext_pub = 1;
                     war[(size_t)k] = std::max(war[(size_t)k], i);
                 }
@@ -731,7 +737,7 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
     p.table_off = (int)((p.slot_off + slot_bytes + 15) & ~(size_t)15);
     p.res_k = res_k_max;
     p.xops = 0;
-    for (int i = 0; i < n_layers; ++i) p.xops |= layers[i].xop != MQ_XOP_NONE;
+    for (int i = 0; i < n_layers; ++i) p.xops |= layers[i].xop != MQ_XOP_NONE || layers[i].yop != MQ_YOP_NONE;
     if (p.xops && (nt != 1 || nplanes != 8))
         return fail(MQ_ERR_INVALID, "fused activation prologues need B <= 8 and parent layers");
     p.res_off = (int)((p.table_off + sizeof(mq::StackLayer) * (size_t)n_layers + 15) & ~(size_t)15);

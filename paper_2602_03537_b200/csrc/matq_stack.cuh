@@ -72,6 +72,7 @@ struct __align__(8) StackLayer {
     const float* norm_w;     // xop 1: RMSNorm weight [K]
     int ldres;
     float eps;
+    int yop;          // MQ_YOP_SILU_PAIRS: rows interleaved 8 gate / 8 up per tile; Y = silu(g) * u, N / 2 wide
     int tk_off;       // S > 1 through the workspace: this layer's own tickets (StackParams::tickets + tk_off)
     long long ws_off;  // and its own partials (StackParams::ws + ws_off): no layer reuses another's, since
                        // without grid barriers a fast CTA may already be a layer ahead
@@ -917,6 +918,36 @@ __device__ __forceinline__ void stack_layer(const StackParams& p, const StackLay
     // the final values of a tile (row r0 + 8h, batch nt * 8 + 2t + c in v[nt][2h + c]):
     // plain bf16 Y and, when a later layer reads it, the LL words (row pairs)
     auto store_final = [&](int rt, const float (&v)[NT][4]) {
+        if (XOPS && L.yop) {
+            // gated output: lane (g, t) holds gate row g (h = 0) and its up row g + 8 (h = 1)
+            // of tile rt for batch columns 2t, 2t + 1 -> act row 8 rt + g
+            const int a = rt * 8 + g;
+            uint16_t ab[NT][2];
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint32_t gw = f32_to_bf16_rn(v[nt][c]), uw = f32_to_bf16_rn(v[nt][2 + c]);
+                    const uint32_t o = silu_mul_bf16x2(gw, uw) & 0xFFFFu;
+                    ab[nt][c] = (uint16_t)o;
+                    const int b = nt * 8 + 2 * t + c;
+                    if (b < p.B && 2 * a < L.N) st_global_u16(L.Y + (long long)b * L.ldy + a, ab[nt][c]);
+                }
+            if (L.yll >= 0) {
+                // act rows (a, a + 1) pair up across lanes g, g + 1 (lane ^ 4): even g writes
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const uint32_t nb = __shfl_xor_sync(0xffffffffu, (uint32_t)ab[nt][c], 4);
+                        const int b = nt * 8 + 2 * t + c;
+                        if ((g & 1) == 0 && b < p.B && 2 * a < L.N)
+                            st_ll(p.ll + L.yll + (long long)b * L.ldyll + (a >> 1), (uint32_t)ab[nt][c] | (nb << 16),
+                                  sh.tag);
+                    }
+            }
+            return;
+        }
         const int r0 = rt * kTileRows + g;
         uint16_t yb[NT][4];
 #pragma unroll

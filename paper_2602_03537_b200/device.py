@@ -355,9 +355,9 @@ class StackProgram:
     """
 
     def __init__(self, layers, r, B: int, ops=None):
-        """``ops``: optional per-layer activation prologue (None or a dict with xop,
-        res_in, res_out, norm_w, eps: mq_stack_layer's fused residual-add + RMSNorm /
-        SiLU gating)."""
+        """``ops``: optional per-layer activation prologue / output epilogue (None or a
+        dict with xop, res_in, res_out, norm_w, eps, yop: mq_stack_layer's fused
+        residual-add + RMSNorm / SiLU gating of the input, gated output)."""
         import ctypes
 
         _lib.require_cuda()
@@ -382,7 +382,8 @@ class StackProgram:
                                      pt.N, pt.K, scale, rs[i])
             op = ops[i] if ops else None
             if op:
-                arr[i].xop = int(op["xop"])
+                arr[i].xop = int(op.get("xop", 0))
+                arr[i].yop = int(op.get("yop", 0))
                 for key in ("res_in", "res_out"):
                     t = op.get(key)
                     if t is not None:

@@ -100,6 +100,14 @@ class LlamaDecoder:
                     pt = PlaneTensor.from_codes(codes[rows, c0:c1].contiguous(), 8,
                                                 scales[rows, g0:g1].contiguous(), 128)
                     del codes, scales
+                elif kind == "gate_up" and linears == "k3s":
+                    # K3S computes silu(gate) * up where the rows finish (MQ_YOP_SILU_PAIRS): the
+                    # fused parent is stored interleaved, 8 gate rows then their 8 up rows per
+                    # 16-row tile (the same weights, another row order)
+                    codes, scales = PlaneTensor.random_parent_codes(N, K, 128, sd, _gain_matched_scales(K), True)
+                    perm = self._glu_rows(N // 2, dev)
+                    pt = PlaneTensor.from_codes(codes[perm].contiguous(), 8, scales[perm].contiguous(), 128)
+                    del codes, scales
                 else:
                     pt = PlaneTensor.random_parent(N, K, seed=sd, scale_range=_gain_matched_scales(K),
                                                    signed_rows=True)
@@ -136,6 +144,20 @@ class LlamaDecoder:
         self.stream = torch.cuda.Stream()
         self.graph = None
         self.segments = None
+
+    @staticmethod
+    def _glu_rows(inter: int, dev) -> torch.Tensor:
+        """Row order of an interleaved gate/up parent: per 16-row tile, gate rows 8t..8t+7
+        then up rows inter + 8t .. inter + 8t + 7."""
+        t = torch.arange(inter // 8, device=dev).repeat_interleave(8) * 8 + torch.arange(8, device=dev).repeat(inter // 8)
+        return torch.stack((t.view(-1, 8), (t + inter).view(-1, 8)), dim=1).reshape(-1)
+
+    @property
+    def gate_up_rows(self):
+        """The gate_up parent's row order (None: [gate | up]), for references that decode it."""
+        if self.linears != "k3s":
+            return None
+        return self._glu_rows(self.inter, self.embed.device)
 
     def _all_reduce(self, t: torch.Tensor) -> None:
         if self.tp > 1:
@@ -179,23 +201,24 @@ class LlamaDecoder:
         self.segments = None
 
     def _build_segments(self) -> None:
-        """K3S programs: block i's [o_i, gate_up_i (+ x += o; RMSNorm ln2), down_i (+ SiLU
-        gating), qkv_{i+1} (+ x += down; RMSNorm ln1 of block i+1; x written back)]; the
-        last block writes its post-attention residual to buf['xr'] for the final norm."""
+        """K3S programs: block i's [o_i, gate_up_i (+ x += o; RMSNorm ln2; SiLU gating of
+        its interleaved rows as it writes them), down_i, qkv_{i+1} (+ x += down; RMSNorm ln1
+        of block i+1; x written back)]; the last block writes its post-attention residual
+        to buf['xr'] for the final norm."""
         from . import _lib
         from .device import StackProgram
 
         b, h, nb = self.buf, self.shape.hidden, len(self.blocks)
         self.segments = []
         for i, blk in enumerate(self.blocks):
-            layers = [(blk["o"].planes, b["att"], b["o"]), (blk["gate_up"].planes, b["o"], b["gu"]),
-                      (blk["down"].planes, b["gu"], b["d"])]
+            layers = [(blk["o"].planes, b["att"], b["o"]), (blk["gate_up"].planes, b["o"], b["act"]),
+                      (blk["down"].planes, b["act"], b["d"])]
             rs = [blk["o"].bits, blk["gate_up"].bits, blk["down"].bits]
             last = i == nb - 1
             ops = [None,
                    dict(xop=_lib.MQ_XOP_ADD_RMSNORM, res_in=b["x"], res_out=b["xr"] if last else None,
-                        norm_w=blk["ln2"], eps=1e-5),
-                   dict(xop=_lib.MQ_XOP_SILU_MUL)]
+                        norm_w=blk["ln2"], eps=1e-5, yop=_lib.MQ_YOP_SILU_PAIRS),
+                   None]
             if not last:
                 nxt = self.blocks[i + 1]
                 layers.append((nxt["qkv"].planes, b["d"], b["qkv"]))

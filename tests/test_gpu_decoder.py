@@ -60,6 +60,11 @@ def _fp32_reference(dec, r):
     x = dec.embed[dec.tokens].float()
     for blk in dec.blocks:
         W = {k: blk[k].planes.decode(r) for k in ("qkv", "o", "gate_up", "down")}
+        perm = dec.gate_up_rows  # k3s decoders store gate/up interleaved (MQ_YOP_SILU_PAIRS)
+        if perm is not None:
+            std = torch.empty_like(W["gate_up"])
+            std[perm] = W["gate_up"]
+            W["gate_up"] = std
         qkv = rms(x, blk["ln1"]) @ W["qkv"].t()
         if s.qk_norm:
             qk = qkv[:, : (nh + nkv) * hd].view(B, nh + nkv, hd)

@@ -201,3 +201,43 @@ def test_llama_fused_glue_matches_torch_glue(model):
         outs[glue] = dec.logits.float().clone()
     assert torch.isfinite(outs["cuda"]).all()
     assert rel_err(outs["cuda"].cpu().numpy(), outs["torch"].cpu().numpy()) <= 2e-2
+
+
+@pytest.mark.parametrize("B", [1, 3])
+@pytest.mark.parametrize("r", [2, 4, 8])
+def test_stack_gated_output_epilogue(model, B, r):
+    """MQ_YOP_SILU_PAIRS: an interleaved gate/up parent (8 gate rows, then their 8 up
+    rows, per 16-row tile) writes bf16(bf16(silu(bf16 g)) * bf16 u) as it finishes each
+    tile, and the next layer stages it through the LL words: against the same parent run
+    as a plain layer, split and gated in torch (the rounding torch's glue applies)."""
+    import paper_2602_03537_b200 as mq
+    from paper_2602_03537_b200 import _lib
+    from paper_2602_03537_b200.llama import LlamaDecoder
+
+    inter, K = 1024, 2048
+    perm = LlamaDecoder._glu_rows(inter, "cuda")
+    codes, scales = mq.PlaneTensor.random_parent_codes(2 * inter, K, 128, 11, (0.005, 0.02), True)
+    gu = mq.PlaneTensor.from_codes(codes[perm].contiguous(), 8, scales[perm].contiguous(), 128)
+    down = mq.PlaneTensor.random_parent(512, inter, 128, 12, (0.005, 0.02))
+    g = torch.Generator(device="cuda").manual_seed(B + r)
+    X = torch.randn(B, K, device="cuda", generator=g).to(torch.bfloat16)
+    act = torch.full((B, inter), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Y = torch.full((B, 512), float("nan"), dtype=torch.bfloat16, device="cuda")
+    prog = mq.StackProgram([(gu, X, act), (down, act, Y)], r, B,
+                           ops=[dict(yop=_lib.MQ_YOP_SILU_PAIRS), None])
+    prog.run()
+    # reference: the same interleaved parent as a plain layer, then split and gate in torch
+    plain = torch.zeros((B, 2 * inter), dtype=torch.bfloat16, device="cuda")
+    mq.StackProgram([(gu, X, plain)], r, B).run()
+    torch.cuda.synchronize()
+    t = plain.view(B, inter // 8, 2, 8)
+    gate, up = t[:, :, 0].reshape(B, inter), t[:, :, 1].reshape(B, inter)
+    want = (torch.nn.functional.silu(gate.float()).to(torch.bfloat16).float() * up.float()).to(torch.bfloat16)
+    assert torch.isfinite(act.float()).all()
+    # same fp32 sums up to summation order -> bf16 inputs may differ by an ulp
+    assert rel_err(act.float().cpu().numpy(), want.float().cpu().numpy()) <= 1e-2
+    y_ref = torch.zeros_like(Y)
+    mq.StackProgram([(down, act, y_ref)], r, B).run()
+    torch.cuda.synchronize()
+    assert torch.isfinite(Y.float()).all()
+    assert rel_err(Y.float().cpu().numpy(), y_ref.float().cpu().numpy()) <= 1e-2
