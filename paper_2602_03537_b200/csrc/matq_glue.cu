@@ -190,12 +190,17 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
             kw = kn[tid];
         }
     }
-    uint4 kreg[DG];
-    const bool has_k = tid < pos;
-    if (has_k) {
-        const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)tid * HD);
+    // K: coalesced -- a key row is read by DG consecutive lanes (16 bytes each); a warp covers
+    // KPW keys per round, the CTA KPR; the first NR rounds (256 keys) are prefetched
+    constexpr int KPW = 32 / DG, KPR = (kAttnThreads / 32) * KPW, NR = 256 / KPR;
+    const int warp = tid >> 5, lane = tid & 31, dch = lane % DG, ksub = lane / DG;
+    const uint4* kbase = reinterpret_cast<const uint4*>(kr) + dch;
+    auto key_of = [&](int k) { return k * KPR + warp * KPW + ksub; };
+    uint4 kreg[NR];
 #pragma unroll
-        for (int i = 0; i < DG; ++i) kreg[i] = __ldg(kp + i);
+    for (int k = 0; k < NR; ++k) {
+        const int t = key_of(k);
+        kreg[k] = t < pos ? __ldg(kbase + (long long)t * DG) : make_uint4(0u, 0u, 0u, 0u);
     }
     uint4 vreg[VPF];
 #pragma unroll
@@ -240,35 +245,38 @@ k_attn_decode(const __nv_bfloat16* __restrict__ qkv, const __nv_bfloat16* __rest
     __syncthreads();
     // ---- scores: thread t owns keys t, t + 256, ...; the new key (index pos) from shared memory ----
     const float scale = rsqrtf((float)HD);
-    auto dot = [&](const uint4 (&u)[DG]) {
+    const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * dch);
+    const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * dch + 4);
+    auto dot8 = [&](const uint4& u) {  // this lane's 8 dims; summed over the key's DG lanes
+        const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u);
         float d = 0.0f;
+        float2 f;
+        f = __bfloat1622float2(e[0]); d = fmaf(qa.x, f.x, d); d = fmaf(qa.y, f.y, d);
+        f = __bfloat1622float2(e[1]); d = fmaf(qa.z, f.x, d); d = fmaf(qa.w, f.y, d);
+        f = __bfloat1622float2(e[2]); d = fmaf(qb.x, f.x, d); d = fmaf(qb.y, f.y, d);
+        f = __bfloat1622float2(e[3]); d = fmaf(qb.z, f.x, d); d = fmaf(qb.w, f.y, d);
 #pragma unroll
-        for (int i = 0; i < DG; ++i) {
-            const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * i);
-            const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * i + 4);
-            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
-            float2 f;
-            f = __bfloat1622float2(e[0]); d = fmaf(qa.x, f.x, d); d = fmaf(qa.y, f.y, d);
-            f = __bfloat1622float2(e[1]); d = fmaf(qa.z, f.x, d); d = fmaf(qa.w, f.y, d);
-            f = __bfloat1622float2(e[2]); d = fmaf(qb.x, f.x, d); d = fmaf(qb.y, f.y, d);
-            f = __bfloat1622float2(e[3]); d = fmaf(qb.z, f.x, d); d = fmaf(qb.w, f.y, d);
-        }
+        for (int o = DG / 2; o >= 1; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
         return d;
     };
     float mx = -INFINITY;
-    if (has_k) {
-        const float d = dot(kreg) * scale;
-        sc[tid] = d;
-        mx = d;
-    }
-    for (int t = tid + kAttnThreads; t < pos; t += kAttnThreads) {
-        uint4 u[DG];
-        const uint4* kp = reinterpret_cast<const uint4*>(kr + (long long)t * HD);
 #pragma unroll
-        for (int i = 0; i < DG; ++i) u[i] = __ldg(kp + i);
-        const float d = dot(u) * scale;
-        sc[t] = d;
-        mx = fmaxf(mx, d);
+    for (int k = 0; k < NR; ++k) {
+        const float d = dot8(kreg[k]) * scale;
+        const int t = key_of(k);
+        if (dch == 0 && t < pos) {
+            sc[t] = d;
+            mx = fmaxf(mx, d);
+        }
+    }
+    for (int k = NR; k * KPR < pos; ++k) {  // contexts past 256 keys
+        const int t = key_of(k);
+        const uint4 u = t < pos ? __ldg(kbase + (long long)t * DG) : make_uint4(0u, 0u, 0u, 0u);
+        const float d = dot8(u) * scale;
+        if (dch == 0 && t < pos) {
+            sc[t] = d;
+            mx = fmaxf(mx, d);
+        }
     }
     if (tid == 0) {
         float d = 0.0f;
