@@ -773,10 +773,11 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
                   void* table_host, size_t* workspace_bytes) {
     const char* env = getenv("MQ_STACK_PAIR");
     bool pair = sm_count() % 2 == 0 && !(env && env[0] == '0');
-    // two n-tiles (B > 8) at r >= 3: the pair slots' shared memory costs the staging more
-    // than the DSMEM reduction saves (B = 16 r = 4 4.10 -> 2.98 ms, r = 8 21.5 -> 4.5 ms
-    // without pairs; r = 2 keeps them: 2.25 vs 2.63 ms)
-    if (B > 8 && r != 2 && r != 0 && !(env && env[0] == '1')) pair = false;
+    // two n-tiles (B > 8) at r >= 3, and r = 8 at B = 8: the pair slots' shared memory costs
+    // the staging more than the DSMEM reduction saves (B = 16 r = 4 4.10 -> 2.98 ms, r = 8
+    // 21.5 -> 4.5 ms; B = 8 r = 8 2.63 -> 2.38 ms without pairs; r = 2 at B = 16 and every
+    // r < 8 at B <= 8 keep them)
+    if (((B > 8 && r != 2) || (B == 8 && r == 8)) && r != 0 && !(env && env[0] == '1')) pair = false;
     int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
     if (st || !pair) return st;
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);

@@ -186,9 +186,9 @@ class LinearStack:
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
         if len(rs) == 1:
             # measured (scripts/dispatch_matrix.py, profiles/r2_dispatch_matrix.txt): K3S wins
-            # at B <= 4 for every r and up to B = 16 for r != 8
+            # at B <= 8 for every r and up to B = 16 for r != 8
             r0 = next(iter(rs))
-            ok = self.B <= 4 or r0 != 8
+            ok = self.B <= 8 or r0 != 8
         else:
             # per-layer r (the dispatch kernel): 1.61 vs 1.96 ms fused, 1.99 vs 2.17 ms for the
             # 224 unfused linears of C3 at B = 1 (scripts/stack_matrix.py)
