@@ -597,11 +597,20 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
             other += nw;
         }
     }
-    // the activation chunk's cap: 80 KB keeps B <= 4 stacks on the measured-best
-    // decompositions; B >= 5 would otherwise split K > 2 ways (global split-K
-    // tails) -- the ring needs only 2 stages (scripts/sweep_stages.sh), so give
-    // staging the rest (B = 8, r = 4: 3.17 -> 2.04 ms/step)
-    const size_t xs_cap = B <= 4 ? (size_t)80 * 1024 : (size_t)192 * 1024;
+    // the activation chunk's cap keeps B <= 4 stacks on the measured-best decompositions;
+    // B >= 5 would otherwise split K > 2 ways (global split-K tails) -- the ring needs only
+    // 2 stages (scripts/sweep_stages.sh), so give staging the rest (B = 8, r = 4: 3.17 ->
+    // 2.04 ms/step)
+    // Measured on the Llama-3.1-8B stack (MQ_STACK_XS_CAP_KB sweep 40..192 KB per B and r):
+    // a smaller cap moves the big-K layers to other K splits; best per batch: 48 KB at
+    // B = 1 / 3 and B = 2 r = 2, 64 KB at B = 2 r >= 3 and B = 4 (B = 2 r = 2 1.448 ->
+    // 1.335 ms, B = 3 r = 4 1.607 -> 1.494, B = 4 r = 4 1.709 -> 1.581 vs the earlier 80 KB)
+    size_t xs_cap = (size_t)192 * 1024;
+    if (B == 1 || B == 3 || (B == 2 && r == 2)) xs_cap = (size_t)48 * 1024;
+    else if (B <= 4) xs_cap = (size_t)64 * 1024;
+    if (const char* e = getenv("MQ_STACK_XS_CAP_KB")) xs_cap = (size_t)atoi(e) * 1024;  // tuning
+    if (res_k_max)  // an add + RMSNorm prologue stages its whole row in one chunk
+        xs_cap = std::max(xs_cap, (size_t)nstage_max * B * (mq::pad256(res_k_max) + 8) * 2);
     const size_t xs_budget = std::min<size_t>(xs_cap, kSmemFullSm - std::min(other, kSmemFullSm));
     for (int i = 0; i < n_layers; ++i) {
         const mq_stack_layer& in = layers[i];
