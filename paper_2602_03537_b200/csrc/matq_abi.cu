@@ -644,8 +644,20 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         uniform = uniform && ri == r_first;
         const bool child = nplanes == ri;
         const int npl = (child || ri == 8) ? ri : ri + 1;
-        const StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair,
-                                               in.xop == MQ_XOP_ADD_RMSNORM);
+        StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair,
+                                         in.xop == MQ_XOP_ADD_RMSNORM);
+        // r = 3: CTA-pair halves for the K <= 4096 layers beat one stream-K chunk (Llama stack
+        // 1.317 -> 1.284 ms at B = 1, 1.443 -> 1.385 at B = 2; r = 4 is slower that way, 2 / 6 / 8
+        // within 1%); MQ_STACK_FORCE_PAIR_K overrides the K limit (tuning)
+        const char* fpk = getenv("MQ_STACK_FORCE_PAIR_K");
+        const int pair_k = fpk ? atoi(fpk) : (r == 3 ? 4096 : 0);
+        {
+            const int nst = mq::pad256(in.K) / 256;
+            if (pair && in.K <= pair_k && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
+                const int cs = mq::cdiv(nst, 2);
+                c = StackCfg{2, cs, std::min(sm_count() / 2, mq::pad16(in.N) / 16)};
+            }
+        }
         if (in.xop == MQ_XOP_ADD_RMSNORM && c.S != 1)
             return fail(MQ_ERR_INVALID, "layer %d: the fused prologue's row does not fit the staging area", i);
         const mq::Layout L = mq::Layout::make(in.N, in.K, 128, nplanes);
