@@ -646,14 +646,17 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         const int npl = (child || ri == 8) ? ri : ri + 1;
         StackCfg c = choose_stack_config(in.N, in.K, B, nstage_max, sm_count(), xs_budget, pair,
                                          in.xop == MQ_XOP_ADD_RMSNORM);
-        // r = 3: CTA-pair halves for the K <= 4096 layers beat one stream-K chunk (Llama stack
-        // 1.317 -> 1.284 ms at B = 1, 1.443 -> 1.385 at B = 2; r = 4 is slower that way, 2 / 6 / 8
-        // within 1%); MQ_STACK_FORCE_PAIR_K overrides the K limit (tuning)
+        // Small layers (K <= 4096, N <= 6144: Llama's qkv and o) as CTA-pair K halves beat one
+        // stream-K chunk: the stream-K boundary exchange and the 1-2 tiles per CTA cost more
+        // than the DSMEM reduction (Llama stack B = 1: r = 4 1.351 -> 1.320 ms, r = 2 1.215 ->
+        // 1.180, r = 3 1.317 -> 1.279; B = 2 r = 4 1.490 -> 1.425).  Larger layers keep the
+        // cost model's choice.  MQ_STACK_FORCE_PAIR_K / _N override the limits (tuning).
         const char* fpk = getenv("MQ_STACK_FORCE_PAIR_K");
-        const int pair_k = fpk ? atoi(fpk) : (r == 3 ? 4096 : 0);
+        const char* fpn = getenv("MQ_STACK_FORCE_PAIR_N");
+        const int pair_k = fpk ? atoi(fpk) : 4096, pair_n = fpn ? atoi(fpn) : 6144;
         {
             const int nst = mq::pad256(in.K) / 256;
-            if (pair && in.K <= pair_k && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
+            if (pair && in.K <= pair_k && in.N <= pair_n && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
                 const int cs = mq::cdiv(nst, 2);
                 c = StackCfg{2, cs, std::min(sm_count() / 2, mq::pad16(in.N) / 16)};
             }
