@@ -557,14 +557,11 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         if (!valid_r(ri)) return fail(MQ_ERR_INVALID, "layer %d: unsupported bits %d", i, ri);
         // k_stack's staging rule: fp16 decode for r in {4, 8} at nt = 1 (copies at
         // offsets {0, 4} / {0}), else the bf16 zero-point copies
-        // At B = 1 the budget keeps one spare copy (the round-1 two-pass staging's raw
-        // bf16 tail, unused since): it steers the 14336-wide down layers to a CTA-pair
-        // split, measured 1% faster there than one stream-K chunk.  At B >= 2 the spare
-        // copy only forced extra K splits: B = 8 r = 4 2.71 -> 1.80 ms, r = 8 4.83 -> 2.63 ms
-        // without it (scripts/ab_k3s.sh).
+        // (round 1 reserved one more copy for the fp16 path's two-pass staging; dropping it
+        // took B = 8 r = 4 2.71 -> 1.80 ms and r = 8 4.83 -> 2.63 ms, neutral at B = 1)
         const bool f16 = mq::stack_f16(ri, nt);
         const int ncopy = f16 ? (ri == 4 ? 2 : 1) : (mq::stack_zp(ri, nt) ? mq::zp_ncopies(ri) : 1);
-        nstage_max = std::max(nstage_max, f16 ? ncopy + (B == 1 ? 1 : 0) : ncopy);
+        nstage_max = std::max(nstage_max, ncopy);
         // k_stack's ZP rule (r = 6: one copy, constants still needed)
         zp_any = zp_any || mq::stack_zp(ri, nt);
         // budget the ring as if for a parent slice (r + 1 planes) even for children,
