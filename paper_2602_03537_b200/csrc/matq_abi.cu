@@ -404,7 +404,9 @@ int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, int ldx, 
 size_t mq_gemm_workspace_bytes(int N, int K, int B, int flags) {
     (void)flags;
     if (N < 1 || K < 1 || B < 1) return 0;
-    return mq::gemm_ws_bytes(mq::choose_gemm_config(N, K, B, sm_count()));
+    // r is not an argument: the larger of the 256- and 512-token tilings' needs
+    return std::max(mq::gemm_ws_bytes(mq::choose_gemm_config(N, K, B, sm_count(), 4)),
+                    mq::gemm_ws_bytes(mq::choose_gemm_config(N, K, B, sm_count(), 8)));
 }
 
 int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int B, int N, int K,
@@ -420,7 +422,7 @@ int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int 
     if (flags & MQ_X_F32) return fail(MQ_ERR_INVALID, "mq_gemm takes bf16 activations");
     if ((ldx & 7) || (reinterpret_cast<uintptr_t>(X) & 15))
         return fail(MQ_ERR_INVALID, "activations must be 16-byte aligned with ldx %% 8 == 0");
-    const mq::GemmConfig c = mq::choose_gemm_config(N, K, B, sm_count());
+    const mq::GemmConfig c = mq::choose_gemm_config(N, K, B, sm_count(), r);
     const size_t need = mq::gemm_ws_bytes(c);
     if (need > workspace_bytes || (need && !workspace))
         return fail(MQ_ERR_WORKSPACE, "workspace %zu bytes < required %zu", workspace_bytes, need);

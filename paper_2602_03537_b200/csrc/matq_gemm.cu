@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "matq_gemm.cuh"
@@ -56,6 +57,9 @@ cudaError_t launch_rc(int bn, const CUtensorMap& map, const GemmParams& p, int g
                       cudaStream_t stream, bool pdl) {
     if (bn == 64) return launch_bn<R, CHILD, 64>(map, p, grid, stream, pdl);
     if (bn == 128) return launch_bn<R, CHILD, 128>(map, p, grid, stream, pdl);
+    if constexpr (gemm_bn512_ok(R)) {
+        if (bn == 512) return launch_bn<R, CHILD, 512>(map, p, grid, stream, pdl);
+    }
     return launch_bn<R, CHILD, 256>(map, p, grid, stream, pdl);
 }
 
@@ -70,9 +74,11 @@ unsigned long long* gemm_dbg_buffer() {
 }
 #endif
 
-GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
+namespace {
+// one token-tile width: the split-K / split-tail plan minimising the busiest CTA's steps
+GemmConfig plan_gemm(int N, int K, int B, int sms, int bn, double* cost_out) {
     GemmConfig c{};
-    c.bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
+    c.bn = bn;
     const int n_bt = cdiv(B, c.bn);
     c.n_tiles = cdiv(N, kGemmBM) * n_bt;
     const int nsteps = pad256(K) / 256;
@@ -116,6 +122,29 @@ GemmConfig choose_gemm_config(int N, int K, int B, int sms) {
     }
     const int units = c.t1 + (c.n_tiles - c.t1) * c.S;
     c.grid = std::min(units, sms);
+    *cost_out = best;
+    return c;
+}
+}  // namespace
+
+GemmConfig choose_gemm_config(int N, int K, int B, int sms, int r) {
+    double cost = 0.0;
+    const int bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
+    GemmConfig c = plan_gemm(N, K, B, sms, bn, &cost);
+    // past 256 tokens a 512-token tile decodes each weight tile once for two N = 256
+    // MMAs (r <= 6: the 8-plane raw ring does not fit beside 2 operand stages of 80 KB).
+    // Its steps are MMA-bound at twice the 256-token step, and 2 operand stages plus a
+    // single TMEM accumulator cost ~10% more (measured: 2.2 x); it wins where the
+    // halved tile count fills the SMs better (Qwen3-14B o / down at B = 384-512)
+    static const bool bn512 = [] {
+        const char* e = getenv("MQ_GEMM_BN512");
+        return !(e && e[0] == '0');
+    }();
+    if (B > 256 && bn512 && gemm_bn512_ok(r)) {
+        double cost512 = 0.0;
+        const GemmConfig c512 = plan_gemm(N, K, B, sms, 512, &cost512);
+        if (2.2 * cost512 < cost) c = c512;
+    }
     return c;
 }
 
@@ -136,7 +165,7 @@ cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, in
     CUtensorMap map;
     const cuuint64_t dims[2] = {(cuuint64_t)L.K, (cuuint64_t)B};
     const cuuint64_t strides[1] = {(cuuint64_t)ldx * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)c.bn};
+    const cuuint32_t box[2] = {(cuuint32_t)kGemmBK, (cuuint32_t)std::min(c.bn, 256)};
     const cuuint32_t estr[2] = {1, 1};
     CUresult cr = enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(X), dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -85,7 +85,9 @@ struct GemmSmem {
     static constexpr uint32_t kRawBytes = kRowTiles * gemm_raw_block_bytes(NPL);
     static constexpr uint32_t kFixed = 1024 + 512;  // alignment slack + barriers
     static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget) ? 3 : 2;
-    static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 4 : 3;
+    static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget)   ? 4
+                            : (kFixed + 3 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 3
+                                                                                       : 2;
     static constexpr uint32_t kRawOff = NS * kOpBytes;
     static constexpr uint32_t kBarOff = kRawOff + RS * kRawBytes;
     static constexpr uint32_t kBytes = kBarOff + kFixed;
@@ -98,7 +100,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int NPL = PlaneCount<R, CHILD>::value;
     using SM = GemmSmem<BN, NPL>;
     constexpr int NS = SM::NS, RS = SM::RS;
-    constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    // BN = 512 (two 256-token halves of one decoded weight tile): two N = 256 MMAs per
+    // k16 into one 512-column accumulator, which fills TMEM, so it is single-buffered
+    constexpr int kMmaN = BN > 256 ? 256 : BN, kNB = BN / kMmaN;
+    constexpr int kNBuf = 2 * BN <= 512 ? 2 : 1;
+    constexpr uint32_t kTmemCols = kNBuf * BN < 32 ? 32 : kNBuf * BN;
+    auto tbuf = [&](int ui) { return kNBuf == 2 ? (ui & 1) : 0; };
+    auto tpar = [&](int ui) { return kNBuf == 2 ? ((ui >> 1) & 1) : (ui & 1); };
     constexpr uint32_t kBlk = gemm_raw_block_bytes(NPL);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t base = (smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -129,7 +137,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_init(raw_full(s), 1);
             mbar_init(raw_empty(s), kNumDecWarps);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < kNBuf; ++b) {
             mbar_init(tfull(b), 1);
             mbar_init(tempty(b), 4);
         }
@@ -189,7 +197,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                         const int s = ks % NS;
                         mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
                         mbar_expect_tx(op_full(s), SM::kBBytes);
-                        tma_load_2d(b_st(s), &tmx, (st0 + si) * 256 + kk * kGemmBK, bt * BN, op_full(s));
+#pragma unroll
+                        for (int nb = 0; nb < kNB; ++nb)
+                            tma_load_2d(b_st(s) + (uint32_t)(nb * kMmaN * 128), &tmx, (st0 + si) * 256 + kk * kGemmBK,
+                                        bt * BN + nb * kMmaN, op_full(s));
                     }
                 }
             }
@@ -222,13 +233,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     } else if (warp == kWarpMma) {
         // ---------------- MMA issuer ----------------------------------------
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc_bf16(kGemmBM, BN);
+            constexpr uint32_t idesc = umma_idesc_bf16(kGemmBM, kMmaN);
             int ks = 0;
             for (int ui = 0; ui < my_units; ++ui) {
                 int tile, split, st0, nst;
                 unit_of(ui, tile, split, st0, nst);
-                const int buf = ui & 1;
-                mbar_wait(tempty(buf), ((ui >> 1) & 1) ^ 1);
+                const int buf = tbuf(ui);
+                mbar_wait(tempty(buf), tpar(ui) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + (uint32_t)(buf * BN);
                 for (int kk = 0; kk < 4 * nst; ++kk, ++ks) {
@@ -239,8 +250,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
                     for (int k16 = 0; k16 < kGemmBK / 16; ++k16) {
                         const uint64_t ad = umma_desc_k_sw128(a_st(s) + (uint32_t)k16 * 32u);
-                        const uint64_t bd = umma_desc_k_sw128(b_st(s) + (uint32_t)k16 * 32u);
-                        umma_bf16(d, ad, bd, idesc, (kk | k16) != 0);
+#pragma unroll
+                        for (int nb = 0; nb < kNB; ++nb) {
+                            const uint64_t bd =
+                                umma_desc_k_sw128(b_st(s) + (uint32_t)(nb * kMmaN * 128) + (uint32_t)k16 * 32u);
+                            umma_bf16(d + (uint32_t)(nb * kMmaN), ad, bd, idesc, (kk | k16) != 0);
+                        }
                     }
                     umma_commit(op_empty(s));
                 }
@@ -257,8 +272,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             int tile, split, st0, nst;
             unit_of(ui, tile, split, st0, nst);
             const int mt = tile / p.n_bt, bt = tile % p.n_bt;
-            const int buf = ui & 1;
-            mbar_wait(tfull(buf), (ui >> 1) & 1);
+            const int buf = tbuf(ui);
+            mbar_wait(tfull(buf), tpar(ui));
             if (warp == kEpiWarp0 && lane == 0 && ui == my_units - 1) MQ_GTS(4);
             tc_fence_after();
             const int row = mt * kGemmBM + et;
@@ -351,6 +366,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // ---------------- decoders: raw blocks -> bf16 A operand -----------------
             const int dw = warp - kDecWarp0;
             const int rtl = dw & (kRowTiles - 1), half = dw >> 3;  // row tile, word pair
+            // with only 2 operand stages (BN = 512) the two decoders of a row tile must not
+            // share a stage slot (a warp could lap the other by a whole mbarrier phase, which
+            // the parity wait cannot see): decoder `half` takes words {half, half + 2}, both
+            // in slot `half`; otherwise words {2 half, 2 half + 1}
+            constexpr bool kSlotPairs = NS == 2;
+            auto word_of = [&](int wi) { return kSlotPairs ? half + 2 * wi : 2 * half + wi; };
             const int g = lane >> 2;
             // stmatrix row address: matrix j = lane >> 3 holds rows +8 (j & 1), columns +8 (j >> 1)
             const int jm = lane >> 3;
@@ -367,18 +388,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     mbar_wait(raw_full(rsl), (fglob / RS) & 1);
                     if (fglob == 0 && dw == 0 && lane == 0) MQ_GTS(1);
                     uint2 raw[NPL];  // the two words (of four) of this decoder's word pair
-                    float sc[2];
+                    uint32_t s_lo[2], s_hi[2];  // per word of the pair: group scale, rows g / g + 8
                     const uint32_t blk = raw_st(rsl) + (uint32_t)rtl * kBlk;
                     if (valid) {
-                        sc[0] = lds32f(blk + 4u * (16 * half + g));
-                        sc[1] = lds32f(blk + 4u * (16 * half + g + 8));
 #pragma unroll
-                        for (int jj = 0; jj < NPL; ++jj) raw[jj] = lds64(blk + 128u + 512u * jj + 16u * lane + 8u * half);
+                        for (int wi = 0; wi < 2; ++wi) {
+                            const int grp = word_of(wi) >> 1;  // 128-column scale group of the word
+                            s_lo[wi] = bf16x2_splat(lds32f(blk + 4u * (16 * grp + g)) * p.out_scale);
+                            s_hi[wi] = bf16x2_splat(lds32f(blk + 4u * (16 * grp + g + 8)) * p.out_scale);
+                        }
+                        if constexpr (kSlotPairs) {
+#pragma unroll
+                            for (int jj = 0; jj < NPL; ++jj) {
+                                const uint32_t wb = blk + 128u + 512u * jj + 16u * lane;
+                                raw[jj] = make_uint2(__float_as_uint(lds32f(wb + 4u * word_of(0))),
+                                                     __float_as_uint(lds32f(wb + 4u * word_of(1))));
+                            }
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < NPL; ++jj)
+                                raw[jj] = lds64(blk + 128u + 512u * jj + 16u * lane + 8u * half);
+                        }
+                    } else {
+                        s_lo[0] = s_lo[1] = s_hi[0] = s_hi[1] = 0u;
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(raw_empty(rsl));
-                    const uint32_t s_lo = valid ? bf16x2_splat(sc[0] * p.out_scale) : 0u;
-                    const uint32_t s_hi = valid ? bf16x2_splat(sc[1] * p.out_scale) : 0u;
 #ifndef MQ_GEMM_PREDECODE
 #define MQ_GEMM_PREDECODE 1
 #endif
@@ -398,12 +433,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                 decode_word<R, false>(Sl, A2[wi]);
 #pragma unroll
                                 for (int qq = 0; qq < 16; ++qq)
-                                    A2[wi][qq] = hmul2_bf16(A2[wi][qq], (qq & 1) ? s_hi : s_lo);
+                                    A2[wi][qq] = hmul2_bf16(A2[wi][qq], (qq & 1) ? s_hi[wi] : s_lo[wi]);
                             }
                         }
 #pragma unroll
                         for (int wi = 0; wi < 2; ++wi) {
-                            const int ks = 4 * fglob + 2 * half + wi;
+                            const int ks = 4 * fglob + word_of(wi);
                             const int s = ks % NS;
                             mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
                             if (valid) {
@@ -423,8 +458,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                     }
 #pragma unroll
                     for (int wi = 0; wi < 2; ++wi) {
-                        const int w = 2 * half + wi;
-                        const int ks = 4 * fglob + w;
+                        const int ks = 4 * fglob + word_of(wi);
                         const int s = ks % NS;
                         mbar_wait(op_empty(s), ((ks / NS) & 1) ^ 1);
                         if (valid) {
@@ -436,7 +470,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                             uint32_t A[16];
                             decode_word<R, false>(Sl, A);
 #pragma unroll
-                            for (int qq = 0; qq < 16; ++qq) A[qq] = hmul2_bf16(A[qq], (qq & 1) ? s_hi : s_lo);
+                            for (int qq = 0; qq < 16; ++qq) A[qq] = hmul2_bf16(A[qq], (qq & 1) ? s_hi[wi] : s_lo[wi]);
                             const uint32_t abase = a_st(s) + row_off;
 #pragma unroll
                             for (int k16 = 0; k16 < 4; ++k16) {

@@ -358,7 +358,8 @@ def _k4_weights(codes, scales, r, G=128):
 
 
 @pytest.mark.parametrize("n,k,B", [(128, 1024, 64), (200, 640, 100), (384, 2048, 300),
-                                   (136, 4096, 33), (1024, 5120, 129)])
+                                   (136, 4096, 33), (1024, 5120, 129), (256, 1024, 512),
+                                   (136, 1536, 600)])
 def test_gemm_vs_oracle(mq, n, k, B):
     """K4 against (a) an exact emulation of its bf16 weight rounding (only the
     fp32 accumulation order differs) and (b) the reference's dequantise-then-
@@ -417,7 +418,7 @@ def test_gemm_qwen_shapes_vs_fp32_torch(mq):
     for (n, k) in ((7168, 5120), (5120, 17408)):
         pt = mq.PlaneTensor.random_parent(n, k, seed=n)
         g = torch.Generator(device="cuda").manual_seed(2)
-        for B in (64, 256, 1024):
+        for B in (64, 256, 512, 1024):
             X = torch.randn(B, k, device="cuda", generator=g).to(torch.bfloat16)
             for r in (4, 8):
                 W = pt.decode(r)
@@ -429,6 +430,31 @@ def test_gemm_qwen_shapes_vs_fp32_torch(mq):
                 # max |y| over K = 17408 when one side splits K 8 ways)
                 half = pt.gemm(X[: B // 2].contiguous(), r, out_dtype=torch.float32)
                 assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 5e-5
+
+
+def test_gemm_512_token_tiles(mq):
+    """Past 256 tokens the planner may take 512-token tiles (one decoded weight tile feeds
+    two N = 256 MMAs into a 512-column TMEM accumulator, two operand stages, each decoder
+    warp owning one stage slot): Qwen3-14B o (5120 x 5120) at B = 384 / 512 / 600 picks
+    them for r <= 6 (r = 8 keeps 256).  Against fp32 torch on the exactly decoded weights,
+    deterministic, and batch rows independent of the tiling the half batch gets."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    if torch.cuda.get_device_properties(0).multi_processor_count != 148:
+        pytest.skip("the tiling choice assumes 148 SMs")
+    n = k = 5120
+    pt = mq.PlaneTensor.random_parent(n, k, seed=11)
+    g = torch.Generator(device="cuda").manual_seed(12)
+    for B in (384, 512, 600):
+        X = torch.randn(B, k, device="cuda", generator=g).to(torch.bfloat16)
+        for r in (2, 4, 6, 8):
+            want = X.float() @ pt.decode(r).T
+            got = pt.gemm(X, r, out_dtype=torch.float32)
+            assert rel_err(got.cpu().numpy(), want.cpu().numpy()) <= 5e-3, (B, r)
+            assert torch.equal(got, pt.gemm(X, r, out_dtype=torch.float32)), (B, r)
+            half = pt.gemm(X[: B // 2].contiguous(), r, out_dtype=torch.float32)
+            assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 5e-5, (B, r)
+            y16 = pt.gemm(X, r)
+            assert rel_err(y16.float().cpu().numpy(), want.cpu().numpy()) <= 1e-2, (B, r)
 
 
 def test_gemm_whole_waves_then_split_tail(mq):
