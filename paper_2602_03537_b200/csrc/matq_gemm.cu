@@ -132,7 +132,7 @@ GemmConfig choose_gemm_config(int N, int K, int B, int sms, int r) {
     const int bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
     GemmConfig c = plan_gemm(N, K, B, sms, bn, &cost);
     // past 256 tokens a 512-token tile decodes each weight tile once for two N = 256
-    // MMAs (r <= 6: the 8-plane raw ring does not fit beside 2 operand stages of 80 KB).
+    // MMAs (two operand stages of 80 KB; at r = 8 one raw stage beside them).
     // Its steps are MMA-bound at twice the 256-token step, and 2 operand stages plus a
     // single TMEM accumulator cost ~10% more (measured: 2.2 x); it wins where the
     // halved tile count fills the SMs better (Qwen3-14B o / down at B = 384-512)

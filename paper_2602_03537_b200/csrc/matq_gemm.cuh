@@ -84,7 +84,9 @@ struct GemmSmem {
     static constexpr uint32_t kOpBytes = kGemmABytes + kBBytes;
     static constexpr uint32_t kRawBytes = kRowTiles * gemm_raw_block_bytes(NPL);
     static constexpr uint32_t kFixed = 1024 + 512;  // alignment slack + barriers
-    static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget) ? 3 : 2;
+    static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget)   ? 3
+                            : (kFixed + 2 * kOpBytes + 2 * kRawBytes <= kSmemBudget) ? 2
+                                                                                       : 1;
     static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget)   ? 4
                             : (kFixed + 3 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 3
                                                                                        : 2;

@@ -73,7 +73,10 @@ struct GemmConfig {
 constexpr size_t kGemmTicketBytes = 64 * 1024;
 // r < 0: the workspace query, which does not know r (the larger of both tilings)
 GemmConfig choose_gemm_config(int N, int K, int B, int sms, int r);
-__host__ __device__ constexpr bool gemm_bn512_ok(int r) { return r >= 0 && r <= 6; }
+#ifndef MQ_GEMM_BN512_R8
+#define MQ_GEMM_BN512_R8 1
+#endif
+__host__ __device__ constexpr bool gemm_bn512_ok(int r) { return r >= 0 && (r <= 6 || MQ_GEMM_BN512_R8); }
 size_t gemm_ws_bytes(const GemmConfig& c);
 cudaError_t launch_gemm(const uint32_t* blob, const Layout& L, const void* X, int ldx, void* Y,
                         int ldy, int B, int r, bool child, float out_scale, bool y_f32,

@@ -436,7 +436,7 @@ def test_gemm_512_token_tiles(mq):
     """Past 256 tokens the planner may take 512-token tiles (one decoded weight tile feeds
     two N = 256 MMAs into a 512-column TMEM accumulator, two operand stages, each decoder
     warp owning one stage slot): Qwen3-14B o (5120 x 5120) at B = 384 / 512 / 600 picks
-    them for r <= 6 (r = 8 keeps 256).  Against fp32 torch on the exactly decoded weights,
+    them at every r (r = 8 with a single raw-weight stage).  Against fp32 torch on the exactly decoded weights,
     deterministic, and batch rows independent of the tiling the half batch gets."""
     torch.backends.cuda.matmul.allow_tf32 = False
     if torch.cuda.get_device_properties(0).multi_processor_count != 148:
