@@ -87,9 +87,17 @@ struct GemmSmem {
     static constexpr int RS = (kFixed + 3 * kOpBytes + 3 * kRawBytes <= kSmemBudget)   ? 3
                             : (kFixed + 2 * kOpBytes + 2 * kRawBytes <= kSmemBudget) ? 2
                                                                                        : 1;
-    static constexpr int NS = (kFixed + 4 * kOpBytes + RS * kRawBytes <= kSmemBudget)   ? 4
-                            : (kFixed + 3 * kOpBytes + RS * kRawBytes <= kSmemBudget) ? 3
-                                                                                       : 2;
+    // operand stages: as many as fit beside the raw ring, up to one step (4; 8 measured
+    // neutral at B = 64-256: the decoders are not waiting on the ring depth).
+    // NS >= 3 keeps a decoder from lapping another on a slot (its stages are at most
+    // 3 apart); NS = 2 (BN = 512) gives each decoder warp its own slot instead
+#ifndef MQ_GEMM_MAX_NS
+#define MQ_GEMM_MAX_NS 4
+#endif
+    static constexpr int fit_ns(int n) {
+        return (n <= 2 || kFixed + (uint32_t)n * kOpBytes + RS * kRawBytes <= kSmemBudget) ? n : fit_ns(n - 1);
+    }
+    static constexpr int NS = fit_ns(MQ_GEMM_MAX_NS);
     static constexpr uint32_t kRawOff = NS * kOpBytes;
     static constexpr uint32_t kBarOff = kRawOff + RS * kRawBytes;
     static constexpr uint32_t kBytes = kBarOff + kFixed;
