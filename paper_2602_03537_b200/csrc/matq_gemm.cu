@@ -136,14 +136,16 @@ GemmConfig choose_gemm_config(int N, int K, int B, int sms, int r) {
     // Its steps are MMA-bound at twice the 256-token step, and 2 operand stages plus a
     // single TMEM accumulator cost ~10% more (measured: 2.2 x); it wins where the
     // halved tile count fills the SMs better (Qwen3-14B o / down at B = 384-512)
-    static const bool bn512 = [] {
+    // MQ_GEMM_BN512: 0 = never, 2 = always past 256 tokens (tests: several 512-token
+    // units per CTA through the single TMEM accumulator), else the cost model
+    static const int bn512 = [] {
         const char* e = getenv("MQ_GEMM_BN512");
-        return !(e && e[0] == '0');
+        return e && (e[0] == '0' || e[0] == '2') ? e[0] - '0' : 1;
     }();
     if (B > 256 && bn512 && gemm_bn512_ok(r)) {
         double cost512 = 0.0;
         const GemmConfig c512 = plan_gemm(N, K, B, sms, 512, &cost512);
-        if (2.2 * cost512 < cost) c = c512;
+        if (bn512 == 2 || 2.2 * cost512 < cost) c = c512;
     }
     return c;
 }

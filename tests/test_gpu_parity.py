@@ -6,6 +6,8 @@ fp32 output, X generated in bf16 (exact in both paths) so the error
 measures only accumulation order and output rounding.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -455,6 +457,38 @@ def test_gemm_512_token_tiles(mq):
             assert rel_err(half.cpu().numpy(), got[: B // 2].cpu().numpy()) <= 5e-5, (B, r)
             y16 = pt.gemm(X, r)
             assert rel_err(y16.float().cpu().numpy(), want.cpu().numpy()) <= 1e-2, (B, r)
+
+
+_FORCED_512 = r"""
+import sys, torch
+sys.path.insert(0, %r)
+import paper_2602_03537_b200 as mq
+torch.backends.cuda.matmul.allow_tf32 = False
+n, k = 40960, 1024  # 320 row tiles: up to 3 units of 512 tokens per CTA
+pt = mq.PlaneTensor.random_parent(n, k, seed=3)
+g = torch.Generator(device="cuda").manual_seed(4)
+for B, r in ((512, 4), (700, 2), (1024, 8)):
+    X = torch.randn(B, k, device="cuda", generator=g).to(torch.bfloat16)
+    want = X.float() @ pt.decode(r).T
+    got = pt.gemm(X, r, out_dtype=torch.float32)
+    err = float((got - want).abs().max() / want.abs().max())
+    assert err <= 5e-3, (B, r, err)
+    assert torch.equal(got, pt.gemm(X, r, out_dtype=torch.float32)), (B, r)
+print("ok")
+"""
+
+
+def test_gemm_512_token_tiles_forced_multi_unit():
+    """MQ_GEMM_BN512=2 forces 512-token tiles past B = 256; on a 40960-row layer each CTA
+    runs several units in turn through the single-buffered 512-column TMEM accumulator
+    (the planner alone never picks that).  Subprocess: the knob is read once per process."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MQ_GEMM_BN512="2")
+    res = subprocess.run([sys.executable, "-c", _FORCED_512 % root], env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert res.returncode == 0 and res.stdout.strip().endswith("ok"), res.stderr[-2000:]
 
 
 def test_gemm_whole_waves_then_split_tail(mq):
