@@ -30,13 +30,11 @@ template <int R, bool CHILD, int BN>
 cudaError_t launch_bn(const CUtensorMap& map, const GemmParams& p, int grid, cudaStream_t stream,
                       bool pdl) {
     auto kern = k_gemm<R, CHILD, BN>;
-    static bool attr_set = false;
     constexpr int smem = (int)GemmSmem<BN, PlaneCount<R, CHILD>::value>::kBytes;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    // once per instantiation; a function-local static is initialised thread-safely
+    static const cudaError_t attr_err =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr_err != cudaSuccess) return attr_err;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kGemmThreads);

@@ -1,3 +1,4 @@
+#include <mutex>
 // Per-bit-width instantiation of the K3 launcher (included by matq_gemv_r*.cu
 // with MQ_R defined, so the five ladder widths compile in parallel).
 #include "matq_gemv.cuh"
@@ -7,11 +8,17 @@ namespace mq {
 template <typename K>
 static cudaError_t launch_one(K kernel, const GemvParams& p, dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, bool pdl, int& smem_set) {
-    if ((int)smem > smem_set) {
-        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        smem_set = (int)smem;
+    {
+        // the limit only grows; serialised so a smaller request cannot lower it under a
+        // concurrent larger one (host threads may launch concurrently)
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        if ((int)smem > smem_set) {
+            cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+            smem_set = (int)smem;
+        }
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
