@@ -655,7 +655,9 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
         const int pair_k = fpk ? atoi(fpk) : 4096, pair_n = fpn ? atoi(fpn) : 6144;
         {
             const int nst = mq::pad256(in.K) / 256;
-            if (pair && in.K <= pair_k && in.N <= pair_n && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
+            // (not at r = 8, B = 1: one chunk balances its 8-plane steps, 1.637 -> 1.618 ms;
+            // at B = 2 the pairs still win, 1.748 -> 1.735)
+            if (pair && !(ri == 8 && B == 1) && in.K <= pair_k && in.N <= pair_n && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
                 const int cs = mq::cdiv(nst, 2);
                 c = StackCfg{2, cs, std::min(sm_count() / 2, mq::pad16(in.N) / 16)};
             }
