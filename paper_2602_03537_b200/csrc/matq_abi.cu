@@ -657,10 +657,13 @@ static int stack_plan_impl(const mq_stack_layer* layers, int n_layers, int B, in
             const int nst = mq::pad256(in.K) / 256;
             // (not at r = 8, B = 1: one chunk balances its 8-plane steps, 1.637 -> 1.618 ms;
             // at B = 2 the pairs still win, 1.748 -> 1.735)
-            if (pair && !(ri == 8 && B == 1) && in.K <= pair_k && in.N <= pair_n && nst >= 2 && in.xop != MQ_XOP_ADD_RMSNORM) {
-                const int cs = mq::cdiv(nst, 2);
+            const int cs = mq::cdiv(nst, 2);
+            // only where the half-K chunk fits the staging budget (which accounts for the
+            // layer table: the 224 unfused C3 linears at B = 4 otherwise left no weight ring)
+            const bool fits = (size_t)nstage_max * B * (cs * 256 + 8) * 2 <= xs_budget;
+            if (pair && fits && !(ri == 8 && B == 1) && in.K <= pair_k && in.N <= pair_n && nst >= 2 &&
+                in.xop != MQ_XOP_ADD_RMSNORM)
                 c = StackCfg{2, cs, std::min(sm_count() / 2, mq::pad16(in.N) / 16)};
-            }
         }
         if (in.xop == MQ_XOP_ADD_RMSNORM && c.S != 1)
             return fail(MQ_ERR_INVALID, "layer %d: the fused prologue's row does not fit the staging area", i);

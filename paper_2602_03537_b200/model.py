@@ -180,7 +180,7 @@ class LinearStack:
         """Where the persistent K3S path is the default (single GPU, B <= 16,
         G = 128), from scripts/stack_matrix.py (profiles/r1_stack_matrix*.txt):
         * uniform r: see the table in the body (profiles/r2_dispatch_matrix.txt);
-        * heterogeneous (per-layer r, parents): at B <= 4, fused or unfused.
+        * heterogeneous (per-layer r, parents): at B <= 2, fused or unfused.
         stack_kernel=True / False forces either path."""
         rs = set(config.values()) if isinstance(config, dict) else {int(config)}
         parents = all(pt.nplanes == 8 for _, _, pt in self.layers)
@@ -190,9 +190,10 @@ class LinearStack:
             r0 = next(iter(rs))
             ok = self.B <= 8 or r0 != 8
         else:
-            # per-layer r (the dispatch kernel): 1.61 vs 1.96 ms fused, 1.99 vs 2.17 ms for the
-            # 224 unfused linears of C3 at B = 1 (scripts/stack_matrix.py)
-            ok = parents and self.B <= 4
+            # per-layer r (the dispatch kernel): 1.61 vs 1.96 ms fused, 2.02 vs 2.16 ms for the
+            # 224 unfused linears of C3 at B = 1, 2.15 vs 2.18 at B = 2; from B = 3 the graph
+            # wins (2.21 vs 2.94 ms; scripts/hetero_matrix.py, profiles/r2_hetero_matrix.txt)
+            ok = parents and self.B <= 2
         return ok and self.B <= 16 and self.G == 128  # tp > 1: one K3S launch per all-reduce segment
 
     def capture(self, config, pdl: bool = True, stack_kernel: bool | None = None, graph: bool = True) -> None:

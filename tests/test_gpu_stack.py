@@ -241,3 +241,25 @@ def test_stack_gated_output_epilogue(model, B, r):
     torch.cuda.synchronize()
     assert torch.isfinite(Y.float()).all()
     assert rel_err(Y.float().cpu().numpy(), y_ref.float().cpu().numpy()) <= 1e-2
+
+
+def test_c3_unfused_heterogeneous_plans_at_every_batch(model):
+    """The 224-linear C3 config (3.5-bit budget, unfused): the per-layer-r K3S plan fits at
+    B = 1, 4, 8 (the small-layer CTA-pair rule respects the staging budget, which counts the
+    224-entry layer table), agrees with the per-layer graph, and the default dispatch takes
+    K3S only at B <= 2 (measured, scripts/hetero_matrix.py)."""
+    from paper_2602_03537_b200.config import budget_config
+
+    cfg = budget_config(3.5, shape=model.LLAMA31_8B, seed=0, mutations=200).assignment
+    stack = model.LinearStack(model.LLAMA31_8B, batch=1, fused=False)
+    for B in (1, 4, 8):
+        stack.set_batch(B)
+        x0 = torch.randn(B, 4096, device="cuda").to(torch.bfloat16) * 0.5
+        stack.capture(cfg, stack_kernel=True)
+        assert stack.launches_per_step() == 1
+        y, _ = _step(stack, x0)
+        stack.capture(cfg, stack_kernel=False)
+        y_ref, _ = _step(stack, x0)
+        assert torch.isfinite(y.float()).all() and torch.isfinite(y_ref.float()).all()
+        assert rel_err(y.float().cpu().numpy(), y_ref.float().cpu().numpy()) <= 3e-2, B
+        assert stack.stack_kernel_ok(cfg) == (B <= 2)
