@@ -1,6 +1,7 @@
-"""C3 (3.5-bit heterogeneous config over the 224 unfused Llama-3.1-8B linears): per-layer-r
-K3S vs the per-layer K3 graph over decode batches -> LinearStack.stack_kernel_ok.
-    python scripts/hetero_matrix.py [batches]"""
+"""C3 (3.5-bit heterogeneous config over the 224 unfused Llama-3.1-8B linears, or a random
+ladder mix over the 128 fused ones): per-layer-r K3S vs the per-layer K3 graph over decode
+batches -> LinearStack.stack_kernel_ok.
+    python scripts/hetero_matrix.py [batches] [fused]"""
 import os
 import sys
 
@@ -24,8 +25,15 @@ def t_step(stack, n=10):
 
 
 batches = [int(b) for b in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8,16").split(",")]
-cfg = budget_config(3.5, shape=LLAMA31_8B, seed=0, mutations=200).assignment
-st = LinearStack(LLAMA31_8B, batch=1, fused=False)
+fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
+st = LinearStack(LLAMA31_8B, batch=1, fused=fused)
+if fused:  # the fused stack's 128 linears: a deterministic mix of the ladder
+    import numpy as np
+
+    rng = np.random.default_rng(0)
+    cfg = {n: int(rng.choice([2, 3, 4, 6, 8])) for n in st.names}
+else:
+    cfg = budget_config(3.5, shape=LLAMA31_8B, seed=0, mutations=200).assignment
 for B in batches:
     st.set_batch(B)
     row = {}
