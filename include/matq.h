@@ -125,7 +125,8 @@ MQ_API int mq_gemv(const uint32_t* blob, const float* tscales, const void* X, in
  * with mq_gemv: same ticket convention) must hold
  * mq_gemm_workspace_bytes(N, K, B, flags) bytes -- nonzero only when the
  * tiles cannot fill the GPU and K is split across CTAs (deterministic
- * in-order reduction).  Replaces the reference's blocked batch path nq_gemm
+ * in-order reduction).  It does not take r: past 256 tokens the tiling may
+ * depend on r (256- or 512-token tiles), so it returns the larger need.  Replaces the reference's blocked batch path nq_gemm
  * (packed_kernels.h:25-27) as driven by _core.pyx:53-63 for batch >= 8. */
 MQ_API size_t mq_gemm_workspace_bytes(int N, int K, int B, int flags);
 MQ_API int mq_gemm(const uint32_t* blob, const void* X, int ldx, void* Y, int ldy, int B, int N,
