@@ -809,6 +809,9 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     // per-layer r (r = 0) at B = 1: no pairs either (the 224-linear C3 stack 2.022 -> 1.978
     // ms, a fused ladder mix 1.604 -> 1.595; at B = 2 the pairs win, 2.895 -> 2.143)
     if (r == 0 && B == 1 && !(env && env[0] == '1')) pair = false;
+    // r = 8 at B = 1: none (stack 1.617 -> 1.612 ms; the decoder's per-block segments
+    // 436 -> 444 tok/s, scripts/full_pair_ab.sh)
+    if (r == 8 && B == 1 && !(env && env[0] == '1')) pair = false;
     int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
     if (st || !pair) return st;
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
