@@ -1,6 +1,6 @@
 # Full-model decode (bench.py full-model leg) under K3S planner knobs: default, no small-layer
 # pairs, no CTA pairs, 64 KB staging cap.  Run under gpurun: bash scripts/full_pair_ab.sh
-for cfg in "" "MQ_STACK_FORCE_PAIR_N=0" "MQ_STACK_PAIR=0" "MQ_STACK_XS_CAP_KB=64"; do
+for cfg in ${CFGS:-"" "MQ_STACK_FORCE_PAIR_N=0" "MQ_STACK_PAIR=0" "MQ_STACK_XS_CAP_KB=64"}; do
   env $cfg timeout 400 python bench.py --steps 20 --warmup 3 --no-sweep --no-cpu --no-hetero --no-prefill --no-quant --no-c1 --no-c2 > gpurun_out/fq.json 2>/dev/null
   python -c "
 import json
