@@ -331,6 +331,7 @@ class LlamaDecoder:
         captured alone in its own CUDA graph (same shapes and buffers), plus
         the whole step.  Under TP, "comm" is the all-reduces."""
         def time_graph(fn):
+            self.stream.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(self.stream):
                 fn()
             self.stream.synchronize()
@@ -393,6 +394,10 @@ class LlamaDecoder:
         torch.matmul(x, self.lm_head.t(), out=self.logits)
 
     def capture(self, graph: bool = True) -> None:
+        # the buffers (tokens, KV cache, ...) were initialised on the caller's stream: without
+        # this wait a fresh decoder could embed stale token ids (seen with a second decoder in
+        # one process: an index_select device assert)
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             self._forward()  # warm up the launch paths (workspaces, cuBLAS handles)
         self.stream.synchronize()
@@ -407,6 +412,7 @@ class LlamaDecoder:
     def step(self) -> None:
         if self.graph is None:
             self.capture()
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             if self.graph is False:
                 self._forward()

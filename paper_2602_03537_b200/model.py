@@ -244,6 +244,8 @@ class LinearStack:
             run = lambda: self.program.run(self.stream)  # noqa: E731
         else:
             run = lambda: self._run(self.config, pdl)  # noqa: E731
+        # buffers (and any activations the caller wrote) were produced on the caller's stream
+        self.stream.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(self.stream):
             run()  # warm the launch path outside capture
         self.stream.synchronize()
@@ -264,6 +266,7 @@ class LinearStack:
 
     def step(self) -> None:
         """Replay one captured decode step (device-resident activations)."""
+        self.stream.wait_stream(torch.cuda.current_stream())  # activations written by the caller
         with torch.cuda.stream(self.stream):
             if self.graph is None:
                 self._eager()

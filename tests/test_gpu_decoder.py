@@ -240,3 +240,18 @@ def test_attn_decode_rejects_bad_shapes(llama):
         with pytest.raises(Exception):
             _lib.call("mq_attn_decode", _lib.ptr(x), _lib.ptr(x), _lib.ptr(x), None, None, 1e-6, _lib.ptr(x),
                       _lib.ptr(x), _lib.ptr(m), _lib.ptr(x), 1, 2, 1, hd, T, pos, _lib.stream_ptr(None))
+
+
+def test_fresh_decoders_in_one_process(llama):
+    """Decoders built one after another in one process (the caching allocator hands the
+    second one the first one's memory): its buffers are initialised on the caller's
+    stream, so capture / step must wait for that stream (before the fix the second
+    decoder embedded stale token ids: an index_select device assert)."""
+    for B in (1, 2, 3, 2):
+        dec = llama.LlamaDecoder(batch=B, n_layers=2)
+        for _ in range(3):
+            dec.step()
+        torch.cuda.synchronize()
+        assert torch.isfinite(dec.logits.float()).all(), B
+        del dec
+        torch.cuda.empty_cache()
