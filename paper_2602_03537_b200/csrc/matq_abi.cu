@@ -812,6 +812,11 @@ int mq_stack_plan(const mq_stack_layer* layers, int n_layers, int B, int r, int 
     // r = 8 at B = 1: none (stack 1.617 -> 1.612 ms; the decoder's per-block segments
     // 436 -> 444 tok/s, scripts/full_pair_ab.sh)
     if (r == 8 && B == 1 && !(env && env[0] == '1')) pair = false;
+    // the decoder's block segments (fused prologues) at r = 2, B = 1: none (full decode
+    // 556 -> 562 tok/s; the bare stack at r = 2 keeps them, 1.180 vs 1.213 ms)
+    bool xops = false;
+    for (int i = 0; i < n_layers && layers; ++i) xops = xops || layers[i].xop != MQ_XOP_NONE || layers[i].yop != MQ_YOP_NONE;
+    if (xops && r == 2 && B == 1 && !(env && env[0] == '1')) pair = false;
     int st = stack_plan_impl(layers, n_layers, B, r, nplanes, plan_host, table_host, workspace_bytes, pair);
     if (st || !pair) return st;
     const StackPlanHost* P = reinterpret_cast<const StackPlanHost*>(plan_host);
